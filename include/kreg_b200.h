@@ -1,0 +1,270 @@
+/* kreg_b200.h — C-ABI of the B200-native CVO registration engine.
+ *
+ * Drop-in boundary for the reference's registration hot path
+ * (/root/reference/proj, a C++20 library `kreg`). The reference has no FFI;
+ * its boundary is the public C++ API. Every entry point below replaces one
+ * function of that API (cited per function) with plain pointers, sizes and
+ * status codes, so a ctypes / cgo / JNI binding can sit on it directly. The
+ * C++ façade in include/kreg_b200/kreg.hpp restores the reference's names,
+ * value types and exceptions on top of this ABI.
+ *
+ * Conventions
+ *  - Isometry = double[12], row-major 3x4 [R | t] (reference se3.hpp:27-34).
+ *  - Twist    = double[6], (omega, v) (reference se3.hpp:11-21).
+ *  - Clouds are uploaded once into device-resident SoA (kreg_cloud); the
+ *    reference's PointCloud is immutable after construction
+ *    (point_cloud.hpp:48-50), so the handle is too.
+ *  - A kreg_ctx is bound to one CUDA device and one stream. It is NOT
+ *    thread-safe: the caller serialises calls on one context. Different
+ *    contexts may be used concurrently from different host threads.
+ *  - Errors: every call returns a kreg_status; the message of the last error
+ *    on the calling thread is kreg_last_error(). The codes map back to the
+ *    reference's exceptions (errors.hpp:9-36; std::invalid_argument;
+ *    std::runtime_error).
+ */
+#ifndef KREG_B200_H_
+#define KREG_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KREG_B200_ABI_VERSION 1
+
+typedef enum {
+  KREG_OK = 0,
+  KREG_INVALID_ARGUMENT = 1, /* std::invalid_argument in the reference        */
+  KREG_NO_OVERLAP = 2,       /* kreg::NoOverlapError (errors.hpp:25-36)        */
+  KREG_CUDA_ERROR = 3,       /* device fault / launch failure                  */
+  KREG_OUT_OF_MEMORY = 4,    /* device allocation failed                       */
+  KREG_RUNTIME_ERROR = 5,    /* std::runtime_error                             */
+  KREG_NO_DEVICE = 6         /* no CUDA device: there is no CPU fallback       */
+} kreg_status;
+
+/* reference point_cloud.hpp:13 ChannelKind */
+typedef enum {
+  KREG_KIND_COLOR = 0,
+  KREG_KIND_INTENSITY = 1,
+  KREG_KIND_SEMANTIC = 2,
+  KREG_KIND_CUSTOM = 3
+} kreg_channel_kind;
+
+/* reference kernels.hpp:14 KernelForm */
+typedef enum { KREG_FORM_SQUARED_EXPONENTIAL = 0, KREG_FORM_LINEAR = 1 } kreg_kernel_form;
+
+/* reference point_cloud.hpp:17-23 Channel */
+typedef struct {
+  const char* name;
+  int32_t dim;
+  int32_t kind; /* kreg_channel_kind */
+} kreg_channel;
+
+/* Host view of reference PointCloud (point_cloud.hpp:51-76): positions n x 3
+ * row-major FP64, features n x dim row-major FP64 (dim = schema total_dim). */
+typedef struct {
+  const double* xyz;
+  int32_t n;
+  const double* features; /* may be NULL when dim == 0 */
+  int32_t dim;
+  const kreg_channel* channels; /* ordered schema; n_channels == 0 => geometric-only */
+  int32_t n_channels;
+} kreg_cloud_view;
+
+/* reference kernels.hpp:16-20 ChannelParams */
+typedef struct {
+  double sigma;
+  double lengthscale;
+  int32_t form; /* kreg_kernel_form */
+} kreg_channel_params;
+
+/* reference kernels.hpp:23-33 KernelParams */
+typedef struct {
+  double sigma;
+  double lengthscale;
+  const kreg_channel_params* per_channel;
+  int32_t n_channels;
+} kreg_kernel_params;
+
+/* reference registration.hpp:13-40 RegistrationConfig */
+typedef struct {
+  double init_lengthscale;
+  double subsequent_lengthscale;
+  double min_lengthscale;
+  double decay_factor;
+  int32_t stabilization_window;
+  double stabilization_rel_tol;
+  int32_t max_iterations;
+  double step_init;
+  double step_shrink;
+  double step_grow;
+  int32_t max_backtracks;
+  double convergence_twist_norm;
+  double cutoff_multiplier;
+  double c_min;
+} kreg_registration_config;
+
+/* reference registration.hpp:45-60 RegistrationResult. Trace arrays are
+ * caller-owned with room for `trace_capacity` entries each (any may be NULL);
+ * `iterations` is always the full count, traces are truncated to capacity. */
+typedef struct {
+  double transform[12];
+  int32_t converged;
+  int32_t iterations;
+  double final_indicator;
+  int32_t trace_capacity;
+  double* objective_trace;
+  double* indicator_trace;
+  double* lengthscale_trace;
+  double* step_trace;
+  double* twist_norm_trace;
+  int64_t* pair_count_trace;
+  uint8_t* rebuild_trace;
+  /* engine statistics (not in the reference): */
+  int32_t sweeps;   /* device evaluation passes issued for this registration */
+  int32_t rebuilds; /* device pair-list builds */
+} kreg_registration_result;
+
+/* reference registration.hpp:85-92 SequenceResult; arrays caller-owned,
+ * sized n_frames - 1 (relative, fallback, converged, final_indicator,
+ * iterations) and n_frames (trajectory). */
+typedef struct {
+  double* relative;   /* (n_frames-1) x 12 */
+  double* trajectory; /* n_frames x 12 */
+  uint8_t* fallback;
+  uint8_t* converged;
+  double* final_indicator;
+  int32_t* iterations;
+} kreg_sequence_result;
+
+typedef struct kreg_ctx kreg_ctx;
+typedef struct kreg_cloud kreg_cloud;
+typedef struct kreg_pairs kreg_pairs;
+
+/* ---------------------------------------------------------------- runtime */
+const char* kreg_last_error(void);
+int32_t kreg_abi_version(void);
+kreg_status kreg_ctx_create(int32_t device, kreg_ctx** out);
+kreg_status kreg_ctx_destroy(kreg_ctx* ctx);
+kreg_status kreg_ctx_synchronize(kreg_ctx* ctx);
+/* Number of device kernels this context has launched so far. */
+int64_t kreg_ctx_kernel_launches(const kreg_ctx* ctx);
+/* Accumulated device time (ms, CUDA events on the context stream) of the
+ * fused sweep kernel and its launch count, for roofline accounting. */
+kreg_status kreg_ctx_sweep_stats(const kreg_ctx* ctx, double* sweep_ms, int64_t* sweep_launches,
+                                 int64_t* pair_evals);
+kreg_status kreg_ctx_set_profiling(kreg_ctx* ctx, int32_t enabled);
+kreg_status kreg_ctx_reset_stats(kreg_ctx* ctx);
+
+/* Upload a cloud into device SoA (replaces constructing kreg::PointCloud,
+ * point_cloud.cpp:49-59; same validation and messages). */
+kreg_status kreg_cloud_create(kreg_ctx* ctx, const kreg_cloud_view* view, kreg_cloud** out);
+kreg_status kreg_cloud_destroy(kreg_cloud* cloud);
+int32_t kreg_cloud_size(const kreg_cloud* cloud);
+
+/* --------------------------------------------------- pair engine (L3) */
+/* reference inner_product.hpp:50-51 / inner_product.cpp:37-95 build_pairs. */
+kreg_status kreg_build_pairs(kreg_ctx* ctx, const kreg_cloud* X, const kreg_cloud* Z,
+                             const double T[12], const kreg_kernel_params* params,
+                             double cutoff_multiplier, double c_min, kreg_pairs** out,
+                             int64_t* n_pairs);
+kreg_status kreg_pairs_destroy(kreg_pairs* pairs);
+int64_t kreg_pairs_size(const kreg_pairs* pairs);
+/* Copy the pair list out in the reference's layout (inner_product.hpp:18-32):
+ * CSR grouped by source j (offsets[n_z+1]), target i ascending inside a group,
+ * coeff per entry. Debug / parity path. */
+kreg_status kreg_pairs_export(kreg_ctx* ctx, const kreg_pairs* pairs, int64_t* offsets,
+                              int32_t* x_index, double* coeff);
+/* reference inner_product.hpp:54-55 inner_product. */
+kreg_status kreg_inner_product(kreg_ctx* ctx, const kreg_pairs* pairs, const kreg_cloud* X,
+                               const kreg_cloud* Z, const double T[12],
+                               const kreg_kernel_params* params, double* value);
+/* reference inner_product.hpp:67-69 objective_and_gradient:
+ * out[0] = F, out[1..3] = grad.omega, out[4..6] = grad.v. */
+kreg_status kreg_objective_and_gradient(kreg_ctx* ctx, const kreg_pairs* pairs,
+                                        const kreg_cloud* X, const kreg_cloud* Z,
+                                        const double T[12], const kreg_kernel_params* params,
+                                        double out[7]);
+/* Batched candidate evaluation (the line-search candidates of
+ * registration.cpp:63-75 in one device pass): K transforms, out K x 8 =
+ * {F, omega[3], v[3], max displacement vs the pair list's build transform}. */
+#define KREG_EVAL_GRAD 1u
+#define KREG_EVAL_DISP 2u
+kreg_status kreg_eval_transforms(kreg_ctx* ctx, const kreg_pairs* pairs, const kreg_cloud* X,
+                                 const kreg_cloud* Z, const double* T, int32_t K,
+                                 const kreg_kernel_params* params, uint32_t flags, double* out);
+/* reference inner_product.hpp:71-75 evaluate_alignment. */
+kreg_status kreg_evaluate_alignment(kreg_ctx* ctx, const kreg_pairs* pairs, const kreg_cloud* X,
+                                    const kreg_cloud* Z, const double T[12],
+                                    const kreg_kernel_params* params, double* value_F,
+                                    double* indicator, int64_t* pair_count);
+/* reference inner_product.hpp:77-80 indicator (fresh pair list). */
+kreg_status kreg_indicator(kreg_ctx* ctx, const kreg_cloud* X, const kreg_cloud* Z,
+                           const double T[12], const kreg_kernel_params* params,
+                           double cutoff_multiplier, double c_min, double* value);
+/* reference inner_product.hpp:86 max_point_displacement. */
+kreg_status kreg_max_point_displacement(kreg_ctx* ctx, const kreg_cloud* Z, const double built[12],
+                                        const double now[12], double* value);
+
+/* ------------------------------------------------------- solver (L4) */
+/* reference registration.hpp:42 check_config. */
+kreg_status kreg_check_config(const kreg_registration_config* config);
+/* reference registration.hpp:13-40 defaults. */
+void kreg_registration_config_default(kreg_registration_config* config);
+/* reference registration.hpp:74-75 anneal_step. */
+kreg_status kreg_anneal_step(double lengthscale, const double* history, int32_t n_history,
+                             const kreg_registration_config* config, double* next);
+/* reference registration.hpp:82-84 line_search. */
+kreg_status kreg_line_search(kreg_ctx* ctx, const kreg_cloud* X, const kreg_cloud* Z,
+                             const double T[12], const double g[6],
+                             const kreg_kernel_params* params, const kreg_pairs* pairs,
+                             const kreg_registration_config* config, double* step);
+/* reference registration.hpp:66-68 register_clouds (X = target, Z = source). */
+kreg_status kreg_register_clouds(kreg_ctx* ctx, const kreg_cloud* X, const kreg_cloud* Z,
+                                 const double initial[12], const kreg_kernel_params* params,
+                                 const kreg_registration_config* config,
+                                 kreg_registration_result* result);
+/* Same, from host views: uploads X and Z, registers, frees (end-to-end call). */
+kreg_status kreg_register_clouds_host(kreg_ctx* ctx, const kreg_cloud_view* X,
+                                      const kreg_cloud_view* Z, const double initial[12],
+                                      const kreg_kernel_params* params,
+                                      const kreg_registration_config* config,
+                                      kreg_registration_result* result);
+/* Throughput mode: n independent registrations advanced in lockstep on one
+ * device (the reference runs these as an OpenMP loop over trials,
+ * eval.cpp:323). statuses[i] receives the per-registration status
+ * (KREG_NO_OVERLAP etc.); the call itself fails only on device errors. */
+kreg_status kreg_register_batch(kreg_ctx* ctx, int32_t n, const kreg_cloud* const* X,
+                                const kreg_cloud* const* Z, const double* initials,
+                                const kreg_kernel_params* params,
+                                const kreg_registration_config* config,
+                                kreg_registration_result* results, int32_t* statuses);
+/* reference registration.hpp:99-100 register_sequence. */
+kreg_status kreg_register_sequence(kreg_ctx* ctx, const kreg_cloud* const* frames,
+                                   int32_t n_frames, const kreg_kernel_params* params,
+                                   const kreg_registration_config* config,
+                                   kreg_sequence_result* result);
+/* Throughput form of register_sequence: frames split into `n_chains`
+ * contiguous chains (adjacent chains share one frame), chains registered
+ * concurrently in lockstep; chain c covers frames [begin_c, end_c]. The
+ * trajectory is composed across chains in order. */
+kreg_status kreg_register_sequence_chains(kreg_ctx* ctx, const kreg_cloud* const* frames,
+                                          int32_t n_frames, int32_t n_chains,
+                                          const kreg_kernel_params* params,
+                                          const kreg_registration_config* config,
+                                          kreg_sequence_result* result);
+
+/* ------------------------------------------------------- SE(3) host math */
+/* reference se3.cpp:48-76 exp, 109-120 compose, 122-127 inverse. */
+kreg_status kreg_se3_exp(const double xi[6], double out[12]);
+void kreg_se3_compose(const double a[12], const double b[12], double out[12]);
+void kreg_se3_inverse(const double T[12], double out[12]);
+double kreg_cloud_diameter(const kreg_cloud_view* view); /* point_cloud.cpp:69-87 */
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* KREG_B200_H_ */

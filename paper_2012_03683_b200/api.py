@@ -1,0 +1,384 @@
+"""Python mirror of the reference's public API on top of the B200 engine.
+
+Same names, argument order and meaning as /root/reference/proj/include/kreg/
+inner_product.hpp:50-87 and registration.hpp:42-100; errors map to the
+reference's exceptions (std::invalid_argument -> ValueError,
+kreg::NoOverlapError -> NoOverlapError). Everything here calls the C-ABI of
+libkreg_b200.so (include/kreg_b200.h); there is no CPU fallback — without the
+library or a CUDA device every call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import os
+import threading
+
+import numpy as np
+
+from . import _abi
+from .types import (Isometry, KernelParams, PointCloud, RegistrationConfig, RegistrationResult,
+                    SequenceBuffers, SequenceResult, raise_for)
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libkreg_b200.so")
+
+_lib = None
+_lib_lock = threading.Lock()
+
+P = C.c_void_p
+D = C.c_double
+VP = C.POINTER(_abi.kreg_cloud_view)
+KP = C.POINTER(_abi.kreg_kernel_params)
+CP = C.POINTER(_abi.kreg_registration_config)
+RP = C.POINTER(_abi.kreg_registration_result)
+
+
+def lib():
+    """Load libkreg_b200.so (fails loudly when it was not built)."""
+    global _lib
+    with _lib_lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2012_03683_b200.build` "
+                              "(the engine has no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        L.kreg_last_error.restype = C.c_char_p
+        L.kreg_abi_version.restype = C.c_int32
+        L.kreg_ctx_create.argtypes = [C.c_int32, C.POINTER(P)]
+        L.kreg_ctx_destroy.argtypes = [P]
+        L.kreg_ctx_synchronize.argtypes = [P]
+        L.kreg_ctx_kernel_launches.argtypes = [P]
+        L.kreg_ctx_kernel_launches.restype = C.c_int64
+        L.kreg_ctx_sweep_stats.argtypes = [P, _abi.dptr, _abi.i64ptr, _abi.i64ptr]
+        L.kreg_ctx_set_profiling.argtypes = [P, C.c_int32]
+        L.kreg_ctx_reset_stats.argtypes = [P]
+        L.kreg_cloud_create.argtypes = [P, VP, C.POINTER(P)]
+        L.kreg_cloud_destroy.argtypes = [P]
+        L.kreg_cloud_size.argtypes = [P]
+        L.kreg_build_pairs.argtypes = [P, P, P, _abi.dptr, KP, D, D, C.POINTER(P), _abi.i64ptr]
+        L.kreg_pairs_destroy.argtypes = [P]
+        L.kreg_pairs_size.argtypes = [P]
+        L.kreg_pairs_size.restype = C.c_int64
+        L.kreg_pairs_export.argtypes = [P, P, _abi.i64ptr, _abi.i32ptr, _abi.dptr]
+        L.kreg_inner_product.argtypes = [P, P, P, P, _abi.dptr, KP, _abi.dptr]
+        L.kreg_objective_and_gradient.argtypes = [P, P, P, P, _abi.dptr, KP, _abi.dptr]
+        L.kreg_eval_transforms.argtypes = [P, P, P, P, _abi.dptr, C.c_int32, KP, C.c_uint32, _abi.dptr]
+        L.kreg_evaluate_alignment.argtypes = [P, P, P, P, _abi.dptr, KP, _abi.dptr, _abi.dptr, _abi.i64ptr]
+        L.kreg_indicator.argtypes = [P, P, P, _abi.dptr, KP, D, D, _abi.dptr]
+        L.kreg_max_point_displacement.argtypes = [P, P, _abi.dptr, _abi.dptr, _abi.dptr]
+        L.kreg_check_config.argtypes = [CP]
+        L.kreg_registration_config_default.argtypes = [CP]
+        L.kreg_anneal_step.argtypes = [D, _abi.dptr, C.c_int32, CP, _abi.dptr]
+        L.kreg_line_search.argtypes = [P, P, P, _abi.dptr, _abi.dptr, KP, P, CP, _abi.dptr]
+        L.kreg_register_clouds.argtypes = [P, P, P, _abi.dptr, KP, CP, RP]
+        L.kreg_register_clouds_host.argtypes = [P, VP, VP, _abi.dptr, KP, CP, RP]
+        L.kreg_register_batch.argtypes = [P, C.c_int32, C.POINTER(P), C.POINTER(P), _abi.dptr, KP, CP, RP, _abi.i32ptr]
+        L.kreg_register_sequence.argtypes = [P, C.POINTER(P), C.c_int32, KP, CP, C.POINTER(_abi.kreg_sequence_result)]
+        L.kreg_register_sequence_chains.argtypes = [P, C.POINTER(P), C.c_int32, C.c_int32, KP, CP,
+                                                    C.POINTER(_abi.kreg_sequence_result)]
+        L.kreg_se3_exp.argtypes = [_abi.dptr, _abi.dptr]
+        L.kreg_se3_compose.argtypes = [_abi.dptr, _abi.dptr, _abi.dptr]
+        L.kreg_se3_inverse.argtypes = [_abi.dptr, _abi.dptr]
+        L.kreg_cloud_diameter.argtypes = [VP]
+        L.kreg_cloud_diameter.restype = D
+        _lib = L
+        return L
+
+
+def _check(rc: int):
+    if rc != 0:
+        raise_for(rc, lib().kreg_last_error().decode())
+
+
+def _t12(T):
+    a = T.as12() if isinstance(T, Isometry) else np.ascontiguousarray(np.asarray(T, dtype=np.float64).reshape(12))
+    return a, _abi.as_ptr(a)
+
+
+class Context:
+    """One CUDA device + stream (kreg_ctx). Not thread-safe."""
+
+    def __init__(self, device: int = 0):
+        h = P()
+        _check(lib().kreg_ctx_create(int(device), C.byref(h)))
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().kreg_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def synchronize(self):
+        _check(lib().kreg_ctx_synchronize(self.h))
+
+    def kernel_launches(self) -> int:
+        return int(lib().kreg_ctx_kernel_launches(self.h))
+
+    def set_profiling(self, on: bool):
+        _check(lib().kreg_ctx_set_profiling(self.h, int(on)))
+
+    def reset_stats(self):
+        _check(lib().kreg_ctx_reset_stats(self.h))
+
+    def sweep_stats(self):
+        ms = np.zeros(1)
+        n = np.zeros(2, dtype=np.int64)
+        _check(lib().kreg_ctx_sweep_stats(self.h, _abi.as_ptr(ms), _abi.as_ptr(n[:1], C.c_int64),
+                                          _abi.as_ptr(n[1:], C.c_int64)))
+        return {"sweep_ms": float(ms[0]), "sweep_rounds": int(n[0]), "pair_evals": int(n[1])}
+
+
+_default_ctx = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(int(os.environ.get("KREG_DEVICE", "0")))
+    return _default_ctx
+
+
+class DeviceCloud:
+    """Device-resident SoA copy of a PointCloud (kreg_cloud)."""
+
+    def __init__(self, cloud: PointCloud, ctx: Context | None = None):
+        self.ctx = ctx or default_context()
+        self.cloud = cloud
+        h = P()
+        _check(lib().kreg_cloud_create(self.ctx.h, cloud.view(), C.byref(h)))
+        self.h = h
+
+    def size(self):
+        return self.cloud.size()
+
+    def __del__(self):
+        try:
+            lib().kreg_cloud_destroy(self.h)
+        except Exception:
+            pass
+
+
+def device_cloud(c, ctx: Context | None = None) -> DeviceCloud:
+    """Upload once per (cloud, context); PointCloud is immutable."""
+    if isinstance(c, DeviceCloud):
+        return c
+    ctx = ctx or default_context()
+    cache = c.__dict__.setdefault("_device", {})
+    dc = cache.get(id(ctx))
+    if dc is None:
+        dc = DeviceCloud(c, ctx)
+        cache[id(ctx)] = dc
+    return dc
+
+
+class PairList:
+    """kreg::PairList (inner_product.hpp:18-32), device resident."""
+
+    def __init__(self, h, X: DeviceCloud, Z: DeviceCloud, n: int, params: KernelParams, T, cutoff_multiplier, c_min):
+        self.h, self.X, self.Z = h, X, Z
+        self.n = n
+        self.built_at_lengthscale = params.lengthscale
+        self.cutoff_radius = cutoff_multiplier * params.lengthscale
+        self.c_min = c_min
+        self.build_transform = T if isinstance(T, Isometry) else Isometry.from12(T)
+        self.n_x = X.size()
+        self.n_z = Z.size()
+
+    def size(self) -> int:
+        return self.n
+
+    def empty(self) -> bool:
+        return self.n == 0
+
+    def export(self):
+        """(offsets, x_index, coeff) in the reference layout."""
+        off = np.zeros(self.n_z + 1, dtype=np.int64)
+        idx = np.zeros(max(self.n, 1), dtype=np.int32)
+        cf = np.zeros(max(self.n, 1))
+        _check(lib().kreg_pairs_export(self.X.ctx.h, self.h, _abi.as_ptr(off, C.c_int64), _abi.as_ptr(idx, C.c_int32),
+                                       _abi.as_ptr(cf)))
+        return off, idx[: self.n], cf[: self.n]
+
+    def __del__(self):
+        try:
+            lib().kreg_pairs_destroy(self.h)
+        except Exception:
+            pass
+
+
+@dataclasses.dataclass
+class Evaluation:
+    value: float
+    grad: np.ndarray  # twist (omega[3], v[3])
+
+
+@dataclasses.dataclass
+class AlignmentReport:
+    value_F: float
+    indicator: float
+    pair_count: int
+
+
+def build_pairs(X, Z, T, params: KernelParams, cutoff_multiplier: float, c_min: float, ctx=None) -> PairList:
+    dx, dz = device_cloud(X, ctx), device_cloud(Z, ctx)
+    t, tp = _t12(T)
+    h = P()
+    n = C.c_int64()
+    _check(lib().kreg_build_pairs(dx.ctx.h, dx.h, dz.h, tp, params.cstruct(), cutoff_multiplier, c_min, C.byref(h),
+                                  C.byref(n)))
+    return PairList(h, dx, dz, n.value, params, T, cutoff_multiplier, c_min)
+
+
+def eval_transforms(pairs: PairList, X, Z, Ts, params: KernelParams) -> np.ndarray:
+    """K transforms in one device pass -> (K, 8): F, omega, v, displacement."""
+    dx, dz = device_cloud(X, pairs.X.ctx), device_cloud(Z, pairs.X.ctx)
+    Ts = [T.as12() if isinstance(T, Isometry) else np.asarray(T, dtype=np.float64).reshape(12) for T in Ts]
+    arr = np.ascontiguousarray(np.stack(Ts)) if Ts else np.zeros((0, 12))
+    out = np.zeros((len(Ts), 8))
+    _check(lib().kreg_eval_transforms(dx.ctx.h, pairs.h, dx.h, dz.h, _abi.as_ptr(arr), len(Ts), params.cstruct(),
+                                      _abi.KREG_EVAL_GRAD | _abi.KREG_EVAL_DISP, _abi.as_ptr(out)))
+    return out
+
+
+def inner_product(pairs: PairList, X, Z, T, params: KernelParams) -> float:
+    return float(eval_transforms(pairs, X, Z, [T], params)[0, 0])
+
+
+def objective_and_gradient(pairs: PairList, X, Z, T, params: KernelParams) -> Evaluation:
+    o = eval_transforms(pairs, X, Z, [T], params)[0]
+    return Evaluation(float(o[0]), o[1:7].copy())
+
+
+def gradient(pairs, X, Z, T, params) -> np.ndarray:
+    return objective_and_gradient(pairs, X, Z, T, params).grad
+
+
+def evaluate_alignment(pairs: PairList, X, Z, T, params: KernelParams) -> AlignmentReport:
+    F = inner_product(pairs, X, Z, T, params)
+    denom = np.sqrt(float(pairs.n_x) * float(pairs.n_z))
+    return AlignmentReport(F, F / denom if denom > 0 else 0.0, pairs.size())
+
+
+def indicator(X, Z, T, params: KernelParams, cutoff_multiplier: float = 3.0, c_min: float = 1e-4, ctx=None) -> float:
+    dx, dz = device_cloud(X, ctx), device_cloud(Z, ctx)
+    t, tp = _t12(T)
+    out = np.zeros(1)
+    _check(lib().kreg_indicator(dx.ctx.h, dx.h, dz.h, tp, params.cstruct(), cutoff_multiplier, c_min, _abi.as_ptr(out)))
+    return float(out[0])
+
+
+def max_point_displacement(Z, built, now, ctx=None) -> float:
+    dz = device_cloud(Z, ctx)
+    a, ap = _t12(built)
+    b, bp = _t12(now)
+    out = np.zeros(1)
+    _check(lib().kreg_max_point_displacement(dz.ctx.h, dz.h, ap, bp, _abi.as_ptr(out)))
+    return float(out[0])
+
+
+def check_config(config: RegistrationConfig):
+    _check(lib().kreg_check_config(C.byref(config.cstruct())))
+
+
+def anneal_step(lengthscale: float, history, config: RegistrationConfig) -> float:
+    h = np.ascontiguousarray(history, dtype=np.float64)
+    out = np.zeros(1)
+    _check(lib().kreg_anneal_step(lengthscale, _abi.as_ptr(h), len(h), C.byref(config.cstruct()), _abi.as_ptr(out)))
+    return float(out[0])
+
+
+def line_search(X, Z, T, g, params: KernelParams, pairs: PairList, config: RegistrationConfig) -> float:
+    dx, dz = device_cloud(X, pairs.X.ctx), device_cloud(Z, pairs.X.ctx)
+    t, tp = _t12(T)
+    gg = np.ascontiguousarray(g, dtype=np.float64)
+    out = np.zeros(1)
+    _check(lib().kreg_line_search(dx.ctx.h, dx.h, dz.h, tp, _abi.as_ptr(gg), params.cstruct(), pairs.h,
+                                  C.byref(config.cstruct()), _abi.as_ptr(out)))
+    return float(out[0])
+
+
+def register_clouds(X, Z, initial, params: KernelParams, config: RegistrationConfig, ctx=None,
+                    trace_capacity: int | None = None) -> RegistrationResult:
+    dx, dz = device_cloud(X, ctx), device_cloud(Z, ctx)
+    buf = _abi.TraceBuffers(trace_capacity or config.max_iterations)
+    t, tp = _t12(initial)
+    cfg = config.cstruct()
+    _check(lib().kreg_register_clouds(dx.ctx.h, dx.h, dz.h, tp, params.cstruct(), C.byref(cfg), C.byref(buf.struct)))
+    return RegistrationResult.from_buffers(buf)
+
+
+def register_clouds_host(X: PointCloud, Z: PointCloud, initial, params: KernelParams, config: RegistrationConfig,
+                         ctx=None, trace_capacity: int | None = None) -> RegistrationResult:
+    """End-to-end call: host clouds in, uploads inside the call."""
+    ctx = ctx or default_context()
+    buf = _abi.TraceBuffers(trace_capacity or config.max_iterations)
+    t, tp = _t12(initial)
+    cfg = config.cstruct()
+    _check(lib().kreg_register_clouds_host(ctx.h, X.view(), Z.view(), tp, params.cstruct(), C.byref(cfg),
+                                           C.byref(buf.struct)))
+    return RegistrationResult.from_buffers(buf)
+
+
+def register_batch(Xs, Zs, initials, params: KernelParams, config: RegistrationConfig, ctx=None,
+                   trace_capacity: int | None = None):
+    """Independent registrations in lockstep on one device.
+    Returns (results, statuses); results[k] is None when statuses[k] != 0."""
+    ctx = ctx or default_context()
+    n = len(Xs)
+    dxs = [device_cloud(x, ctx) for x in Xs]
+    dzs = [device_cloud(z, ctx) for z in Zs]
+    xh = (P * n)(*[d.h for d in dxs])
+    zh = (P * n)(*[d.h for d in dzs])
+    inits = np.ascontiguousarray(np.stack([T.as12() if isinstance(T, Isometry) else np.asarray(T, np.float64).reshape(12)
+                                           for T in initials])) if n else np.zeros((0, 12))
+    bufs = [_abi.TraceBuffers(trace_capacity or config.max_iterations) for _ in range(n)]
+    res = (_abi.kreg_registration_result * max(n, 1))(*[b.struct for b in bufs])
+    st = np.zeros(max(n, 1), dtype=np.int32)
+    cfg = config.cstruct()
+    _check(lib().kreg_register_batch(ctx.h, n, xh, zh, _abi.as_ptr(inits), params.cstruct(), C.byref(cfg), res,
+                                     _abi.as_ptr(st, C.c_int32)))
+    out = []
+    for k in range(n):
+        bufs[k].struct = res[k]
+        out.append(RegistrationResult.from_buffers(bufs[k]) if st[k] == 0 else None)
+    return out, st[:n].copy()
+
+
+def register_sequence(frames, params: KernelParams, config: RegistrationConfig, ctx=None,
+                      chains: int | None = None) -> SequenceResult:
+    ctx = ctx or default_context()
+    n = len(frames)
+    ds = [device_cloud(f, ctx) for f in frames]
+    fh = (P * max(n, 1))(*[d.h for d in ds])
+    sb = SequenceBuffers(max(n, 1))
+    cfg = config.cstruct()
+    if chains is None:
+        _check(lib().kreg_register_sequence(ctx.h, fh, n, params.cstruct(), C.byref(cfg), C.byref(sb.struct)))
+    else:
+        _check(lib().kreg_register_sequence_chains(ctx.h, fh, n, int(chains), params.cstruct(), C.byref(cfg),
+                                                   C.byref(sb.struct)))
+    return sb.result()
+
+
+def se3_exp(xi) -> Isometry:
+    xi = np.ascontiguousarray(xi, dtype=np.float64)
+    out = np.zeros(12)
+    _check(lib().kreg_se3_exp(_abi.as_ptr(xi), _abi.as_ptr(out)))
+    return Isometry.from12(out)
+
+
+def se3_compose(a, b) -> Isometry:
+    x, xp = _t12(a)
+    y, yp = _t12(b)
+    out = np.zeros(12)
+    lib().kreg_se3_compose(xp, yp, _abi.as_ptr(out))
+    return Isometry.from12(out)

@@ -1,0 +1,523 @@
+// C-ABI of the B200 CVO engine (include/kreg_b200.h). Every entry point maps
+// C++ exceptions to kreg_status + a thread-local message; there is no CPU
+// fallback: without a CUDA device every compute entry point fails with
+// KREG_NO_DEVICE / KREG_CUDA_ERROR.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <vector>
+
+#include "../../include/kreg_b200.h"
+#include "engine_host.hpp"
+#include "se3_host.hpp"
+#include "solver.hpp"
+
+using namespace kreg_host;
+
+namespace {
+
+template <typename Fn>
+kreg_status guarded(Fn&& fn) {
+  try {
+    fn();
+    return KREG_OK;
+  } catch (const Error& e) {
+    set_last_error(e.what());
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    set_last_error("host allocation failed");
+    return KREG_OUT_OF_MEMORY;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return KREG_RUNTIME_ERROR;
+  }
+}
+
+void require(bool ok, const char* what) {
+  if (!ok) throw Error(KREG_INVALID_ARGUMENT, what);
+}
+
+void check_build_args(const kreg_cloud* X, const kreg_cloud* Z, const Params& p, double cutoff_multiplier,
+                      double c_min) {
+  // inner_product.cpp:39-46
+  check_same_schema(X, Z, "");
+  check_kernel_params(p, X);
+  if (!(cutoff_multiplier >= 1.0)) throw Error(KREG_INVALID_ARGUMENT, "build_pairs: cutoff_multiplier must be >= 1");
+  if (c_min < 0.0 || c_min >= 1.0) throw Error(KREG_INVALID_ARGUMENT, "build_pairs: c_min must lie in [0, 1)");
+}
+
+// Evaluate K transforms (any K) against a built pair list; out K x 8.
+void eval_many(kreg_ctx* ctx, kreg_pairs* p, const double* T, int K, double lengthscale, double* out) {
+  std::vector<BuildJob> none;
+  std::vector<EvalJob> evals;
+  for (int b = 0; b < K; b += kreg_dev::kMaxCandidates) {
+    EvalJob e;
+    e.pairs = p;
+    e.M = std::min(kreg_dev::kMaxCandidates, K - b);
+    for (int m = 0; m < e.M; ++m) std::memcpy(e.T[m], T + 12 * (b + m), sizeof(double) * 12);
+    e.lengthscale = lengthscale;
+    e.out = out + static_cast<size_t>(b) * kreg_dev::kOut;
+    evals.push_back(e);
+  }
+  run_round(ctx, none, evals);
+}
+
+kreg_pairs* build(kreg_ctx* ctx, const kreg_cloud* X, const kreg_cloud* Z, const double* T, const Params& p,
+                  double cutoff_multiplier, double c_min) {
+  check_build_args(X, Z, p, cutoff_multiplier, c_min);
+  auto pr = std::make_unique<kreg_pairs>();
+  pr->ctx = ctx;
+  pr->X = X;
+  pr->Z = Z;
+  pr->built_at_lengthscale = p.lengthscale;
+  pr->cutoff_radius = cutoff_multiplier * p.lengthscale;
+  pr->c_min = c_min;
+  pr->sigma = p.sigma;
+  std::memcpy(pr->T_build, T, sizeof(double) * 12);
+  pr->P = 0;
+  if (X->n > 0 && Z->n > 0) {  // inner_product.cpp:55-56: empty clouds => empty list
+    std::vector<BuildJob> builds(1);
+    builds[0].pairs = pr.get();
+    builds[0].X = X;
+    builds[0].Z = Z;
+    std::memcpy(builds[0].T, T, sizeof(double) * 12);
+    builds[0].params = p;
+    builds[0].cutoff_multiplier = cutoff_multiplier;
+    builds[0].c_min = c_min;
+    std::vector<EvalJob> none;
+    run_round(ctx, builds, none);
+  }
+  return pr.release();
+}
+
+void check_pairs_match(const kreg_pairs* p, const kreg_cloud* X, const kreg_cloud* Z) {
+  require(p != nullptr, "pairs must not be NULL");
+  require(p->X == X && p->Z == Z, "pair list was built for different clouds");
+}
+
+void fill_sequence(const std::vector<double>& rel, const std::vector<uint8_t>& fb, const std::vector<uint8_t>& cv,
+                   const std::vector<double>& fi, const std::vector<int>& it, kreg_sequence_result* out) {
+  const size_t m = fb.size();
+  double traj[12];
+  kreg_se3::identity(traj);
+  std::memcpy(out->trajectory, traj, sizeof(traj));
+  for (size_t k = 0; k < m; ++k) {
+    std::memcpy(out->relative + 12 * k, rel.data() + 12 * k, sizeof(double) * 12);
+    out->fallback[k] = fb[k];
+    out->converged[k] = cv[k];
+    out->final_indicator[k] = fi[k];
+    out->iterations[k] = it[k];
+    double next[12];
+    kreg_se3::compose(traj, rel.data() + 12 * k, next);  // registration.cpp:226
+    std::memcpy(traj, next, sizeof(traj));
+    std::memcpy(out->trajectory + 12 * (k + 1), traj, sizeof(traj));
+  }
+}
+
+// Registers the chains [begin_c, end_c] of `frames` concurrently. Inside a
+// chain, pair k starts from the previous relative motion at the subsequent
+// lengthscale (registration.cpp:191-230); NoOverlapError => fallback.
+void run_chains(kreg_ctx* ctx, const kreg_cloud* const* frames, int n_frames, const std::vector<int>& begins,
+                const std::vector<int>& ends, const Params& params, const kreg_registration_config& config,
+                kreg_sequence_result* out) {
+  const int m = n_frames - 1;
+  std::vector<double> rel(static_cast<size_t>(m) * 12);
+  std::vector<uint8_t> fb(static_cast<size_t>(m)), cv(static_cast<size_t>(m));
+  std::vector<double> fi(static_cast<size_t>(m));
+  std::vector<int> it(static_cast<size_t>(m));
+  const int nc = static_cast<int>(begins.size());
+  std::vector<int> cursor(begins);           // frame index k-1 of the next pair
+  std::vector<std::vector<double>> prev(static_cast<size_t>(nc), std::vector<double>(12));
+  for (auto& p : prev) kreg_se3::identity(p.data());
+  std::vector<kreg_registration_result> results(static_cast<size_t>(nc));
+  std::vector<long long> hint(static_cast<size_t>(nc), 0);
+  for (;;) {
+    std::vector<RegJob> jobs;
+    std::vector<int> chain_of;
+    for (int c = 0; c < nc; ++c) {
+      if (cursor[c] >= ends[c]) continue;
+      const int k = cursor[c] + 1;  // pair (k-1, k)
+      RegJob j;
+      j.X = frames[k - 1];
+      j.Z = frames[k];
+      std::memcpy(j.initial, prev[c].data(), sizeof(j.initial));
+      j.params = params;
+      j.cfg = config;
+      if (k - begins[c] > 1) j.cfg.init_lengthscale = config.subsequent_lengthscale;
+      j.cfg.min_lengthscale = std::min(j.cfg.min_lengthscale, j.cfg.init_lengthscale);
+      std::memset(&results[c], 0, sizeof(kreg_registration_result));
+      j.out = &results[c];
+      j.expected_pairs = hint[c];
+      jobs.push_back(j);
+      chain_of.push_back(c);
+    }
+    if (jobs.empty()) break;
+    register_many(ctx, jobs);
+    for (size_t q = 0; q < jobs.size(); ++q) {
+      const int c = chain_of[q];
+      const int k = cursor[c] + 1;
+      const int slot = k - 1;
+      const RegJob& j = jobs[q];
+      if (j.status == KREG_OK) {
+        std::memcpy(rel.data() + 12 * slot, results[c].transform, sizeof(double) * 12);
+        fb[slot] = 0;
+        cv[slot] = results[c].converged ? 1 : 0;
+        fi[slot] = results[c].final_indicator;
+        it[slot] = results[c].iterations;
+      } else if (j.status == KREG_NO_OVERLAP) {
+        std::memcpy(rel.data() + 12 * slot, prev[c].data(), sizeof(double) * 12);
+        fb[slot] = 1;
+        cv[slot] = 0;
+        fi[slot] = 0.0;
+        it[slot] = 0;
+      } else {
+        throw Error(j.status, j.error);
+      }
+      std::memcpy(prev[c].data(), rel.data() + 12 * slot, sizeof(double) * 12);
+      cursor[c] = k;
+    }
+  }
+  fill_sequence(rel, fb, cv, fi, it, out);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* kreg_last_error(void) { return last_error(); }
+int32_t kreg_abi_version(void) { return KREG_B200_ABI_VERSION; }
+
+kreg_status kreg_ctx_create(int32_t device, kreg_ctx** out) {
+  return guarded([&] {
+    require(out != nullptr, "out must not be NULL");
+    int n = 0;
+    const cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0) {
+      cudaGetLastError();
+      throw Error(KREG_NO_DEVICE, "no CUDA device available (the engine has no CPU fallback)");
+    }
+    require(device >= 0 && device < n, "device index out of range");
+    auto ctx = std::make_unique<kreg_ctx>();
+    ctx->device = device;
+    KREG_CUDA(cudaSetDevice(device));
+    KREG_CUDA(cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device));
+    KREG_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    KREG_CUDA(cudaEventCreate(&ctx->ev_sweep0));
+    KREG_CUDA(cudaEventCreate(&ctx->ev_sweep1));
+    ctx->launches_base = kreg_dev::kernel_launch_count();
+    *out = ctx.release();
+  });
+}
+
+kreg_status kreg_ctx_destroy(kreg_ctx* ctx) {
+  return guarded([&] {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    ctx->d_build.release();
+    ctx->d_sweep.release();
+    ctx->d_results.release();
+    ctx->d_T2.release();
+    ctx->d_disp.release();
+    cudaEventDestroy(ctx->ev_sweep0);
+    cudaEventDestroy(ctx->ev_sweep1);
+    cudaStreamDestroy(ctx->stream);
+    delete ctx;
+  });
+}
+
+kreg_status kreg_ctx_synchronize(kreg_ctx* ctx) {
+  return guarded([&] { KREG_CUDA(cudaStreamSynchronize(ctx->stream)); });
+}
+
+int64_t kreg_ctx_kernel_launches(const kreg_ctx* ctx) { return kreg_dev::kernel_launch_count() - ctx->launches_base; }
+
+kreg_status kreg_ctx_sweep_stats(const kreg_ctx* ctx, double* sweep_ms, int64_t* sweep_launches, int64_t* pair_evals) {
+  return guarded([&] {
+    if (sweep_ms) *sweep_ms = ctx->sweep_ms;
+    if (sweep_launches) *sweep_launches = ctx->sweep_launches;
+    if (pair_evals) *pair_evals = ctx->pair_evals;
+  });
+}
+
+kreg_status kreg_ctx_set_profiling(kreg_ctx* ctx, int32_t enabled) {
+  return guarded([&] { ctx->profiling = enabled != 0; });
+}
+
+kreg_status kreg_ctx_reset_stats(kreg_ctx* ctx) {
+  return guarded([&] {
+    ctx->sweep_ms = 0.0;
+    ctx->sweep_launches = 0;
+    ctx->pair_evals = 0;
+    ctx->launches_base = kreg_dev::kernel_launch_count();
+  });
+}
+
+kreg_status kreg_cloud_create(kreg_ctx* ctx, const kreg_cloud_view* view, kreg_cloud** out) {
+  return guarded([&] {
+    require(ctx && view && out, "NULL argument");
+    *out = cloud_create(ctx, view);
+  });
+}
+
+kreg_status kreg_cloud_destroy(kreg_cloud* cloud) {
+  return guarded([&] { delete cloud; });
+}
+
+int32_t kreg_cloud_size(const kreg_cloud* cloud) { return cloud ? cloud->n : 0; }
+
+kreg_status kreg_build_pairs(kreg_ctx* ctx, const kreg_cloud* X, const kreg_cloud* Z, const double T[12],
+                             const kreg_kernel_params* params, double cutoff_multiplier, double c_min,
+                             kreg_pairs** out, int64_t* n_pairs) {
+  return guarded([&] {
+    require(ctx && X && Z && T && params && out, "NULL argument");
+    kreg_pairs* p = build(ctx, X, Z, T, to_params(params), cutoff_multiplier, c_min);
+    *out = p;
+    if (n_pairs) *n_pairs = p->P;
+  });
+}
+
+kreg_status kreg_pairs_destroy(kreg_pairs* pairs) {
+  return guarded([&] { delete pairs; });
+}
+
+int64_t kreg_pairs_size(const kreg_pairs* pairs) { return pairs ? pairs->P : 0; }
+
+kreg_status kreg_pairs_export(kreg_ctx* ctx, const kreg_pairs* pairs, int64_t* offsets, int32_t* x_index,
+                              double* coeff) {
+  return guarded([&] {
+    require(ctx && pairs && offsets, "NULL argument");
+    if (!pairs->Z || pairs->Z->n == 0 || pairs->P == 0) {
+      const int nz = pairs->Z ? pairs->Z->n : 0;
+      for (int j = 0; j <= nz; ++j) offsets[j] = 0;
+      return;
+    }
+    pairs_export(ctx, pairs, offsets, x_index, coeff);
+  });
+}
+
+kreg_status kreg_eval_transforms(kreg_ctx* ctx, const kreg_pairs* pairs, const kreg_cloud* X, const kreg_cloud* Z,
+                                 const double* T, int32_t K, const kreg_kernel_params* params, uint32_t flags,
+                                 double* out) {
+  (void)flags;  // gradient and displacement are always produced by the fused sweep
+  return guarded([&] {
+    require(ctx && pairs && T && params && out && K >= 0, "invalid argument");
+    check_pairs_match(pairs, X, Z);
+    if (K == 0) return;
+    if (pairs->P == 0) {
+      // inner_product.cpp:98 / :124: empty list => zeros (displacement still defined)
+      for (int k = 0; k < K; ++k) {
+        std::memset(out + 8 * k, 0, sizeof(double) * 8);
+        out[8 * k + 7] = max_point_displacement_dev(ctx, Z, pairs->T_build, T + 12 * k);
+      }
+      return;
+    }
+    eval_many(ctx, const_cast<kreg_pairs*>(pairs), T, K, params->lengthscale, out);
+  });
+}
+
+kreg_status kreg_inner_product(kreg_ctx* ctx, const kreg_pairs* pairs, const kreg_cloud* X, const kreg_cloud* Z,
+                               const double T[12], const kreg_kernel_params* params, double* value) {
+  double o[8];
+  const kreg_status s = kreg_eval_transforms(ctx, pairs, X, Z, T, 1, params, 0, o);
+  if (s == KREG_OK) *value = o[0];
+  return s;
+}
+
+kreg_status kreg_objective_and_gradient(kreg_ctx* ctx, const kreg_pairs* pairs, const kreg_cloud* X,
+                                        const kreg_cloud* Z, const double T[12], const kreg_kernel_params* params,
+                                        double out[7]) {
+  double o[8];
+  const kreg_status s = kreg_eval_transforms(ctx, pairs, X, Z, T, 1, params, KREG_EVAL_GRAD, o);
+  if (s == KREG_OK) std::memcpy(out, o, sizeof(double) * 7);
+  return s;
+}
+
+kreg_status kreg_evaluate_alignment(kreg_ctx* ctx, const kreg_pairs* pairs, const kreg_cloud* X, const kreg_cloud* Z,
+                                    const double T[12], const kreg_kernel_params* params, double* value_F,
+                                    double* indicator, int64_t* pair_count) {
+  double o[8];
+  const kreg_status s = kreg_eval_transforms(ctx, pairs, X, Z, T, 1, params, 0, o);
+  if (s != KREG_OK) return s;
+  // inner_product.cpp:159-168
+  const double denom = std::sqrt(static_cast<double>(X->n) * static_cast<double>(Z->n));
+  if (value_F) *value_F = o[0];
+  if (indicator) *indicator = denom > 0.0 ? o[0] / denom : 0.0;
+  if (pair_count) *pair_count = pairs->P;
+  return KREG_OK;
+}
+
+kreg_status kreg_indicator(kreg_ctx* ctx, const kreg_cloud* X, const kreg_cloud* Z, const double T[12],
+                           const kreg_kernel_params* params, double cutoff_multiplier, double c_min, double* value) {
+  return guarded([&] {
+    require(ctx && X && Z && T && params && value, "NULL argument");
+    // inner_product.cpp:170-177
+    if (X->n == 0 || Z->n == 0) throw Error(KREG_INVALID_ARGUMENT, "indicator: clouds must be non-empty");
+    std::unique_ptr<kreg_pairs> p(build(ctx, X, Z, T, to_params(params), cutoff_multiplier, c_min));
+    double o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (p->P > 0) eval_many(ctx, p.get(), T, 1, params->lengthscale, o);
+    const double denom = std::sqrt(static_cast<double>(X->n) * static_cast<double>(Z->n));
+    *value = denom > 0.0 ? o[0] / denom : 0.0;
+  });
+}
+
+kreg_status kreg_max_point_displacement(kreg_ctx* ctx, const kreg_cloud* Z, const double built[12],
+                                        const double now[12], double* value) {
+  return guarded([&] {
+    require(ctx && Z && built && now && value, "NULL argument");
+    *value = max_point_displacement_dev(ctx, Z, built, now);
+  });
+}
+
+kreg_status kreg_check_config(const kreg_registration_config* config) {
+  return guarded([&] { check_config(*config); });
+}
+
+void kreg_registration_config_default(kreg_registration_config* c) {
+  // registration.hpp:18-39
+  c->init_lengthscale = 0.95;
+  c->subsequent_lengthscale = 0.1;
+  c->min_lengthscale = 0.0475;
+  c->decay_factor = 0.98;
+  c->stabilization_window = 5;
+  c->stabilization_rel_tol = 1e-5;
+  c->max_iterations = 2000;
+  c->step_init = 0.1;
+  c->step_shrink = 0.5;
+  c->step_grow = 1.2;
+  c->max_backtracks = 20;
+  c->convergence_twist_norm = 1e-5;
+  c->cutoff_multiplier = 3.0;
+  c->c_min = 1e-4;
+}
+
+kreg_status kreg_anneal_step(double lengthscale, const double* history, int32_t n_history,
+                             const kreg_registration_config* config, double* next) {
+  return guarded([&] { *next = anneal_step(lengthscale, history, n_history, *config); });
+}
+
+kreg_status kreg_line_search(kreg_ctx* ctx, const kreg_cloud* X, const kreg_cloud* Z, const double T[12],
+                             const double g[6], const kreg_kernel_params* params, const kreg_pairs* pairs,
+                             const kreg_registration_config* config, double* step) {
+  return guarded([&] {
+    require(ctx && X && Z && T && g && params && pairs && config && step, "NULL argument");
+    check_pairs_match(pairs, X, Z);
+    // registration.cpp:86-98
+    const double gnorm = kreg_se3::twist_norm6(g);
+    if (!(gnorm > 0.0)) throw Error(KREG_INVALID_ARGUMENT, "line_search: gradient norm must be > 0");
+    const int K = config->max_backtracks + 1;
+    std::vector<double> Ts(static_cast<size_t>(K + 1) * 12), out(static_cast<size_t>(K + 1) * 8, 0.0);
+    std::memcpy(Ts.data(), T, sizeof(double) * 12);
+    std::vector<double> eps(static_cast<size_t>(K));
+    double e = config->step_init * params->lengthscale;
+    const double s = 1.0 / gnorm;
+    for (int k = 0; k < K; ++k) {
+      double tw[6], E[12];
+      for (int t = 0; t < 6; ++t) tw[t] = (g[t] * s) * e;
+      if (!kreg_se3::exp(tw, E)) throw Error(KREG_INVALID_ARGUMENT, "exp: twist has non-finite components");
+      kreg_se3::compose(E, T, Ts.data() + 12 * (k + 1));
+      eps[static_cast<size_t>(k)] = e;
+      e *= config->step_shrink;
+    }
+    if (pairs->P > 0) eval_many(ctx, const_cast<kreg_pairs*>(pairs), Ts.data(), K + 1, params->lengthscale, out.data());
+    *step = 0.0;
+    for (int k = 0; k < K; ++k)
+      if (out[8 * (k + 1)] > out[0]) {
+        *step = eps[static_cast<size_t>(k)];
+        break;
+      }
+  });
+}
+
+static void make_jobs(const kreg_cloud* X, const kreg_cloud* Z, const double* initial, const kreg_kernel_params* params,
+                      const kreg_registration_config* config, kreg_registration_result* result, RegJob& j) {
+  require(X && Z && initial && params && config && result, "NULL argument");
+  j.X = X;
+  j.Z = Z;
+  std::memcpy(j.initial, initial, sizeof(j.initial));
+  j.params = to_params(params);
+  j.cfg = *config;
+  j.out = result;
+}
+
+kreg_status kreg_register_clouds(kreg_ctx* ctx, const kreg_cloud* X, const kreg_cloud* Z, const double initial[12],
+                                 const kreg_kernel_params* params, const kreg_registration_config* config,
+                                 kreg_registration_result* result) {
+  return guarded([&] {
+    require(ctx != nullptr, "NULL context");
+    std::vector<RegJob> jobs(1);
+    make_jobs(X, Z, initial, params, config, result, jobs[0]);
+    register_many(ctx, jobs);
+    if (jobs[0].status != KREG_OK) throw Error(jobs[0].status, jobs[0].error);
+  });
+}
+
+kreg_status kreg_register_clouds_host(kreg_ctx* ctx, const kreg_cloud_view* X, const kreg_cloud_view* Z,
+                                      const double initial[12], const kreg_kernel_params* params,
+                                      const kreg_registration_config* config, kreg_registration_result* result) {
+  return guarded([&] {
+    require(ctx && X && Z, "NULL argument");
+    std::unique_ptr<kreg_cloud> cx(cloud_create(ctx, X));
+    std::unique_ptr<kreg_cloud> cz(cloud_create(ctx, Z));
+    std::vector<RegJob> jobs(1);
+    make_jobs(cx.get(), cz.get(), initial, params, config, result, jobs[0]);
+    register_many(ctx, jobs);
+    if (jobs[0].status != KREG_OK) throw Error(jobs[0].status, jobs[0].error);
+  });
+}
+
+kreg_status kreg_register_batch(kreg_ctx* ctx, int32_t n, const kreg_cloud* const* X, const kreg_cloud* const* Z,
+                                const double* initials, const kreg_kernel_params* params,
+                                const kreg_registration_config* config, kreg_registration_result* results,
+                                int32_t* statuses) {
+  return guarded([&] {
+    require(ctx && (n == 0 || (X && Z && initials && results && statuses)), "NULL argument");
+    std::vector<RegJob> jobs(static_cast<size_t>(n));
+    for (int k = 0; k < n; ++k) make_jobs(X[k], Z[k], initials + 12 * k, params, config, &results[k], jobs[k]);
+    register_many(ctx, jobs);
+    for (int k = 0; k < n; ++k) statuses[k] = jobs[k].status;
+  });
+}
+
+kreg_status kreg_register_sequence(kreg_ctx* ctx, const kreg_cloud* const* frames, int32_t n_frames,
+                                   const kreg_kernel_params* params, const kreg_registration_config* config,
+                                   kreg_sequence_result* result) {
+  return guarded([&] {
+    // registration.cpp:191-230
+    if (n_frames < 2) throw Error(KREG_INVALID_ARGUMENT, "register_sequence: need at least 2 frames");
+    require(ctx && frames && params && config && result, "NULL argument");
+    run_chains(ctx, frames, n_frames, {0}, {n_frames - 1}, to_params(params), *config, result);
+  });
+}
+
+kreg_status kreg_register_sequence_chains(kreg_ctx* ctx, const kreg_cloud* const* frames, int32_t n_frames,
+                                          int32_t n_chains, const kreg_kernel_params* params,
+                                          const kreg_registration_config* config, kreg_sequence_result* result) {
+  return guarded([&] {
+    if (n_frames < 2) throw Error(KREG_INVALID_ARGUMENT, "register_sequence: need at least 2 frames");
+    require(ctx && frames && params && config && result && n_chains >= 1, "invalid argument");
+    const int m = n_frames - 1;
+    const int nc = std::min(n_chains, m);
+    std::vector<int> b, e;
+    for (int c = 0; c < nc; ++c) {
+      b.push_back(static_cast<int>(static_cast<long long>(m) * c / nc));
+      e.push_back(static_cast<int>(static_cast<long long>(m) * (c + 1) / nc));
+    }
+    run_chains(ctx, frames, n_frames, b, e, to_params(params), *config, result);
+  });
+}
+
+kreg_status kreg_se3_exp(const double xi[6], double out[12]) {
+  return guarded([&] {
+    if (!kreg_se3::exp(xi, out)) throw Error(KREG_INVALID_ARGUMENT, "exp: twist has non-finite components");
+  });
+}
+
+void kreg_se3_compose(const double a[12], const double b[12], double out[12]) { kreg_se3::compose(a, b, out); }
+void kreg_se3_inverse(const double T[12], double out[12]) { kreg_se3::inverse(T, out); }
+double kreg_cloud_diameter(const kreg_cloud_view* view) { return diameter_host(view->xyz, view->n); }
+
+}  // extern "C"

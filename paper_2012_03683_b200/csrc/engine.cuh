@@ -1,0 +1,113 @@
+// Device-side data layout and kernel entry points of the B200 CVO engine.
+//
+// Layout in HBM (one registration "slot"; see DESIGN.md §Data layout):
+//   Cloud (uploaded once, spatially sorted by a 63-bit Morton key so that
+//   index locality == spatial locality):
+//     x/y/z        FP64 SoA positions            (build test, q = T z)
+//     feat         FP32 rows, stride fstride=4k  (c_ij in the pair build)
+//   Grid (per lengthscale level, over target X): dense cell index over the
+//     bbox of X, cell = cutoff*(1+1e-7) so the 27-cell stencil is a superset
+//     of the FP64 cutoff ball; counting sort with a deterministic order
+//     inside a cell (ascending point index) -> cell_start[] / cell_items[]
+//     plus cell-ordered FP64 copies cx/cy/cz for coalesced candidate tests.
+//   Pair list (per build): CSR by source j: offsets int64[n_z+1];
+//     pairs int2 {i, float_as_int(log2 c)} = 8 B/pair; chunk_j[] = owning j
+//     of every E-pair chunk (flattened, load-balanced sweep); xq int4[n_x]
+//     = X in fixed point (2^-k m units around the X bbox centre).
+//   Sweep scratch: q int4[M][n_z] (magic - fixed-point T z) per candidate;
+//     per-virtual-block FP64 partials; per-request completion counters.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace kreg_dev {
+
+constexpr int kPairsPerChunk = 8;   // E: pairs per thread chunk in the sweep
+constexpr int kSweepThreads = 256;  // threads per (virtual) sweep block
+constexpr int kPairsPerVBlock = kPairsPerChunk * kSweepThreads;
+constexpr int kMaxChannels = 8;
+constexpr int kMaxCandidates = 8;   // candidate transforms per sweep request
+constexpr int kOut = 8;             // {F, omega[3], v[3], max displacement}
+constexpr int kScanTile = 2048;     // elements per scan tile
+constexpr unsigned kMagic = 0x4B400000u;  // bits of 1.5 * 2^23
+
+struct ChannelDev {
+  int offset;     // float offset inside the feature row
+  int dim;
+  int linear;     // 1 = linear form (dot), 0 = squared exponential
+  float kappa;    // SE: -log2(e) / (2 l_c^2)
+  float sigma2;   // SE amplitude sigma_c^2 (linear ignores sigma, kernels.cpp:37-42)
+};
+
+struct CoeffParams {
+  int n_channels;  // 0 => geometric-only (c == 1)
+  int fstride;
+  float c_min;
+  ChannelDev ch[kMaxChannels];
+};
+
+// One pair-list build (K1 grid + K2 pairs) for one registration.
+struct BuildReq {
+  const double* xx; const double* xy; const double* xz; const float* xfeat; int n_x;
+  const double* zx; const double* zy; const double* zz; const float* zfeat; int n_z;
+  double T[12];          // build transform, row-major 3x4
+  double origin[3];      // grid origin (componentwise min of X)
+  double inv_h;          // 1 / cell size
+  int gx, gy, gz;        // grid dims
+  long long n_cells;
+  double cutoff_sq;
+  int* cell_count;       // n_cells (all zero between builds)
+  int* cell_start;       // n_cells + 1
+  int* cell_of;          // n_x
+  int* tmp_items;        // n_x
+  int* cell_items;       // n_x
+  double* cx; double* cy; double* cz;  // n_x cell-ordered positions
+  int* count;            // n_z
+  long long* offsets;    // n_z + 1
+  int2* pairs;           // capacity
+  long long capacity;
+  int* chunk_j;          // capacity / E + 1
+  double* status;        // {P, P > capacity} written by the count scan
+  int4* xq;              // n_x fixed-point X
+  double anchor[3];
+  double qscale;         // 2^k
+  long long* scan_tiles; // scan workspace (tile sums)
+  CoeffParams cp;
+};
+
+// One sweep request: M candidate transforms against one pair list.
+struct SweepReq {
+  const long long* offsets;
+  const int2* pairs;
+  long long capacity;    // pairs capacity (an overflowed build is skipped)
+  const int* chunk_j;
+  const int4* xq;
+  const double* zx; const double* zy; const double* zz;  // source, sorted
+  int4* q;               // M x n_z scratch
+  int n_z;
+  int M;
+  double T[kMaxCandidates][12];
+  double Tb[12];         // pair-list build transform (displacement reference)
+  double anchor[3];
+  double qscale;         // 2^k
+  float kappa;           // -log2(e) / (2 l^2 qscale^2): ex2 argument per unit^2
+  double sigma2;
+  double inv_l2;
+  double* partials;      // nvb_cap x M x 7
+  long long nvb_cap;
+  unsigned int* counter; // per request, self-resetting
+  unsigned long long* disp_bits;  // M, max squared displacement (self-resetting)
+  double* out;           // M x kOut
+};
+
+// All launches go to `stream`; d_reqs are device copies of h_reqs.
+void build_pairs_batched(const BuildReq* h_reqs, const BuildReq* d_reqs, int n, cudaStream_t stream);
+void sweep_batched(const SweepReq* h_reqs, const SweepReq* d_reqs, int n, int blocks_per_req,
+                   cudaStream_t stream, cudaEvent_t sweep_begin, cudaEvent_t sweep_end);
+void displacement(const double* zx, const double* zy, const double* zz, int n, const double* d_T2,
+                  unsigned long long* d_out, cudaStream_t stream);
+
+long long kernel_launch_count();
+
+}  // namespace kreg_dev

@@ -1,0 +1,504 @@
+// Host runtime: contexts, cloud upload (Morton-sorted device SoA), pair-list
+// workspaces and the batched round executor.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <sstream>
+
+#include "engine_host.hpp"
+
+namespace kreg_host {
+
+namespace {
+thread_local std::string g_last_error;
+constexpr long long kMaxCells = 1LL << 24;  // dense grid cap; larger => coarser cells
+}  // namespace
+
+void set_last_error(const std::string& m) { g_last_error = m; }
+const char* last_error() { return g_last_error.c_str(); }
+
+void throw_cuda(cudaError_t e, const char* what) {
+  cudaGetLastError();
+  const kreg_status code = e == cudaErrorMemoryAllocation ? KREG_OUT_OF_MEMORY
+                           : (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver) ? KREG_NO_DEVICE
+                                                                                          : KREG_CUDA_ERROR;
+  throw Error(code, std::string("CUDA error ") + cudaGetErrorString(e) + " in " + what);
+}
+
+Params to_params(const kreg_kernel_params* p) {
+  Params out;
+  out.sigma = p->sigma;
+  out.lengthscale = p->lengthscale;
+  for (int k = 0; k < p->n_channels; ++k) out.per_channel.push_back(p->per_channel[k]);
+  return out;
+}
+
+static const char* kind_name(int k) {
+  switch (k) {
+    case KREG_KIND_COLOR: return "color";
+    case KREG_KIND_INTENSITY: return "intensity";
+    case KREG_KIND_SEMANTIC: return "semantic";
+    default: return "custom";
+  }
+}
+
+std::string describe_schema(const kreg_cloud* c) {
+  // point_cloud.cpp:33-43
+  if (c->schema.empty()) return "<geometric-only>";
+  std::ostringstream os;
+  for (size_t k = 0; k < c->schema.size(); ++k) {
+    if (k) os << ",";
+    os << c->schema[k].name << "(" << kind_name(c->schema[k].kind) << ":" << c->schema[k].dim << ")";
+  }
+  return os.str();
+}
+
+void check_same_schema(const kreg_cloud* X, const kreg_cloud* Z, const char* prefix) {
+  // inner_product.cpp:26-33 / registration.cpp:77-82
+  bool same = X->schema.size() == Z->schema.size();
+  for (size_t k = 0; same && k < X->schema.size(); ++k) {
+    same = X->schema[k].name == Z->schema[k].name && X->schema[k].dim == Z->schema[k].dim &&
+           X->schema[k].kind == Z->schema[k].kind;
+  }
+  if (!same) {
+    throw Error(KREG_INVALID_ARGUMENT, std::string(prefix) + "schema mismatch: X has " + describe_schema(X) +
+                                           ", Z has " + describe_schema(Z));
+  }
+}
+
+void check_kernel_params(const Params& p, const kreg_cloud* c) {
+  // kernels.cpp:70-95
+  if (!(p.lengthscale > 0.0))
+    throw Error(KREG_INVALID_ARGUMENT,
+                "kernel params: geometric lengthscale must be > 0, got " + std::to_string(p.lengthscale));
+  if (!(p.sigma > 0.0)) throw Error(KREG_INVALID_ARGUMENT, "kernel params: sigma must be > 0");
+  if (p.per_channel.size() != c->schema.size()) {
+    std::ostringstream os;
+    os << "kernel params: " << p.per_channel.size() << " channel entries for schema " << describe_schema(c);
+    throw Error(KREG_INVALID_ARGUMENT, os.str());
+  }
+  for (size_t k = 0; k < p.per_channel.size(); ++k) {
+    const kreg_channel_params& cp = p.per_channel[k];
+    if (cp.form == KREG_FORM_SQUARED_EXPONENTIAL && !(cp.lengthscale > 0.0))
+      throw Error(KREG_INVALID_ARGUMENT,
+                  "kernel params: lengthscale of channel '" + c->schema[k].name + "' must be > 0");
+    if (!(cp.sigma > 0.0))
+      throw Error(KREG_INVALID_ARGUMENT, "kernel params: sigma of channel '" + c->schema[k].name + "' must be > 0");
+  }
+  if (p.per_channel.size() > static_cast<size_t>(kreg_dev::kMaxChannels))
+    throw Error(KREG_INVALID_ARGUMENT, "kernel params: at most 8 feature channels are supported");
+}
+
+void check_config(const kreg_registration_config& c) {
+  // registration.cpp:12-34
+  auto fail = [](const std::string& what) { throw Error(KREG_INVALID_ARGUMENT, "config: " + what); };
+  if (!(c.decay_factor > 0.0 && c.decay_factor < 1.0))
+    fail("decay_factor must lie in (0, 1), got " + std::to_string(c.decay_factor));
+  if (!(c.min_lengthscale > 0.0)) fail("min_lengthscale must be > 0");
+  if (!(c.min_lengthscale <= c.init_lengthscale)) fail("min_lengthscale must not exceed init_lengthscale");
+  if (!(c.subsequent_lengthscale > 0.0)) fail("subsequent_lengthscale must be > 0");
+  if (c.max_iterations < 1) fail("max_iterations must be >= 1");
+  if (c.stabilization_window < 1) fail("stabilization_window must be >= 1");
+  if (!(c.stabilization_rel_tol > 0.0)) fail("stabilization_rel_tol must be > 0");
+  if (!(c.step_init > 0.0)) fail("step_init must be > 0");
+  if (!(c.step_shrink > 0.0 && c.step_shrink < 1.0)) fail("step_shrink must lie in (0, 1)");
+  if (!(c.step_grow >= 1.0)) fail("step_grow must be >= 1");
+  if (c.max_backtracks < 0) fail("max_backtracks must be >= 0");
+  if (!(c.convergence_twist_norm > 0.0)) fail("convergence_twist_norm must be > 0");
+  if (!(c.cutoff_multiplier >= 1.0)) fail("cutoff_multiplier must be >= 1");
+  if (c.c_min < 0.0 || c.c_min >= 1.0) fail("c_min must lie in [0, 1)");
+}
+
+double diameter_host(const double* xyz, int n) {
+  // point_cloud.cpp:69-87
+  if (n <= 1) return 0.0;
+  if (n <= 2000) {
+    double best = 0.0;
+    for (int i = 0; i < n; ++i)
+      for (int j = i + 1; j < n; ++j) {
+        const double dx = xyz[3 * i] - xyz[3 * j], dy = xyz[3 * i + 1] - xyz[3 * j + 1],
+                     dz = xyz[3 * i + 2] - xyz[3 * j + 2];
+        best = std::max(best, dx * dx + dy * dy + dz * dz);
+      }
+    return std::sqrt(best);
+  }
+  double lo[3], hi[3];
+  for (int k = 0; k < 3; ++k) lo[k] = hi[k] = xyz[k];
+  for (int i = 1; i < n; ++i)
+    for (int k = 0; k < 3; ++k) {
+      lo[k] = std::min(lo[k], xyz[3 * i + k]);
+      hi[k] = std::max(hi[k], xyz[3 * i + k]);
+    }
+  const double d0 = hi[0] - lo[0], d1 = hi[1] - lo[1], d2 = hi[2] - lo[2];
+  return std::sqrt(d0 * d0 + d1 * d1 + d2 * d2);
+}
+
+static uint64_t spread3(uint64_t v) {
+  v &= 0x1FFFFF;
+  v = (v | v << 32) & 0x1F00000000FFFFULL;
+  v = (v | v << 16) & 0x1F0000FF0000FFULL;
+  v = (v | v << 8) & 0x100F00F00F00F00FULL;
+  v = (v | v << 4) & 0x10C30C30C30C30C3ULL;
+  v = (v | v << 2) & 0x1249249249249249ULL;
+  return v;
+}
+
+kreg_cloud* cloud_create(kreg_ctx* ctx, const kreg_cloud_view* v) {
+  if (v->n < 0) throw Error(KREG_INVALID_ARGUMENT, "PointCloud: negative point count");
+  int total = 0;
+  for (int k = 0; k < v->n_channels; ++k) {
+    if (v->channels[k].dim <= 0)
+      throw Error(KREG_INVALID_ARGUMENT, std::string("FeatureSchema: channel '") + v->channels[k].name +
+                                             "' has non-positive dim");
+    for (int k2 = 0; k2 < k; ++k2)
+      if (std::strcmp(v->channels[k].name, v->channels[k2].name) == 0)
+        throw Error(KREG_INVALID_ARGUMENT,
+                    std::string("FeatureSchema: duplicate channel name '") + v->channels[k].name + "'");
+    total += v->channels[k].dim;
+  }
+  if (total != v->dim) {
+    std::ostringstream os;
+    os << "PointCloud: feature block has " << static_cast<long long>(v->n) * v->dim << " values, schema with "
+       << v->n << " points requires " << static_cast<long long>(v->n) * total;
+    throw Error(KREG_INVALID_ARGUMENT, os.str());
+  }
+  if (total > 64) throw Error(KREG_INVALID_ARGUMENT, "PointCloud: feature dim > 64 is not supported");
+  auto* c = new kreg_cloud;
+  c->ctx = ctx;
+  c->n = v->n;
+  c->dim = total;
+  c->fstride = (total + 3) / 4 * 4;
+  for (int k = 0; k < v->n_channels; ++k)
+    c->schema.push_back({v->channels[k].name, v->channels[k].dim, v->channels[k].kind});
+  const int n = v->n;
+  c->diam = diameter_host(v->xyz, n);
+  if (n > 0) {
+    for (int k = 0; k < 3; ++k) c->lo[k] = c->hi[k] = v->xyz[k];
+    for (int i = 1; i < n; ++i)
+      for (int k = 0; k < 3; ++k) {
+        c->lo[k] = std::min(c->lo[k], v->xyz[3 * i + k]);
+        c->hi[k] = std::max(c->hi[k], v->xyz[3 * i + k]);
+      }
+  }
+  // spatial (Morton) order so that index locality is spatial locality
+  std::vector<std::pair<uint64_t, int>> keys(static_cast<size_t>(n));
+  double span = 0.0;
+  for (int k = 0; k < 3; ++k) span = std::max(span, c->hi[k] - c->lo[k]);
+  const double s = span > 0 ? (double)((1 << 21) - 1) / span : 0.0;
+  for (int i = 0; i < n; ++i) {
+    uint64_t m = 0;
+    for (int k = 0; k < 3; ++k) {
+      const double f = (v->xyz[3 * i + k] - c->lo[k]) * s;
+      const uint64_t q = std::isfinite(f) ? static_cast<uint64_t>(std::min(std::max(f, 0.0), 2097151.0)) : 0;
+      m |= spread3(q) << k;
+    }
+    keys[static_cast<size_t>(i)] = {m, i};
+  }
+  std::sort(keys.begin(), keys.end());
+  c->order.resize(static_cast<size_t>(n));
+  c->rank.resize(static_cast<size_t>(n));
+  std::vector<double> hx(static_cast<size_t>(n)), hy(static_cast<size_t>(n)), hz(static_cast<size_t>(n));
+  std::vector<float> hf(static_cast<size_t>(n) * c->fstride, 0.0f);
+  for (int r = 0; r < n; ++r) {
+    const int i = keys[static_cast<size_t>(r)].second;
+    c->order[static_cast<size_t>(r)] = i;
+    c->rank[static_cast<size_t>(i)] = r;
+    hx[static_cast<size_t>(r)] = v->xyz[3 * i];
+    hy[static_cast<size_t>(r)] = v->xyz[3 * i + 1];
+    hz[static_cast<size_t>(r)] = v->xyz[3 * i + 2];
+    for (int d = 0; d < total; ++d)
+      hf[static_cast<size_t>(r) * c->fstride + d] = static_cast<float>(v->features[static_cast<size_t>(i) * total + d]);
+  }
+  try {
+    KREG_CUDA(cudaSetDevice(ctx->device));
+    c->x.ensure(n, false, 1.0);
+    c->y.ensure(n, false, 1.0);
+    c->z.ensure(n, false, 1.0);
+    c->feat.ensure(static_cast<size_t>(n) * c->fstride + 4, false, 1.0);
+    if (n) {
+      KREG_CUDA(cudaMemcpyAsync(c->x.ptr, hx.data(), sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+      KREG_CUDA(cudaMemcpyAsync(c->y.ptr, hy.data(), sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+      KREG_CUDA(cudaMemcpyAsync(c->z.ptr, hz.data(), sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+      if (c->fstride)
+        KREG_CUDA(cudaMemcpyAsync(c->feat.ptr, hf.data(), sizeof(float) * hf.size(), cudaMemcpyHostToDevice,
+                                  ctx->stream));
+      KREG_CUDA(cudaStreamSynchronize(ctx->stream));  // host staging vectors go out of scope
+    }
+  } catch (...) {
+    delete c;
+    throw;
+  }
+  return c;
+}
+
+// ------------------------------------------------------------ build setup
+static void prepare_build(kreg_ctx* ctx, BuildJob& job, kreg_dev::BuildReq& R) {
+  kreg_pairs* p = job.pairs;
+  const kreg_cloud* X = job.X;
+  const kreg_cloud* Z = job.Z;
+  p->ctx = ctx;
+  p->X = X;
+  p->Z = Z;
+  p->built_at_lengthscale = job.params.lengthscale;
+  p->cutoff_radius = job.cutoff_multiplier * job.params.lengthscale;
+  p->c_min = job.c_min;
+  p->sigma = job.params.sigma;
+  std::memcpy(p->T_build, job.T, sizeof(p->T_build));
+
+  std::memset(&R, 0, sizeof(R));
+  R.xx = X->x.ptr; R.xy = X->y.ptr; R.xz = X->z.ptr; R.xfeat = X->feat.ptr; R.n_x = X->n;
+  R.zx = Z->x.ptr; R.zy = Z->y.ptr; R.zz = Z->z.ptr; R.zfeat = Z->feat.ptr; R.n_z = Z->n;
+  std::memcpy(R.T, job.T, sizeof(R.T));
+  const double cutoff = p->cutoff_radius;
+  R.cutoff_sq = cutoff * cutoff;  // inner_product.cpp:59
+
+  // dense grid over X's bbox; cell >= cutoff (margin keeps the 27-cell
+  // stencil a superset of the FP64 cutoff ball under rounding)
+  double h = cutoff * (1.0 + 1e-7);
+  long long g[3];
+  for (;;) {
+    long long cells = 1;
+    for (int k = 0; k < 3; ++k) {
+      g[k] = X->n ? static_cast<long long>(std::floor((X->hi[k] - X->lo[k]) / h)) + 1 : 1;
+      cells *= g[k];
+    }
+    if (cells <= kMaxCells) break;
+    h *= 1.25;
+  }
+  for (int k = 0; k < 3; ++k) R.origin[k] = X->lo[k];
+  R.inv_h = 1.0 / h;
+  R.gx = static_cast<int>(g[0]);
+  R.gy = static_cast<int>(g[1]);
+  R.gz = static_cast<int>(g[2]);
+  R.n_cells = g[0] * g[1] * g[2];
+  p->n_cells = R.n_cells;
+  p->gx = R.gx; p->gy = R.gy; p->gz = R.gz;
+
+  // fixed point for the sweep: 2^22 units >= 8.5 l (kernel < 2e-16 beyond,
+  // where the 1.5*2^23 conversion saturates) and |x - anchor| < 2^28 units
+  double maxabs = 1e-3;
+  for (int k = 0; k < 3; ++k) {
+    p->anchor[k] = 0.5 * (X->lo[k] + X->hi[k]);
+    maxabs = std::max(maxabs, std::max(X->hi[k] - p->anchor[k], p->anchor[k] - X->lo[k]));
+  }
+  const int k1 = static_cast<int>(std::floor(std::log2(4194304.0 / (8.5 * job.params.lengthscale))));
+  const int k2 = static_cast<int>(std::floor(std::log2(268435456.0 / (maxabs * 1.0001))));
+  const int kq = std::max(-30, std::min(std::min(k1, k2), 40));
+  p->qscale = std::ldexp(1.0, kq);
+  for (int k = 0; k < 3; ++k) R.anchor[k] = p->anchor[k];
+  R.qscale = p->qscale;
+
+  // buffers
+  const int nx = X->n, nz = Z->n;
+  p->cell_count.ensure(static_cast<size_t>(R.n_cells) + 1, /*zero=*/true);
+  p->cell_start.ensure(static_cast<size_t>(R.n_cells) + 1);
+  p->cell_of.ensure(nx + 1);
+  p->tmp_items.ensure(nx + 1);
+  p->cell_items.ensure(nx + 1);
+  p->cx.ensure(nx + 1);
+  p->cy.ensure(nx + 1);
+  p->cz.ensure(nx + 1);
+  p->count.ensure(nz + 1);
+  p->offsets.ensure(nz + 2);
+  p->xq.ensure(nx + 1);
+  p->scan_tiles.ensure(static_cast<size_t>(std::max<long long>(R.n_cells, nz) / kreg_dev::kScanTile + 4));
+  long long want = p->expected_pairs > 0 ? p->expected_pairs : static_cast<long long>(nz) * 32 + 1024;
+  if (p->pairs.cap < static_cast<size_t>(want)) p->pairs.ensure(static_cast<size_t>(want));
+  p->chunk_j.ensure(p->pairs.cap / kreg_dev::kPairsPerChunk + 2);
+
+  R.cell_count = p->cell_count.ptr;
+  R.cell_start = p->cell_start.ptr;
+  R.cell_of = p->cell_of.ptr;
+  R.tmp_items = p->tmp_items.ptr;
+  R.cell_items = p->cell_items.ptr;
+  R.cx = p->cx.ptr; R.cy = p->cy.ptr; R.cz = p->cz.ptr;
+  R.count = p->count.ptr;
+  R.offsets = p->offsets.ptr;
+  R.pairs = p->pairs.ptr;
+  R.capacity = static_cast<long long>(p->pairs.cap);
+  R.chunk_j = p->chunk_j.ptr;
+  R.xq = p->xq.ptr;
+  R.scan_tiles = p->scan_tiles.ptr;
+
+  // coefficient params (kernels.cpp:18-53)
+  R.cp.n_channels = static_cast<int>(job.params.per_channel.size());
+  R.cp.fstride = X->fstride;
+  R.cp.c_min = static_cast<float>(job.c_min);
+  int off = 0;
+  for (int k = 0; k < R.cp.n_channels; ++k) {
+    const kreg_channel_params& cp = job.params.per_channel[static_cast<size_t>(k)];
+    kreg_dev::ChannelDev& ch = R.cp.ch[k];
+    ch.offset = off;
+    ch.dim = X->schema[static_cast<size_t>(k)].dim;
+    ch.linear = cp.form == KREG_FORM_LINEAR ? 1 : 0;
+    ch.kappa = static_cast<float>(-1.4426950408889634 / (2.0 * cp.lengthscale * cp.lengthscale));
+    ch.sigma2 = static_cast<float>(cp.sigma * cp.sigma);
+    off += ch.dim;
+  }
+}
+
+static void prepare_sweep(EvalJob& job, kreg_dev::SweepReq& R) {
+  kreg_pairs* p = job.pairs;
+  std::memset(&R, 0, sizeof(R));
+  const int nz = p->Z->n;
+  R.offsets = p->offsets.ptr;
+  R.pairs = p->pairs.ptr;
+  R.capacity = static_cast<long long>(p->pairs.cap);
+  R.chunk_j = p->chunk_j.ptr;
+  R.xq = p->xq.ptr;
+  R.zx = p->Z->x.ptr; R.zy = p->Z->y.ptr; R.zz = p->Z->z.ptr;
+  p->q.ensure(static_cast<size_t>(kreg_dev::kMaxCandidates) * (nz + 1));
+  R.q = p->q.ptr;
+  R.n_z = nz;
+  R.M = job.M;
+  for (int m = 0; m < job.M; ++m) std::memcpy(R.T[m], job.T[m], sizeof(double) * 12);
+  std::memcpy(R.Tb, p->T_build, sizeof(R.Tb));
+  for (int k = 0; k < 3; ++k) R.anchor[k] = p->anchor[k];
+  R.qscale = p->qscale;
+  const double l = job.lengthscale;
+  R.kappa = static_cast<float>(-1.4426950408889634 / (2.0 * l * l) / (p->qscale * p->qscale));
+  R.sigma2 = p->sigma * p->sigma;
+  R.inv_l2 = 1.0 / (l * l);
+  const long long nvb = static_cast<long long>(p->pairs.cap) / kreg_dev::kPairsPerVBlock + 2;
+  p->partials.ensure(static_cast<size_t>(nvb) * kreg_dev::kMaxCandidates * 7);
+  R.partials = p->partials.ptr;
+  R.nvb_cap = nvb;
+  p->counter.ensure(1, true);
+  p->disp_bits.ensure(kreg_dev::kMaxCandidates, true);
+  R.counter = p->counter.ptr;
+  R.disp_bits = p->disp_bits.ptr;
+}
+
+void run_round(kreg_ctx* ctx, std::vector<BuildJob>& builds, std::vector<EvalJob>& evals) {
+  const int nb = static_cast<int>(builds.size());
+  const int ne = static_cast<int>(evals.size());
+  if (nb == 0 && ne == 0) return;
+  KREG_CUDA(cudaSetDevice(ctx->device));
+  ctx->h_build.ensure(nb + 1);
+  ctx->d_build.ensure(nb + 1);
+  ctx->h_sweep.ensure(ne + 1);
+  ctx->d_sweep.ensure(ne + 1);
+  const size_t n_res = static_cast<size_t>(ne) * kreg_dev::kMaxCandidates * kreg_dev::kOut + 2 * nb + 2;
+  ctx->d_results.ensure(n_res);
+  ctx->h_results.ensure(n_res);
+
+  for (int b = 0; b < nb; ++b) {
+    prepare_build(ctx, builds[b], ctx->h_build.ptr[b]);
+    ctx->h_build.ptr[b].status = ctx->d_results.ptr + static_cast<size_t>(ne) * kreg_dev::kMaxCandidates * kreg_dev::kOut + 2 * b;
+  }
+  long long max_nvb_est = 1;
+  for (int e = 0; e < ne; ++e) {
+    prepare_sweep(evals[e], ctx->h_sweep.ptr[e]);
+    ctx->h_sweep.ptr[e].out = ctx->d_results.ptr + static_cast<size_t>(e) * kreg_dev::kMaxCandidates * kreg_dev::kOut;
+    const long long est = std::max<long long>(evals[e].pairs->P, evals[e].pairs->expected_pairs);
+    max_nvb_est = std::max(max_nvb_est, est / kreg_dev::kPairsPerVBlock + 1);
+  }
+  if (nb)
+    KREG_CUDA(cudaMemcpyAsync(ctx->d_build.ptr, ctx->h_build.ptr, sizeof(kreg_dev::BuildReq) * nb,
+                              cudaMemcpyHostToDevice, ctx->stream));
+  if (ne)
+    KREG_CUDA(cudaMemcpyAsync(ctx->d_sweep.ptr, ctx->h_sweep.ptr, sizeof(kreg_dev::SweepReq) * ne,
+                              cudaMemcpyHostToDevice, ctx->stream));
+  if (nb) kreg_dev::build_pairs_batched(ctx->h_build.ptr, ctx->d_build.ptr, nb, ctx->stream);
+  if (ne) {
+    // ~6 resident sweep blocks per SM spread over the requests
+    const long long target = static_cast<long long>(ctx->sm_count) * 6;
+    int bpr = static_cast<int>(std::max<long long>(1, std::min<long long>(max_nvb_est, (target + ne - 1) / ne)));
+    kreg_dev::sweep_batched(ctx->h_sweep.ptr, ctx->d_sweep.ptr, ne, bpr, ctx->stream,
+                            ctx->profiling ? ctx->ev_sweep0 : nullptr, ctx->profiling ? ctx->ev_sweep1 : nullptr);
+  }
+  KREG_CUDA(cudaGetLastError());
+  KREG_CUDA(cudaMemcpyAsync(ctx->h_results.ptr, ctx->d_results.ptr, sizeof(double) * n_res,
+                            cudaMemcpyDeviceToHost, ctx->stream));
+  KREG_CUDA(cudaStreamSynchronize(ctx->stream));
+
+  const double* res = ctx->h_results.ptr;
+  std::vector<int> redo;
+  for (int b = 0; b < nb; ++b) {
+    const double* st = res + static_cast<size_t>(ne) * kreg_dev::kMaxCandidates * kreg_dev::kOut + 2 * b;
+    builds[b].pairs->P = static_cast<long long>(st[0]);
+    if (st[1] != 0.0) {
+      builds[b].pairs->expected_pairs = static_cast<long long>(st[0] * 1.15) + 1024;
+      redo.push_back(b);
+    } else {
+      builds[b].pairs->expected_pairs = std::max(builds[b].pairs->expected_pairs, builds[b].pairs->P);
+    }
+  }
+  if (!redo.empty()) {
+    // grow and re-run the overflowed builds and every evaluation in this round
+    std::vector<BuildJob> b2;
+    for (int b : redo) b2.push_back(builds[b]);
+    run_round(ctx, b2, evals);
+    return;
+  }
+  for (int e = 0; e < ne; ++e) {
+    std::memcpy(evals[e].out, res + static_cast<size_t>(e) * kreg_dev::kMaxCandidates * kreg_dev::kOut,
+                sizeof(double) * kreg_dev::kOut * evals[e].M);
+    ctx->pair_evals += evals[e].pairs->P * evals[e].M;
+  }
+  if (ne) {
+    ctx->sweep_launches += 1;
+    if (ctx->profiling) {
+      float ms = 0.0f;
+      KREG_CUDA(cudaEventElapsedTime(&ms, ctx->ev_sweep0, ctx->ev_sweep1));
+      ctx->sweep_ms += ms;
+    }
+  }
+}
+
+double max_point_displacement_dev(kreg_ctx* ctx, const kreg_cloud* Z, const double* built, const double* now) {
+  if (Z->n == 0) return 0.0;
+  ctx->d_T2.ensure(24);
+  ctx->d_disp.ensure(1);
+  ctx->h_results.ensure(4);
+  double T2[24];
+  std::memcpy(T2, built, sizeof(double) * 12);
+  std::memcpy(T2 + 12, now, sizeof(double) * 12);
+  KREG_CUDA(cudaMemcpyAsync(ctx->d_T2.ptr, T2, sizeof(T2), cudaMemcpyHostToDevice, ctx->stream));
+  KREG_CUDA(cudaMemsetAsync(ctx->d_disp.ptr, 0, sizeof(unsigned long long), ctx->stream));
+  kreg_dev::displacement(Z->x.ptr, Z->y.ptr, Z->z.ptr, Z->n, ctx->d_T2.ptr, ctx->d_disp.ptr, ctx->stream);
+  unsigned long long bits = 0;
+  KREG_CUDA(cudaMemcpyAsync(&bits, ctx->d_disp.ptr, sizeof(bits), cudaMemcpyDeviceToHost, ctx->stream));
+  KREG_CUDA(cudaStreamSynchronize(ctx->stream));
+  double d2;
+  std::memcpy(&d2, &bits, sizeof(d2));
+  return std::sqrt(d2);
+}
+
+void pairs_export(kreg_ctx* ctx, const kreg_pairs* p, int64_t* offsets, int32_t* x_index, double* coeff) {
+  // reference layout: CSR by ORIGINAL source index j, ascending ORIGINAL i
+  const int nz = p->Z ? p->Z->n : 0;
+  std::vector<long long> off(static_cast<size_t>(nz) + 1, 0);
+  std::vector<int2> pr(static_cast<size_t>(p->P));
+  if (nz) {
+    KREG_CUDA(cudaMemcpyAsync(off.data(), p->offsets.ptr, sizeof(long long) * (nz + 1), cudaMemcpyDeviceToHost,
+                              ctx->stream));
+    if (p->P)
+      KREG_CUDA(cudaMemcpyAsync(pr.data(), p->pairs.ptr, sizeof(int2) * p->P, cudaMemcpyDeviceToHost, ctx->stream));
+    KREG_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  std::vector<long long> cnt(static_cast<size_t>(nz), 0);
+  for (int js = 0; js < nz; ++js) cnt[static_cast<size_t>(p->Z->order[js])] = off[js + 1] - off[js];
+  offsets[0] = 0;
+  for (int j = 0; j < nz; ++j) offsets[j + 1] = offsets[j] + cnt[static_cast<size_t>(j)];
+  std::vector<std::pair<int, double>> tmp;
+  for (int js = 0; js < nz; ++js) {
+    const int j = p->Z->order[js];
+    tmp.clear();
+    for (long long e = off[js]; e < off[js + 1]; ++e) {
+      float lc;
+      std::memcpy(&lc, &pr[static_cast<size_t>(e)].y, sizeof(float));
+      tmp.push_back({p->X->order[pr[static_cast<size_t>(e)].x], std::exp2(static_cast<double>(lc))});
+    }
+    std::sort(tmp.begin(), tmp.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+    long long at = offsets[j];
+    for (const auto& [i, c] : tmp) {
+      x_index[at] = i;
+      coeff[at] = c;
+      ++at;
+    }
+  }
+}
+
+}  // namespace kreg_host

@@ -1,0 +1,204 @@
+// Host-side runtime of the B200 CVO engine: device contexts, uploaded clouds,
+// pair-list workspaces and the batched "round" executor that the solver
+// drives (one round = batched builds + batched sweeps + one D2H).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/kreg_b200.h"
+#include "engine.cuh"
+
+namespace kreg_host {
+
+// Exception carrying a kreg_status; the C-ABI maps it back to a code.
+struct Error : std::runtime_error {
+  kreg_status code;
+  Error(kreg_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] void throw_cuda(cudaError_t e, const char* what);
+#define KREG_CUDA(call)                                   \
+  do {                                                    \
+    cudaError_t e_ = (call);                              \
+    if (e_ != cudaSuccess) ::kreg_host::throw_cuda(e_, #call); \
+  } while (0)
+
+template <typename T>
+struct DevBuf {
+  T* ptr = nullptr;
+  size_t cap = 0;  // elements
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    cap = 0;
+  }
+  // grow (discarding contents) to hold at least n elements; optional zero fill
+  void ensure(size_t n, bool zero = false, double slack = 1.25) {
+    if (n <= cap && ptr) return;
+    release();
+    size_t want = n < 16 ? 16 : static_cast<size_t>(static_cast<double>(n) * slack);
+    cudaError_t e = cudaMalloc(&ptr, want * sizeof(T));
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      ptr = nullptr;
+      throw Error(KREG_OUT_OF_MEMORY, "device allocation of " + std::to_string(want * sizeof(T)) + " bytes failed");
+    }
+    cap = want;
+    if (zero) KREG_CUDA(cudaMemset(ptr, 0, want * sizeof(T)));
+  }
+};
+
+template <typename T>
+struct PinnedBuf {
+  T* ptr = nullptr;
+  size_t cap = 0;
+  ~PinnedBuf() {
+    if (ptr) cudaFreeHost(ptr);
+  }
+  void ensure(size_t n) {
+    if (n <= cap && ptr) return;
+    if (ptr) cudaFreeHost(ptr);
+    size_t want = n < 16 ? 16 : n * 2;
+    KREG_CUDA(cudaMallocHost(&ptr, want * sizeof(T)));
+    cap = want;
+  }
+};
+
+struct ChannelInfo {
+  std::string name;
+  int dim;
+  int kind;
+};
+
+struct Params {  // flattened KernelParams (kernels.hpp:23-33)
+  double sigma = 1.0;
+  double lengthscale = 1.0;
+  std::vector<kreg_channel_params> per_channel;
+};
+
+struct Config {  // RegistrationConfig (registration.hpp:13-40)
+  kreg_registration_config c;
+};
+
+}  // namespace kreg_host
+
+struct kreg_ctx {
+  int device = 0;
+  int sm_count = 148;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev_sweep0 = nullptr, ev_sweep1 = nullptr;
+  bool profiling = false;
+  double sweep_ms = 0.0;
+  long long sweep_launches = 0;
+  long long pair_evals = 0;
+  long long launches_base = 0;
+  // round staging
+  kreg_host::DevBuf<kreg_dev::BuildReq> d_build;
+  kreg_host::DevBuf<kreg_dev::SweepReq> d_sweep;
+  kreg_host::PinnedBuf<kreg_dev::BuildReq> h_build;
+  kreg_host::PinnedBuf<kreg_dev::SweepReq> h_sweep;
+  kreg_host::DevBuf<double> d_results;
+  kreg_host::PinnedBuf<double> h_results;
+  kreg_host::DevBuf<double> d_T2;
+  kreg_host::DevBuf<unsigned long long> d_disp;
+};
+
+struct kreg_cloud {
+  kreg_ctx* ctx = nullptr;
+  int n = 0;
+  int dim = 0;
+  int fstride = 0;
+  std::vector<kreg_host::ChannelInfo> schema;
+  double diam = 0.0;
+  double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+  kreg_host::DevBuf<double> x, y, z;  // sorted order
+  kreg_host::DevBuf<float> feat;      // sorted order, stride fstride
+  std::vector<int> order;              // sorted rank -> original index
+  std::vector<int> rank;               // original index -> sorted rank
+};
+
+// A pair list plus all device workspace needed to (re)build and sweep it.
+// The solver keeps one per registration slot and rebuilds it in place.
+struct kreg_pairs {
+  kreg_ctx* ctx = nullptr;
+  const kreg_cloud* X = nullptr;
+  const kreg_cloud* Z = nullptr;
+  // reference PairList metadata (inner_product.hpp:18-32)
+  double built_at_lengthscale = 0.0;
+  double cutoff_radius = 0.0;
+  double c_min = 0.0;
+  double T_build[12] = {1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1, 0};
+  long long P = 0;           // valid after the build round completed
+  double sigma = 1.0;
+  // grid
+  long long n_cells = 0;
+  int gx = 0, gy = 0, gz = 0;
+  kreg_host::DevBuf<int> cell_count, cell_start, cell_of, tmp_items, cell_items, count;
+  kreg_host::DevBuf<double> cx, cy, cz;
+  kreg_host::DevBuf<long long> offsets, scan_tiles;
+  kreg_host::DevBuf<int2> pairs;
+  kreg_host::DevBuf<int> chunk_j, overflow;
+  kreg_host::DevBuf<int4> xq;
+  double anchor[3] = {0, 0, 0};
+  double qscale = 1.0;
+  // sweep scratch
+  kreg_host::DevBuf<int4> q;
+  kreg_host::DevBuf<double> partials;
+  kreg_host::DevBuf<unsigned int> counter;
+  kreg_host::DevBuf<unsigned long long> disp_bits;
+  long long expected_pairs = 0;  // capacity hint
+};
+
+namespace kreg_host {
+
+void set_last_error(const std::string& m);
+const char* last_error();
+
+Params to_params(const kreg_kernel_params* p);
+void check_kernel_params(const Params& p, const kreg_cloud* schema_of);
+void check_same_schema(const kreg_cloud* X, const kreg_cloud* Z, const char* prefix);
+std::string describe_schema(const kreg_cloud* c);
+void check_config(const kreg_registration_config& c);
+
+kreg_cloud* cloud_create(kreg_ctx* ctx, const kreg_cloud_view* v);
+double diameter_host(const double* xyz, int n);
+
+// One build request; `pairs` is (re)initialised for X, Z at transform T.
+struct BuildJob {
+  kreg_pairs* pairs;
+  const kreg_cloud* X;
+  const kreg_cloud* Z;
+  double T[12];
+  Params params;       // lengthscale = the build lengthscale
+  double cutoff_multiplier;
+  double c_min;
+};
+
+// One evaluation request: M (<= 8) transforms against a built pair list.
+struct EvalJob {
+  kreg_pairs* pairs;
+  int M;
+  double T[kreg_dev::kMaxCandidates][12];
+  double lengthscale;  // kernel lengthscale of the evaluation
+  double* out;         // host, M x 8 {F, omega, v, disp}; filled after run_round
+};
+
+// Executes builds (then, in stream order, evaluations) as batched launches,
+// one D2H, one synchronize. Builds whose pair list overflowed its capacity
+// are grown and re-run transparently. Updates pairs->P.
+void run_round(kreg_ctx* ctx, std::vector<BuildJob>& builds, std::vector<EvalJob>& evals);
+
+double max_point_displacement_dev(kreg_ctx* ctx, const kreg_cloud* Z, const double* built, const double* now);
+
+void pairs_export(kreg_ctx* ctx, const kreg_pairs* p, int64_t* offsets, int32_t* x_index, double* coeff);
+
+}  // namespace kreg_host

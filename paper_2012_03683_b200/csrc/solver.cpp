@@ -1,0 +1,444 @@
+// Host registration loop (reference registration.cpp:100-189), written as a
+// per-registration state machine so that any number of independent
+// registrations advance in lockstep on one device: every round issues the
+// batched pair builds and candidate sweeps of all active registrations, then
+// one D2H + synchronize, then each state machine consumes its results.
+//
+// Parity contract: identical decisions to the
+// reference given identical F/grad values — rebuild rule, skip rule, step
+// candidates eps_k = step0 * shrink^k (running product), first F > f0
+// accepted, step_factor adaptation, traces, convergence and annealing. The
+// device differs only in HOW it evaluates:
+//  * the line-search candidates are evaluated K at a time (with gradient and
+//    displacement), and the accepted candidate's gradient is reused as the
+//    next iteration's objective_and_gradient at the same T and pair list
+//    (bitwise what a fresh evaluation would return: the sweep is
+//    deterministic and independent of batch composition);
+//  * candidate values are memoised across iterations while (T, dir, pair
+//    list) are unchanged (a failed search re-tries the same candidates with
+//    a halved step, registration.cpp:154).
+#include <algorithm>
+#include <cfloat>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <vector>
+
+#include "engine_host.hpp"
+#include "se3_host.hpp"
+#include "solver.hpp"
+
+namespace kreg_host {
+
+double anneal_step(double lengthscale, const double* hist, int n, const kreg_registration_config& c) {
+  // registration.cpp:36-52
+  const int window = c.stabilization_window;
+  if (n < window) return lengthscale;
+  const double* last = hist + (n - window);
+  double lo = last[0], hi = last[0], scale = std::abs(last[0]);
+  for (int k = 0; k < window; ++k) {
+    lo = std::min(lo, last[k]);
+    hi = std::max(hi, last[k]);
+    scale = std::max(scale, std::abs(last[k]));
+  }
+  if (hi - lo > c.stabilization_rel_tol * std::max(scale, DBL_MIN)) return lengthscale;
+  const double decayed = lengthscale * c.decay_factor;
+  return decayed >= c.min_lengthscale ? decayed : lengthscale;
+}
+
+namespace {
+
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atoi(v) : dflt;
+}
+
+struct Memo {
+  double eps;
+  double out[kreg_dev::kOut];
+};
+
+enum class Phase { kInit, kStartIter, kAwaitEval, kSearchSetup, kSearch, kAwaitCandidates, kDone };
+
+struct Reg {
+  RegJob* job = nullptr;
+  kreg_registration_config cfg{};
+  Params wp;
+  std::unique_ptr<kreg_pairs> pairs;
+  double v_scale = 1.0, denom = 1.0;
+  double lengthscale = 0.0;
+  double T[12];
+  std::vector<double> window;
+  double step_factor = 1.0;
+  // evaluation at T with the current pair list
+  bool have_eval = false;
+  double ev[kreg_dev::kOut];  // F, omega, v, disp
+  bool rebuilt = false;       // this iteration rebuilt the pair list
+  bool awaiting_build = false;
+  // line search
+  double dir[6];
+  double step0 = 0.0;
+  int k_next = 0;            // next candidate index
+  double eps_next = 0.0;     // eps of candidate k_next
+  std::vector<Memo> memo;    // candidates known for (T, dir, pairs)
+  int pending = 0;           // candidates in flight
+  double cand_T[24][12];
+  double cand_eps[24];
+  double cand_out[24][kreg_dev::kOut];
+  // outputs
+  std::vector<double> tr_obj, tr_ind, tr_l, tr_step, tr_tn;
+  std::vector<long long> tr_pc;
+  std::vector<uint8_t> tr_rb;
+  bool converged = false;
+  Phase phase = Phase::kInit;
+  int sweeps = 0, rebuilds = 0;
+};
+
+void finish(Reg& r) {
+  RegJob& j = *r.job;
+  kreg_registration_result* o = j.out;
+  std::memcpy(o->transform, r.T, sizeof(r.T));
+  o->converged = r.converged ? 1 : 0;
+  o->iterations = static_cast<int>(r.tr_obj.size());
+  o->final_indicator = r.tr_ind.empty() ? 0.0 : r.tr_ind.back();
+  const int n = std::min(o->trace_capacity, o->iterations);
+  for (int i = 0; i < n; ++i) {
+    if (o->objective_trace) o->objective_trace[i] = r.tr_obj[i];
+    if (o->indicator_trace) o->indicator_trace[i] = r.tr_ind[i];
+    if (o->lengthscale_trace) o->lengthscale_trace[i] = r.tr_l[i];
+    if (o->step_trace) o->step_trace[i] = r.tr_step[i];
+    if (o->twist_norm_trace) o->twist_norm_trace[i] = r.tr_tn[i];
+    if (o->pair_count_trace) o->pair_count_trace[i] = r.tr_pc[i];
+    if (o->rebuild_trace) o->rebuild_trace[i] = r.tr_rb[i];
+  }
+  o->sweeps = r.sweeps;
+  o->rebuilds = r.rebuilds;
+  j.status = KREG_OK;
+  r.phase = Phase::kDone;
+  r.pairs.reset();
+}
+
+// End of one reference iteration (registration.cpp:145-182).
+void end_iteration(Reg& r, bool searched, bool accepted, int backtracks, double eps, const double* cand_T,
+                   const double* cand_out) {
+  const kreg_registration_config& c = r.cfg;
+  double accepted_step = 0.0, twist_norm = 0.0, f_now = r.ev[0];
+  if (searched) {
+    if (accepted) {
+      accepted_step = eps;
+      f_now = cand_out[0];
+      double applied[6];
+      for (int k = 0; k < 6; ++k) applied[k] = r.dir[k] * accepted_step;
+      std::memcpy(r.T, cand_T, sizeof(r.T));  // == compose(exp(applied), T)
+      twist_norm = std::sqrt(applied[0] * applied[0] + applied[1] * applied[1] + applied[2] * applied[2]) +
+                   std::sqrt(applied[3] * applied[3] + applied[4] * applied[4] + applied[5] * applied[5]) / r.v_scale;
+      r.step_factor = backtracks == 0 ? std::min(r.step_factor * c.step_grow, 1e3)
+                                      : std::max(r.step_factor * std::pow(c.step_shrink, backtracks), 1e-6);
+      std::memcpy(r.ev, cand_out, sizeof(r.ev));  // F, grad and displacement at the new T
+      r.have_eval = true;
+      r.memo.clear();
+    } else {
+      r.step_factor = std::max(r.step_factor * c.step_shrink, 1e-6);
+    }
+  }
+  const double ind = f_now / r.denom;
+  r.tr_l.push_back(r.lengthscale);
+  r.tr_obj.push_back(f_now);
+  r.tr_ind.push_back(ind);
+  r.tr_step.push_back(accepted_step);
+  r.tr_tn.push_back(twist_norm);
+  r.tr_pc.push_back(r.pairs->P);
+  r.tr_rb.push_back(r.rebuilt ? 1 : 0);
+  r.window.push_back(ind);
+
+  const bool at_floor = r.lengthscale * c.decay_factor < c.min_lengthscale;
+  if (at_floor && twist_norm < c.convergence_twist_norm) {
+    r.converged = true;
+    finish(r);
+    return;
+  }
+  const double next = anneal_step(r.lengthscale, r.window.data(), static_cast<int>(r.window.size()), c);
+  if (next != r.lengthscale) {
+    r.lengthscale = next;
+    r.wp.lengthscale = next;
+    r.window.clear();
+    r.step_factor = 1.0;
+  }
+  r.phase = Phase::kStartIter;
+}
+
+void schedule_build_eval(Reg& r, std::vector<BuildJob>& builds, std::vector<EvalJob>& evals,
+                         std::vector<Reg*>& eval_owner) {
+  BuildJob b;
+  b.pairs = r.pairs.get();
+  b.X = r.job->X;
+  b.Z = r.job->Z;
+  std::memcpy(b.T, r.T, sizeof(r.T));
+  b.params = r.wp;
+  b.cutoff_multiplier = r.cfg.cutoff_multiplier;
+  b.c_min = r.cfg.c_min;
+  builds.push_back(b);
+  EvalJob e;
+  e.pairs = r.pairs.get();
+  e.M = 1;
+  std::memcpy(e.T[0], r.T, sizeof(r.T));
+  e.lengthscale = r.lengthscale;
+  e.out = r.ev;
+  evals.push_back(e);
+  eval_owner.push_back(&r);
+  r.memo.clear();
+  r.have_eval = false;
+  r.awaiting_build = true;
+  ++r.rebuilds;
+  ++r.sweeps;
+}
+
+// Advance host-only logic until the registration needs device work.
+void plan(Reg& r, std::vector<BuildJob>& builds, std::vector<EvalJob>& evals, std::vector<Reg*>& owners,
+          int k_first) {
+  const kreg_registration_config& c = r.cfg;
+  for (;;) {
+    switch (r.phase) {
+      case Phase::kDone:
+      case Phase::kAwaitEval:
+      case Phase::kAwaitCandidates:
+        return;
+      case Phase::kInit:
+        // registration.cpp:110-115: initial build at T0 (+ the first evaluation)
+        schedule_build_eval(r, builds, evals, owners);
+        r.phase = Phase::kAwaitEval;
+        return;
+      case Phase::kStartIter: {
+        if (static_cast<int>(r.tr_obj.size()) >= c.max_iterations) {
+          finish(r);
+          return;
+        }
+        // registration.cpp:123-128 rebuild rule (displacement of T vs T_build
+        // comes from the sweep that evaluated T)
+        r.rebuilt = false;
+        if (r.pairs->built_at_lengthscale != r.lengthscale || r.ev[7] > 0.5 * r.pairs->cutoff_radius ||
+            !r.have_eval) {
+          const bool must = r.pairs->built_at_lengthscale != r.lengthscale || r.ev[7] > 0.5 * r.pairs->cutoff_radius;
+          if (must) {
+            r.rebuilt = true;
+            schedule_build_eval(r, builds, evals, owners);
+            r.phase = Phase::kAwaitEval;
+            return;
+          }
+          EvalJob e;
+          e.pairs = r.pairs.get();
+          e.M = 1;
+          std::memcpy(e.T[0], r.T, sizeof(r.T));
+          e.lengthscale = r.lengthscale;
+          e.out = r.ev;
+          evals.push_back(e);
+          owners.push_back(&r);
+          ++r.sweeps;
+          r.phase = Phase::kAwaitEval;
+          return;
+        }
+        r.phase = Phase::kSearchSetup;
+        break;
+      }
+      case Phase::kSearchSetup: {
+        const double* g = r.ev + 1;
+        const double gnorm = kreg_se3::twist_norm6(g);
+        r.step0 = c.step_init * r.lengthscale * r.step_factor;  // registration.cpp:132
+        // registration.cpp:139 skip rule
+        if (gnorm > 0.0 && r.step0 * gnorm > 1e-12 * std::max(std::abs(r.ev[0]), 1.0)) {
+          const double s = 1.0 / gnorm;
+          double dir[6];
+          for (int k = 0; k < 6; ++k) dir[k] = g[k] * s;
+          if (std::memcmp(dir, r.dir, sizeof(dir)) != 0) r.memo.clear();
+          std::memcpy(r.dir, dir, sizeof(dir));
+          r.k_next = 0;
+          r.eps_next = r.step0;
+          r.phase = Phase::kSearch;
+        } else {
+          end_iteration(r, false, false, 0, 0.0, nullptr, nullptr);
+          if (r.phase == Phase::kDone) return;
+        }
+        break;
+      }
+      case Phase::kSearch: {
+        // registration.cpp:63-75: candidates k = k_next.. with eps_k = step0 * shrink^k
+        const int remaining = c.max_backtracks + 1 - r.k_next;
+        const int K = std::min(remaining, r.k_next == 0 ? k_first : 24);
+        // resolve memoised candidates first (same T, dir, pair list)
+        int n_new = 0;
+        r.pending = 0;
+        double eps = r.eps_next;
+        bool resolved = false;
+        const int k0 = r.k_next;
+        for (int m = 0; m < K; ++m) {
+          const int k = k0 + m;
+          const Memo* hit = nullptr;
+          for (const Memo& mm : r.memo)
+            if (mm.eps == eps) hit = &mm;
+          double cand[12], tw[6], E[12];
+          for (int t = 0; t < 6; ++t) tw[t] = r.dir[t] * eps;
+          kreg_se3::exp(tw, E);
+          kreg_se3::compose(E, r.T, cand);
+          if (hit && n_new == 0) {
+            if (hit->out[0] > r.ev[0]) {
+              end_iteration(r, true, true, k, eps, cand, hit->out);
+              resolved = true;
+              break;
+            }
+            r.k_next = k + 1;
+            r.eps_next = eps * c.step_shrink;
+          } else {
+            std::memcpy(r.cand_T[n_new], cand, sizeof(cand));
+            r.cand_eps[n_new] = eps;
+            ++n_new;
+          }
+          eps *= c.step_shrink;
+        }
+        if (resolved) {
+          if (r.phase == Phase::kDone) return;
+          break;
+        }
+        if (n_new == 0) {
+          if (r.k_next > c.max_backtracks) {
+            end_iteration(r, true, false, 0, 0.0, nullptr, nullptr);
+            if (r.phase == Phase::kDone) return;
+          }
+          break;  // continue searching (more memo hits or new candidates)
+        }
+        for (int b = 0; b < n_new; b += kreg_dev::kMaxCandidates) {
+          EvalJob e;
+          e.pairs = r.pairs.get();
+          e.M = std::min(kreg_dev::kMaxCandidates, n_new - b);
+          for (int m = 0; m < e.M; ++m) std::memcpy(e.T[m], r.cand_T[b + m], sizeof(double) * 12);
+          e.lengthscale = r.lengthscale;
+          e.out = &r.cand_out[b][0];
+          evals.push_back(e);
+          owners.push_back(&r);
+          ++r.sweeps;
+        }
+        r.pending = n_new;
+        r.phase = Phase::kAwaitCandidates;
+        return;
+      }
+    }
+  }
+}
+
+void consume(Reg& r) {
+  const kreg_registration_config& c = r.cfg;
+  if (r.phase == Phase::kAwaitEval) {
+    if (r.awaiting_build) {
+      r.awaiting_build = false;
+      if (r.pairs->P == 0) {
+        if (r.tr_obj.empty() && !r.rebuilt) {
+          // registration.cpp:115
+          char msg[160];
+          std::snprintf(msg, sizeof(msg), "no overlapping pairs within cutoff radius %f m", r.pairs->cutoff_radius);
+          r.job->status = KREG_NO_OVERLAP;
+          r.job->error = msg;
+          r.phase = Phase::kDone;
+          r.pairs.reset();
+          return;
+        }
+        finish(r);  // registration.cpp:127: drifted out of support, unconverged
+        return;
+      }
+    }
+    r.have_eval = true;
+    r.phase = Phase::kSearchSetup;
+    return;
+  }
+  if (r.phase == Phase::kAwaitCandidates) {
+    for (int m = 0; m < r.pending; ++m) {
+      Memo mm;
+      mm.eps = r.cand_eps[m];
+      std::memcpy(mm.out, r.cand_out[m], sizeof(mm.out));
+      r.memo.push_back(mm);
+    }
+    for (int m = 0; m < r.pending; ++m) {
+      const int k = r.k_next + m;
+      if (r.cand_out[m][0] > r.ev[0]) {
+        double T[12], out[kreg_dev::kOut];
+        std::memcpy(T, r.cand_T[m], sizeof(T));
+        std::memcpy(out, r.cand_out[m], sizeof(out));
+        end_iteration(r, true, true, k, r.cand_eps[m], T, out);
+        return;
+      }
+    }
+    r.k_next += r.pending;
+    r.eps_next = r.cand_eps[r.pending - 1] * c.step_shrink;
+    if (r.k_next > c.max_backtracks) {
+      end_iteration(r, true, false, 0, 0.0, nullptr, nullptr);
+    } else {
+      r.phase = Phase::kSearch;
+    }
+  }
+}
+
+}  // namespace
+
+void register_many(kreg_ctx* ctx, std::vector<RegJob>& jobs) {
+  const int k_first = std::max(1, std::min(8, env_int("KREG_K_FIRST", 2)));
+  std::vector<std::unique_ptr<Reg>> regs;
+  for (RegJob& j : jobs) {
+    j.status = KREG_OK;
+    auto r = std::make_unique<Reg>();
+    r->job = &j;
+    try {
+      check_config(j.cfg);                          // registration.cpp:102
+      check_same_schema(j.X, j.Z, "register: ");    // :103-104
+      Params p0 = j.params;
+      p0.lengthscale = j.cfg.init_lengthscale;
+      check_kernel_params(p0, j.X);
+      if (!(j.cfg.cutoff_multiplier >= 1.0))
+        throw Error(KREG_INVALID_ARGUMENT, "build_pairs: cutoff_multiplier must be >= 1");
+    } catch (const Error& e) {
+      j.status = e.code;
+      j.error = e.what();
+      continue;
+    }
+    r->cfg = j.cfg;
+    r->wp = j.params;
+    const double diam = j.X->diam;
+    r->v_scale = diam > 0.0 ? diam : 1.0;
+    r->denom = std::sqrt(static_cast<double>(std::max(j.X->n, 1)) * static_cast<double>(std::max(j.Z->n, 1)));
+    r->lengthscale = j.cfg.init_lengthscale;
+    r->wp.lengthscale = r->lengthscale;
+    std::memcpy(r->T, j.initial, sizeof(r->T));
+    for (double& d : r->dir) d = 0.0;
+    r->pairs = std::make_unique<kreg_pairs>();
+    r->pairs->expected_pairs = j.expected_pairs;
+    if (j.X->n == 0 || j.Z->n == 0) {
+      // empty cloud: build_pairs yields an empty list -> NoOverlapError
+      char msg[160];
+      std::snprintf(msg, sizeof(msg), "no overlapping pairs within cutoff radius %f m",
+                    j.cfg.cutoff_multiplier * j.cfg.init_lengthscale);
+      j.status = KREG_NO_OVERLAP;
+      j.error = msg;
+      continue;
+    }
+    regs.push_back(std::move(r));
+  }
+
+  std::vector<BuildJob> builds;
+  std::vector<EvalJob> evals;
+  std::vector<Reg*> owners;
+  for (;;) {
+    builds.clear();
+    evals.clear();
+    owners.clear();
+    for (auto& r : regs) plan(*r, builds, evals, owners, k_first);
+    if (builds.empty() && evals.empty()) break;
+    run_round(ctx, builds, evals);
+    // each registration consumes once per round
+    Reg* last = nullptr;
+    for (Reg* r : owners) {
+      if (r == last) continue;
+      last = r;
+      consume(*r);
+    }
+  }
+}
+
+}  // namespace kreg_host
