@@ -156,6 +156,9 @@ int64_t kreg_ctx_kernel_launches(const kreg_ctx* ctx);
 kreg_status kreg_ctx_sweep_stats(const kreg_ctx* ctx, double* sweep_ms, int64_t* sweep_launches,
                                  int64_t* pair_evals);
 kreg_status kreg_ctx_set_profiling(kreg_ctx* ctx, int32_t enabled);
+/* Host-side round accounting: {rounds, s preparing + launching, s waiting for
+ * the device, reserved}. */
+kreg_status kreg_ctx_host_stats(const kreg_ctx* ctx, double out[4]);
 kreg_status kreg_ctx_reset_stats(kreg_ctx* ctx);
 
 /* Upload a cloud into device SoA (replaces constructing kreg::PointCloud,

@@ -53,6 +53,7 @@ def lib():
         L.kreg_ctx_kernel_launches.restype = C.c_int64
         L.kreg_ctx_sweep_stats.argtypes = [P, _abi.dptr, _abi.i64ptr, _abi.i64ptr]
         L.kreg_ctx_set_profiling.argtypes = [P, C.c_int32]
+        L.kreg_ctx_host_stats.argtypes = [P, _abi.dptr]
         L.kreg_ctx_reset_stats.argtypes = [P]
         L.kreg_cloud_create.argtypes = [P, VP, C.POINTER(P)]
         L.kreg_cloud_destroy.argtypes = [P]
@@ -128,6 +129,11 @@ class Context:
 
     def reset_stats(self):
         _check(lib().kreg_ctx_reset_stats(self.h))
+
+    def host_stats(self):
+        out = np.zeros(4)
+        _check(lib().kreg_ctx_host_stats(self.h, _abi.as_ptr(out)))
+        return {"rounds": int(out[0]), "t_prepare_s": float(out[1]), "t_wait_s": float(out[2])}
 
     def sweep_stats(self):
         ms = np.zeros(1)

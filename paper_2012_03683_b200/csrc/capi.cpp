@@ -243,6 +243,15 @@ kreg_status kreg_ctx_sweep_stats(const kreg_ctx* ctx, double* sweep_ms, int64_t*
   });
 }
 
+kreg_status kreg_ctx_host_stats(const kreg_ctx* ctx, double out[4]) {
+  return guarded([&] {
+    out[0] = static_cast<double>(ctx->rounds);
+    out[1] = ctx->t_prepare;
+    out[2] = ctx->t_wait;
+    out[3] = ctx->t_total;
+  });
+}
+
 kreg_status kreg_ctx_set_profiling(kreg_ctx* ctx, int32_t enabled) {
   return guarded([&] { ctx->profiling = enabled != 0; });
 }
@@ -252,6 +261,8 @@ kreg_status kreg_ctx_reset_stats(kreg_ctx* ctx) {
     ctx->sweep_ms = 0.0;
     ctx->sweep_launches = 0;
     ctx->pair_evals = 0;
+    ctx->rounds = 0;
+    ctx->t_prepare = ctx->t_wait = ctx->t_total = 0.0;
     ctx->launches_base = kreg_dev::kernel_launch_count();
   });
 }

@@ -10,12 +10,14 @@
 //     of the FP64 cutoff ball; counting sort with a deterministic order
 //     inside a cell (ascending point index) -> cell_start[] / cell_items[]
 //     plus cell-ordered FP64 copies cx/cy/cz for coalesced candidate tests.
-//   Pair list (per build): CSR by source j: offsets int64[n_z+1];
-//     pairs int2 {i, float_as_int(log2 c)} = 8 B/pair; chunk_j[] = owning j
-//     of every E-pair chunk (flattened, load-balanced sweep); xq int4[n_x]
-//     = X in fixed point (2^-k m units around the X bbox centre).
+//   Pair list (per build): sliced ELL over tiles of 32 consecutive sources:
+//     tile t holds 32 columns (one per source j = 32 t + l) of tile_deg[t]
+//     slots; slot (t, k, l) = tile_off[t] + 32 k + l; a slot is int2
+//     {i, float_as_int(log2 c)} = 8 B, padding {0, -inf}. CSR offsets
+//     (int64[n_z+1]) record the true degrees; xq int4[n_x] = X in fixed
+//     point (2^-k m units around the X bbox centre).
 //   Sweep scratch: q int4[M][n_z] (magic - fixed-point T z) per candidate;
-//     per-virtual-block FP64 partials; per-request completion counters.
+//     per-work-block FP64 partials; per-request completion counters.
 #pragma once
 
 #include <cstdint>
@@ -23,9 +25,10 @@
 
 namespace kreg_dev {
 
-constexpr int kPairsPerChunk = 8;   // E: pairs per thread chunk in the sweep
 constexpr int kSweepThreads = 256;  // threads per (virtual) sweep block
-constexpr int kPairsPerVBlock = kPairsPerChunk * kSweepThreads;
+constexpr int kUnitSteps = 8;          // degree steps per sweep work unit (x 32 lanes)
+constexpr long long kUnitsPerBlock = 32;  // work units per sweep work block (4 per warp)
+constexpr long long kMaxSweepBlocks = 1184;  // 8 x 148 SMs
 constexpr int kMaxChannels = 8;
 constexpr int kMaxCandidates = 8;   // candidate transforms per sweep request
 constexpr int kOut = 8;             // {F, omega[3], v[3], max displacement}
@@ -63,25 +66,35 @@ struct BuildReq {
   int* tmp_items;        // n_x
   int* cell_items;       // n_x
   double* cx; double* cy; double* cz;  // n_x cell-ordered positions
-  int* count;            // n_z
-  long long* offsets;    // n_z + 1
-  int2* pairs;           // capacity
+  int* count;            // n_z: degree of every source
+  long long* offsets;    // n_z + 1: CSR offsets (pair count, export)
+  int n_tiles;           // ceil(n_z / 32)
+  int* tile_deg;         // n_tiles: max degree in the tile
+  int* tile_slots;       // n_tiles: 32 * tile_deg
+  int* tile_units;       // n_tiles: ceil(tile_deg / kUnitSteps)
+  long long* tile_off;   // n_tiles + 1: sliced-ELL slot offsets
+  int* unit_off;         // n_tiles + 1: sweep work-unit offsets
+  int* unit_tile;        // capacity / 256 + n_tiles + 1: tile of every work unit
+  int2* pairs;           // capacity slots {i, float_as_int(log2 c)}
   long long capacity;
-  int* chunk_j;          // capacity / E + 1
-  double* status;        // {P, P > capacity} written by the count scan
+  double* status;        // {P, slots > capacity, slots}
   int4* xq;              // n_x fixed-point X
   double anchor[3];
   double qscale;         // 2^k
-  long long* scan_tiles; // scan workspace (tile sums)
+  long long* scan_tiles; // scan workspace (tile sums), 4 modes x scan_stride
+  long long scan_stride;
   CoeffParams cp;
 };
 
 // One sweep request: M candidate transforms against one pair list.
 struct SweepReq {
-  const long long* offsets;
+  const long long* tile_off;
+  const int* unit_off;
+  const int* unit_tile;
+  const int* tile_deg;
+  int n_tiles;
   const int2* pairs;
   long long capacity;    // pairs capacity (an overflowed build is skipped)
-  const int* chunk_j;
   const int4* xq;
   const double* zx; const double* zy; const double* zz;  // source, sorted
   int4* q;               // M x n_z scratch
@@ -94,8 +107,7 @@ struct SweepReq {
   float kappa;           // -log2(e) / (2 l^2 qscale^2): ex2 argument per unit^2
   double sigma2;
   double inv_l2;
-  double* partials;      // nvb_cap x M x 7
-  long long nvb_cap;
+  double* partials;      // kMaxSweepBlocks x M x 7
   unsigned int* counter; // per request, self-resetting
   unsigned long long* disp_bits;  // M, max squared displacement (self-resetting)
   double* out;           // M x kOut

@@ -1,12 +1,18 @@
 // Host runtime: contexts, cloud upload (Morton-sorted device SoA), pair-list
 // workspaces and the batched round executor.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <numeric>
 #include <sstream>
 
 #include "engine_host.hpp"
+
+kreg_ctx::~kreg_ctx() {
+  for (kreg_pairs* p : pool) delete p;
+  pool.clear();
+}
 
 namespace kreg_host {
 
@@ -163,14 +169,26 @@ kreg_cloud* cloud_create(kreg_ctx* ctx, const kreg_cloud_view* v) {
        << v->n << " points requires " << static_cast<long long>(v->n) * total;
     throw Error(KREG_INVALID_ARGUMENT, os.str());
   }
-  if (total > 64) throw Error(KREG_INVALID_ARGUMENT, "PointCloud: feature dim > 64 is not supported");
   auto* c = new kreg_cloud;
   c->ctx = ctx;
   c->n = v->n;
   c->dim = total;
-  c->fstride = (total + 3) / 4 * 4;
-  for (int k = 0; k < v->n_channels; ++k)
+  // device rows: every channel 16-B aligned and zero-padded to 4k floats
+  int padded = 0;
+  std::vector<int> src_off;
+  int so = 0;
+  for (int k = 0; k < v->n_channels; ++k) {
     c->schema.push_back({v->channels[k].name, v->channels[k].dim, v->channels[k].kind});
+    c->chan_off.push_back(padded);
+    src_off.push_back(so);
+    padded += (v->channels[k].dim + 3) / 4 * 4;
+    so += v->channels[k].dim;
+  }
+  c->fstride = padded;
+  if (padded > 64) {
+    delete c;
+    throw Error(KREG_INVALID_ARGUMENT, "PointCloud: padded feature row > 64 floats is not supported");
+  }
   const int n = v->n;
   c->diam = diameter_host(v->xyz, n);
   if (n > 0) {
@@ -207,8 +225,10 @@ kreg_cloud* cloud_create(kreg_ctx* ctx, const kreg_cloud_view* v) {
     hx[static_cast<size_t>(r)] = v->xyz[3 * i];
     hy[static_cast<size_t>(r)] = v->xyz[3 * i + 1];
     hz[static_cast<size_t>(r)] = v->xyz[3 * i + 2];
-    for (int d = 0; d < total; ++d)
-      hf[static_cast<size_t>(r) * c->fstride + d] = static_cast<float>(v->features[static_cast<size_t>(i) * total + d]);
+    for (int k = 0; k < v->n_channels; ++k)
+      for (int d = 0; d < v->channels[k].dim; ++d)
+        hf[static_cast<size_t>(r) * c->fstride + c->chan_off[k] + d] =
+            static_cast<float>(v->features[static_cast<size_t>(i) * total + src_off[k] + d]);
   }
   try {
     KREG_CUDA(cudaSetDevice(ctx->device));
@@ -302,10 +322,25 @@ static void prepare_build(kreg_ctx* ctx, BuildJob& job, kreg_dev::BuildReq& R) {
   p->count.ensure(nz + 1);
   p->offsets.ensure(nz + 2);
   p->xq.ensure(nx + 1);
-  p->scan_tiles.ensure(static_cast<size_t>(std::max<long long>(R.n_cells, nz) / kreg_dev::kScanTile + 4));
-  long long want = p->expected_pairs > 0 ? p->expected_pairs : static_cast<long long>(nz) * 32 + 1024;
+  R.scan_stride = std::max<long long>(R.n_cells, nz) / kreg_dev::kScanTile + 4;
+  p->scan_tiles.ensure(static_cast<size_t>(4 * R.scan_stride));
+  long long want = p->expected_pairs > 0 ? p->expected_pairs : static_cast<long long>(nz) * 48 + 1024;
   if (p->pairs.cap < static_cast<size_t>(want)) p->pairs.ensure(static_cast<size_t>(want));
-  p->chunk_j.ensure(p->pairs.cap / kreg_dev::kPairsPerChunk + 2);
+  const int n_tiles = (nz + 31) / 32;
+  p->n_tiles = n_tiles;
+  p->tile_deg.ensure(n_tiles + 1);
+  p->tile_slots.ensure(n_tiles + 1);
+  p->tile_units.ensure(n_tiles + 1);
+  p->tile_off.ensure(n_tiles + 2);
+  p->unit_off.ensure(n_tiles + 2);
+  p->unit_tile.ensure(p->pairs.cap / (32 * kreg_dev::kUnitSteps) + n_tiles + 2);
+  R.unit_tile = p->unit_tile.ptr;
+  R.n_tiles = n_tiles;
+  R.tile_deg = p->tile_deg.ptr;
+  R.tile_slots = p->tile_slots.ptr;
+  R.tile_units = p->tile_units.ptr;
+  R.tile_off = p->tile_off.ptr;
+  R.unit_off = p->unit_off.ptr;
 
   R.cell_count = p->cell_count.ptr;
   R.cell_start = p->cell_start.ptr;
@@ -317,7 +352,6 @@ static void prepare_build(kreg_ctx* ctx, BuildJob& job, kreg_dev::BuildReq& R) {
   R.offsets = p->offsets.ptr;
   R.pairs = p->pairs.ptr;
   R.capacity = static_cast<long long>(p->pairs.cap);
-  R.chunk_j = p->chunk_j.ptr;
   R.xq = p->xq.ptr;
   R.scan_tiles = p->scan_tiles.ptr;
 
@@ -325,31 +359,45 @@ static void prepare_build(kreg_ctx* ctx, BuildJob& job, kreg_dev::BuildReq& R) {
   R.cp.n_channels = static_cast<int>(job.params.per_channel.size());
   R.cp.fstride = X->fstride;
   R.cp.c_min = static_cast<float>(job.c_min);
-  int off = 0;
   for (int k = 0; k < R.cp.n_channels; ++k) {
     const kreg_channel_params& cp = job.params.per_channel[static_cast<size_t>(k)];
     kreg_dev::ChannelDev& ch = R.cp.ch[k];
-    ch.offset = off;
+    ch.offset = X->chan_off[static_cast<size_t>(k)];
     ch.dim = X->schema[static_cast<size_t>(k)].dim;
     ch.linear = cp.form == KREG_FORM_LINEAR ? 1 : 0;
     ch.kappa = static_cast<float>(-1.4426950408889634 / (2.0 * cp.lengthscale * cp.lengthscale));
     ch.sigma2 = static_cast<float>(cp.sigma * cp.sigma);
-    off += ch.dim;
   }
 }
 
-static void prepare_sweep(EvalJob& job, kreg_dev::SweepReq& R) {
+// Scratch of request e lives in per-round arenas of the context (several
+// requests of one round may sweep the same pair list).
+struct SweepScratch {
+  size_t q_off = 0, part_off = 0;
+};
+
+static size_t sweep_nvb_cap(const EvalJob& job) {
+  // units <= slots / (32 kUnitSteps) + n_tiles
+  const long long units = static_cast<long long>(job.pairs->pairs.cap) / (32 * kreg_dev::kUnitSteps) +
+                          job.pairs->n_tiles + 1;
+  const long long b = units / kreg_dev::kUnitsPerBlock + 2;
+  return static_cast<size_t>(std::min(b, kreg_dev::kMaxSweepBlocks));
+}
+
+static void prepare_sweep(kreg_ctx* ctx, EvalJob& job, kreg_dev::SweepReq& R, const SweepScratch& s, int e) {
   kreg_pairs* p = job.pairs;
   std::memset(&R, 0, sizeof(R));
   const int nz = p->Z->n;
-  R.offsets = p->offsets.ptr;
+  R.tile_off = p->tile_off.ptr;
+  R.unit_off = p->unit_off.ptr;
+  R.unit_tile = p->unit_tile.ptr;
+  R.tile_deg = p->tile_deg.ptr;
+  R.n_tiles = p->n_tiles;
   R.pairs = p->pairs.ptr;
   R.capacity = static_cast<long long>(p->pairs.cap);
-  R.chunk_j = p->chunk_j.ptr;
   R.xq = p->xq.ptr;
   R.zx = p->Z->x.ptr; R.zy = p->Z->y.ptr; R.zz = p->Z->z.ptr;
-  p->q.ensure(static_cast<size_t>(kreg_dev::kMaxCandidates) * (nz + 1));
-  R.q = p->q.ptr;
+  R.q = ctx->q_arena.ptr + s.q_off;
   R.n_z = nz;
   R.M = job.M;
   for (int m = 0; m < job.M; ++m) std::memcpy(R.T[m], job.T[m], sizeof(double) * 12);
@@ -360,39 +408,49 @@ static void prepare_sweep(EvalJob& job, kreg_dev::SweepReq& R) {
   R.kappa = static_cast<float>(-1.4426950408889634 / (2.0 * l * l) / (p->qscale * p->qscale));
   R.sigma2 = p->sigma * p->sigma;
   R.inv_l2 = 1.0 / (l * l);
-  const long long nvb = static_cast<long long>(p->pairs.cap) / kreg_dev::kPairsPerVBlock + 2;
-  p->partials.ensure(static_cast<size_t>(nvb) * kreg_dev::kMaxCandidates * 7);
-  R.partials = p->partials.ptr;
-  R.nvb_cap = nvb;
-  p->counter.ensure(1, true);
-  p->disp_bits.ensure(kreg_dev::kMaxCandidates, true);
-  R.counter = p->counter.ptr;
-  R.disp_bits = p->disp_bits.ptr;
+  R.partials = ctx->part_arena.ptr + s.part_off;
+  R.counter = ctx->counter_arena.ptr + e;
+  R.disp_bits = ctx->disp_arena.ptr + static_cast<size_t>(e) * kreg_dev::kMaxCandidates;
 }
 
 void run_round(kreg_ctx* ctx, std::vector<BuildJob>& builds, std::vector<EvalJob>& evals) {
   const int nb = static_cast<int>(builds.size());
   const int ne = static_cast<int>(evals.size());
   if (nb == 0 && ne == 0) return;
+  using clk = std::chrono::steady_clock;
+  const auto t0 = clk::now();
   KREG_CUDA(cudaSetDevice(ctx->device));
   ctx->h_build.ensure(nb + 1);
   ctx->d_build.ensure(nb + 1);
   ctx->h_sweep.ensure(ne + 1);
   ctx->d_sweep.ensure(ne + 1);
-  const size_t n_res = static_cast<size_t>(ne) * kreg_dev::kMaxCandidates * kreg_dev::kOut + 2 * nb + 2;
+  const size_t n_res = static_cast<size_t>(ne) * kreg_dev::kMaxCandidates * kreg_dev::kOut + 4 * nb + 4;
   ctx->d_results.ensure(n_res);
   ctx->h_results.ensure(n_res);
 
   for (int b = 0; b < nb; ++b) {
     prepare_build(ctx, builds[b], ctx->h_build.ptr[b]);
-    ctx->h_build.ptr[b].status = ctx->d_results.ptr + static_cast<size_t>(ne) * kreg_dev::kMaxCandidates * kreg_dev::kOut + 2 * b;
+    ctx->h_build.ptr[b].status = ctx->d_results.ptr + static_cast<size_t>(ne) * kreg_dev::kMaxCandidates * kreg_dev::kOut + 4 * b;
   }
   long long max_nvb_est = 1;
+  std::vector<SweepScratch> scratch(static_cast<size_t>(ne));
+  size_t q_total = 0, part_total = 0;
   for (int e = 0; e < ne; ++e) {
-    prepare_sweep(evals[e], ctx->h_sweep.ptr[e]);
+    scratch[e].q_off = q_total;
+    scratch[e].part_off = part_total;
+    q_total += static_cast<size_t>(evals[e].M) * (evals[e].pairs->Z->n + 1);
+    part_total += sweep_nvb_cap(evals[e]) * evals[e].M * 7;
+  }
+  if (ne) {
+    ctx->q_arena.ensure(q_total + 1);
+    ctx->part_arena.ensure(part_total + 1);
+    ctx->counter_arena.ensure(ne + 1, /*zero=*/true);
+    ctx->disp_arena.ensure(static_cast<size_t>(ne + 1) * kreg_dev::kMaxCandidates, /*zero=*/true);
+  }
+  for (int e = 0; e < ne; ++e) {
+    prepare_sweep(ctx, evals[e], ctx->h_sweep.ptr[e], scratch[e], e);
     ctx->h_sweep.ptr[e].out = ctx->d_results.ptr + static_cast<size_t>(e) * kreg_dev::kMaxCandidates * kreg_dev::kOut;
-    const long long est = std::max<long long>(evals[e].pairs->P, evals[e].pairs->expected_pairs);
-    max_nvb_est = std::max(max_nvb_est, est / kreg_dev::kPairsPerVBlock + 1);
+    max_nvb_est = std::max<long long>(max_nvb_est, static_cast<long long>(sweep_nvb_cap(evals[e])));
   }
   if (nb)
     KREG_CUDA(cudaMemcpyAsync(ctx->d_build.ptr, ctx->h_build.ptr, sizeof(kreg_dev::BuildReq) * nb,
@@ -402,27 +460,32 @@ void run_round(kreg_ctx* ctx, std::vector<BuildJob>& builds, std::vector<EvalJob
                               cudaMemcpyHostToDevice, ctx->stream));
   if (nb) kreg_dev::build_pairs_batched(ctx->h_build.ptr, ctx->d_build.ptr, nb, ctx->stream);
   if (ne) {
-    // ~6 resident sweep blocks per SM spread over the requests
-    const long long target = static_cast<long long>(ctx->sm_count) * 6;
-    int bpr = static_cast<int>(std::max<long long>(1, std::min<long long>(max_nvb_est, (target + ne - 1) / ne)));
+    // one physical block per work block (blocks beyond a request's work exit at once)
+    const int bpr = static_cast<int>(max_nvb_est);
     kreg_dev::sweep_batched(ctx->h_sweep.ptr, ctx->d_sweep.ptr, ne, bpr, ctx->stream,
                             ctx->profiling ? ctx->ev_sweep0 : nullptr, ctx->profiling ? ctx->ev_sweep1 : nullptr);
   }
   KREG_CUDA(cudaGetLastError());
   KREG_CUDA(cudaMemcpyAsync(ctx->h_results.ptr, ctx->d_results.ptr, sizeof(double) * n_res,
                             cudaMemcpyDeviceToHost, ctx->stream));
+  const auto t1 = clk::now();
   KREG_CUDA(cudaStreamSynchronize(ctx->stream));
+  const auto t2 = clk::now();
+  ctx->rounds += 1;
+  ctx->t_prepare += std::chrono::duration<double>(t1 - t0).count();
+  ctx->t_wait += std::chrono::duration<double>(t2 - t1).count();
 
   const double* res = ctx->h_results.ptr;
   std::vector<int> redo;
   for (int b = 0; b < nb; ++b) {
-    const double* st = res + static_cast<size_t>(ne) * kreg_dev::kMaxCandidates * kreg_dev::kOut + 2 * b;
+    const double* st = res + static_cast<size_t>(ne) * kreg_dev::kMaxCandidates * kreg_dev::kOut + 4 * b;
     builds[b].pairs->P = static_cast<long long>(st[0]);
+    builds[b].pairs->slots = static_cast<long long>(st[2]);
     if (st[1] != 0.0) {
-      builds[b].pairs->expected_pairs = static_cast<long long>(st[0] * 1.15) + 1024;
+      builds[b].pairs->expected_pairs = static_cast<long long>(st[2] * 1.15) + 1024;
       redo.push_back(b);
     } else {
-      builds[b].pairs->expected_pairs = std::max(builds[b].pairs->expected_pairs, builds[b].pairs->P);
+      builds[b].pairs->expected_pairs = std::max(builds[b].pairs->expected_pairs, builds[b].pairs->slots);
     }
   }
   if (!redo.empty()) {
@@ -470,12 +533,15 @@ void pairs_export(kreg_ctx* ctx, const kreg_pairs* p, int64_t* offsets, int32_t*
   // reference layout: CSR by ORIGINAL source index j, ascending ORIGINAL i
   const int nz = p->Z ? p->Z->n : 0;
   std::vector<long long> off(static_cast<size_t>(nz) + 1, 0);
-  std::vector<int2> pr(static_cast<size_t>(p->P));
+  std::vector<long long> toff(static_cast<size_t>(p->n_tiles) + 1, 0);
+  std::vector<int2> pr(static_cast<size_t>(p->slots));
   if (nz) {
     KREG_CUDA(cudaMemcpyAsync(off.data(), p->offsets.ptr, sizeof(long long) * (nz + 1), cudaMemcpyDeviceToHost,
                               ctx->stream));
-    if (p->P)
-      KREG_CUDA(cudaMemcpyAsync(pr.data(), p->pairs.ptr, sizeof(int2) * p->P, cudaMemcpyDeviceToHost, ctx->stream));
+    KREG_CUDA(cudaMemcpyAsync(toff.data(), p->tile_off.ptr, sizeof(long long) * (p->n_tiles + 1),
+                              cudaMemcpyDeviceToHost, ctx->stream));
+    if (p->slots)
+      KREG_CUDA(cudaMemcpyAsync(pr.data(), p->pairs.ptr, sizeof(int2) * p->slots, cudaMemcpyDeviceToHost, ctx->stream));
     KREG_CUDA(cudaStreamSynchronize(ctx->stream));
   }
   std::vector<long long> cnt(static_cast<size_t>(nz), 0);
@@ -486,10 +552,12 @@ void pairs_export(kreg_ctx* ctx, const kreg_pairs* p, int64_t* offsets, int32_t*
   for (int js = 0; js < nz; ++js) {
     const int j = p->Z->order[js];
     tmp.clear();
-    for (long long e = off[js]; e < off[js + 1]; ++e) {
+    const long long col = toff[static_cast<size_t>(js >> 5)] + (js & 31);  // sliced-ELL column of js
+    for (long long k = 0; k < off[js + 1] - off[js]; ++k) {
+      const int2 s = pr[static_cast<size_t>(col + 32 * k)];
       float lc;
-      std::memcpy(&lc, &pr[static_cast<size_t>(e)].y, sizeof(float));
-      tmp.push_back({p->X->order[pr[static_cast<size_t>(e)].x], std::exp2(static_cast<double>(lc))});
+      std::memcpy(&lc, &s.y, sizeof(float));
+      tmp.push_back({p->X->order[s.x], std::exp2(static_cast<double>(lc))});
     }
     std::sort(tmp.begin(), tmp.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
     long long at = offsets[j];

@@ -110,13 +110,25 @@ struct kreg_ctx {
   kreg_host::PinnedBuf<double> h_results;
   kreg_host::DevBuf<double> d_T2;
   kreg_host::DevBuf<unsigned long long> d_disp;
+  // per-round sweep scratch arenas (one slice per request)
+  kreg_host::DevBuf<int4> q_arena;
+  kreg_host::DevBuf<double> part_arena;
+  kreg_host::DevBuf<unsigned int> counter_arena;        // self-resetting, zero between rounds
+  kreg_host::DevBuf<unsigned long long> disp_arena;    // self-resetting, zero between rounds
+  // pair-list workspaces kept across registrations (device buffers keep capacity)
+  std::vector<kreg_pairs*> pool;
+  // host-side round accounting (seconds)
+  long long rounds = 0;
+  double t_prepare = 0.0, t_wait = 0.0, t_total = 0.0;
+  ~kreg_ctx();
 };
 
 struct kreg_cloud {
   kreg_ctx* ctx = nullptr;
   int n = 0;
   int dim = 0;
-  int fstride = 0;
+  int fstride = 0;                     // padded device row (floats)
+  std::vector<int> chan_off;           // padded channel offsets in a device row
   std::vector<kreg_host::ChannelInfo> schema;
   double diam = 0.0;
   double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
@@ -144,17 +156,14 @@ struct kreg_pairs {
   int gx = 0, gy = 0, gz = 0;
   kreg_host::DevBuf<int> cell_count, cell_start, cell_of, tmp_items, cell_items, count;
   kreg_host::DevBuf<double> cx, cy, cz;
-  kreg_host::DevBuf<long long> offsets, scan_tiles;
-  kreg_host::DevBuf<int2> pairs;
-  kreg_host::DevBuf<int> chunk_j, overflow;
+  kreg_host::DevBuf<long long> offsets, scan_tiles, tile_off;
+  kreg_host::DevBuf<int2> pairs;           // sliced-ELL slots
+  kreg_host::DevBuf<int> tile_deg, tile_slots, tile_units, unit_off, unit_tile;
+  int n_tiles = 0;
+  long long slots = 0;                     // valid after the build round
   kreg_host::DevBuf<int4> xq;
   double anchor[3] = {0, 0, 0};
   double qscale = 1.0;
-  // sweep scratch
-  kreg_host::DevBuf<int4> q;
-  kreg_host::DevBuf<double> partials;
-  kreg_host::DevBuf<unsigned int> counter;
-  kreg_host::DevBuf<unsigned long long> disp_bits;
   long long expected_pairs = 0;  // capacity hint
 };
 
@@ -200,5 +209,9 @@ void run_round(kreg_ctx* ctx, std::vector<BuildJob>& builds, std::vector<EvalJob
 double max_point_displacement_dev(kreg_ctx* ctx, const kreg_cloud* Z, const double* built, const double* now);
 
 void pairs_export(kreg_ctx* ctx, const kreg_pairs* p, int64_t* offsets, int32_t* x_index, double* coeff);
+
+// Workspace pool (ctx may be null: plain new/delete).
+kreg_pairs* acquire_workspace(kreg_ctx* ctx);
+void release_workspace(kreg_ctx* ctx, kreg_pairs* p);
 
 }  // namespace kreg_host

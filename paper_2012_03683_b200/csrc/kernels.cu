@@ -125,6 +125,8 @@ __global__ void k_rank(const BuildReq* reqs) {
 // --------------------------------------------------- batched exclusive scan
 // mode 0: cell_count (int32, n_cells) -> cell_start (int32, n_cells + 1)
 // mode 1: count      (int32, n_z)     -> offsets    (int64, n_z + 1)
+// mode 2: tile_slots (int32, n_tiles) -> tile_off   (int64, n_tiles + 1)
+// mode 3: tile_units (int32, n_tiles) -> unit_off   (int32, n_tiles + 1)
 struct ScanView {
   const int* in;
   long long n;
@@ -135,12 +137,18 @@ struct ScanView {
 
 __device__ __forceinline__ ScanView scan_view(const BuildReq& R, int mode) {
   ScanView v;
+  v.out32 = nullptr;
+  v.out64 = nullptr;
   if (mode == 0) {
-    v.in = R.cell_count; v.n = R.n_cells; v.out32 = R.cell_start; v.out64 = nullptr;
+    v.in = R.cell_count; v.n = R.n_cells; v.out32 = R.cell_start;
+  } else if (mode == 1) {
+    v.in = R.count; v.n = R.n_z; v.out64 = R.offsets;
+  } else if (mode == 2) {
+    v.in = R.tile_slots; v.n = R.n_tiles; v.out64 = R.tile_off;
   } else {
-    v.in = R.count; v.n = R.n_z; v.out32 = nullptr; v.out64 = R.offsets;
+    v.in = R.tile_units; v.n = R.n_tiles; v.out32 = R.unit_off;
   }
-  v.tiles = R.scan_tiles;
+  v.tiles = R.scan_tiles + (long long)mode * R.scan_stride;
   return v;
 }
 
@@ -174,13 +182,13 @@ __global__ void k_scan_tile_prefix(const BuildReq* reqs, int mode) {
     carry += tot;
   }
   if (threadIdx.x == 0) {
-    if (v.out32) {
-      v.out32[v.n] = (int)carry;
-    } else {
-      const BuildReq& R = reqs[blockIdx.x];
-      v.out64[v.n] = carry;
-      R.status[0] = (double)carry;
+    const BuildReq& R = reqs[blockIdx.x];
+    if (v.out32) v.out32[v.n] = (int)carry;
+    else v.out64[v.n] = carry;
+    if (mode == 1) R.status[0] = (double)carry;  // pairs
+    if (mode == 2) {                               // sliced-ELL slots (incl. padding)
       R.status[1] = carry > R.capacity ? 1.0 : 0.0;
+      R.status[2] = (double)carry;
     }
   }
 }
@@ -215,19 +223,34 @@ __global__ void k_scan_apply(const BuildReq* reqs, int mode) {
 // ------------------------------------------------------------------ K2
 // c_ij = prod_k (SE: s^2 exp(-|u-v|^2/(2l^2)) | linear: <u, v>)  (kernels.cpp:18-53),
 // FP32, exp on the MUFU pipe; returns log2(c) through *lc (c > 0 on accept).
+// Every channel starts on a 16-B boundary and is zero-padded to a multiple of
+// 4 floats (cloud upload), so rows stream as float4 and padding adds zero.
 __device__ __forceinline__ bool coefficient(const CoeffParams& cp, const float* __restrict__ u,
                                             const float* zf, float* lc) {
   float c = 1.0f;
   for (int k = 0; k < cp.n_channels; ++k) {
     const ChannelDev& ch = cp.ch[k];
+    const float4* u4 = reinterpret_cast<const float4*>(u + ch.offset);
+    const float4* z4 = reinterpret_cast<const float4*>(zf + ch.offset);
+    const int n4 = (ch.dim + 3) >> 2;
     float acc = 0.0f;
     if (ch.linear) {
-      for (int d = 0; d < ch.dim; ++d) acc = fmaf(__ldg(u + ch.offset + d), zf[ch.offset + d], acc);
+      for (int d = 0; d < n4; ++d) {
+        const float4 a = __ldg(u4 + d), b = z4[d];
+        acc = fmaf(a.x, b.x, acc);
+        acc = fmaf(a.y, b.y, acc);
+        acc = fmaf(a.z, b.z, acc);
+        acc = fmaf(a.w, b.w, acc);
+      }
       c *= acc;
     } else {
-      for (int d = 0; d < ch.dim; ++d) {
-        const float df = __ldg(u + ch.offset + d) - zf[ch.offset + d];
-        acc = fmaf(df, df, acc);
+      for (int d = 0; d < n4; ++d) {
+        const float4 a = __ldg(u4 + d), b = z4[d];
+        const float e0 = a.x - b.x, e1 = a.y - b.y, e2 = a.z - b.z, e3 = a.w - b.w;
+        acc = fmaf(e0, e0, acc);
+        acc = fmaf(e1, e1, acc);
+        acc = fmaf(e2, e2, acc);
+        acc = fmaf(e3, e3, acc);
       }
       c *= ch.sigma2 * ex2_approx(acc * ch.kappa);
     }
@@ -241,15 +264,16 @@ constexpr int kMaxFeat = 64;  // max padded feature row handled in registers/sme
 // One warp per source point j: 27-cell stencil = 9 contiguous x-rows of the
 // dense grid; lanes stride over candidates (coalesced FP64 loads), FP64
 // distance test (kernels.hpp:37-42, inner_product.cpp:69), c_ij, c > c_min.
-// EMIT=false writes count[j]; EMIT=true writes the pairs in stencil order and
-// the chunk -> j table.
+// EMIT=false writes count[j]; EMIT=true writes j's pairs in stencil order
+// into its sliced-ELL column: slot(k) = tile_off[j/32] + 32 k + (j%32), and
+// pads the column to the tile's max degree with {0, -inf} (w = 0).
 template <bool EMIT>
 __global__ void __launch_bounds__(256) k_pair_pass(const BuildReq* reqs) {
   const BuildReq& R = reqs[blockIdx.y];
   const int lane = threadIdx.x & 31;
   const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (j >= R.n_z) return;
-  __shared__ float zf_s[8][kMaxFeat];
+  __shared__ __align__(16) float zf_s[8][kMaxFeat];
   float* zf = zf_s[threadIdx.x >> 5];
   const int fs = R.cp.fstride;
   for (int d = lane; d < fs; d += 32) zf[d] = R.zfeat[(long long)j * fs + d];
@@ -263,8 +287,8 @@ __global__ void __launch_bounds__(256) k_pair_pass(const BuildReq* reqs) {
 
   long long out = 0;
   if (EMIT) {
-    out = R.offsets[j];
-    if (R.offsets[R.n_z] > R.capacity) return;  // host grows and re-runs
+    if (R.tile_off[R.n_tiles] > R.capacity) return;  // host grows and re-runs
+    out = R.tile_off[j >> 5] + (j & 31);
   }
   int cnt = 0;
   const bool geo = R.cp.n_channels == 0;
@@ -295,7 +319,7 @@ __global__ void __launch_bounds__(256) k_pair_pass(const BuildReq* reqs) {
           const unsigned m = __ballot_sync(0xffffffffu, keep);
           if (EMIT && keep) {
             const int pos = __popc(m & ((1u << lane) - 1u));
-            R.pairs[out + cnt + pos] = make_int2(i, __float_as_int(lc));
+            R.pairs[out + 32LL * (cnt + pos)] = make_int2(i, __float_as_int(lc));
           }
           cnt += __popc(m);
         }
@@ -305,11 +329,35 @@ __global__ void __launch_bounds__(256) k_pair_pass(const BuildReq* reqs) {
   if (!EMIT) {
     if (lane == 0) R.count[j] = cnt;
   } else {
-    // chunks whose first pair belongs to j
-    const long long e0 = out, e1 = out + cnt;
-    for (long long c = (e0 + kPairsPerChunk - 1) / kPairsPerChunk + lane; c * kPairsPerChunk < e1; c += 32)
-      R.chunk_j[c] = j;
+    // pad the column to the tile's max degree: w = ex2(-inf) = 0
+    const int dmax = R.tile_deg[j >> 5];
+    for (int k = cnt + lane; k < dmax; k += 32) R.pairs[out + 32LL * k] = make_int2(0, __float_as_int(-INFINITY));
   }
+}
+
+// Per tile of 32 consecutive sources: max degree, sliced-ELL slot count and
+// sweep work units (kUnitSteps degree steps each).
+__global__ void k_tile_sizes(const BuildReq* reqs) {
+  const BuildReq& R = reqs[blockIdx.y];
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int t = j >> 5;
+  if (t >= R.n_tiles) return;
+  int d = j < R.n_z ? R.count[j] : 0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) d = max(d, __shfl_xor_sync(0xffffffffu, d, o));
+  if ((threadIdx.x & 31) == 0) {
+    R.tile_deg[t] = d;
+    R.tile_slots[t] = 32 * d;
+    R.tile_units[t] = (d + kUnitSteps - 1) / kUnitSteps;
+  }
+}
+
+// unit -> tile table for the sweep
+__global__ void k_unit_tiles(const BuildReq* reqs) {
+  const BuildReq& R = reqs[blockIdx.y];
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= R.n_tiles || R.tile_off[R.n_tiles] > R.capacity) return;
+  for (int u = R.unit_off[t]; u < R.unit_off[t + 1]; ++u) R.unit_tile[u] = t;
 }
 
 // ------------------------------------------------------------------ K3
@@ -364,65 +412,95 @@ __device__ __forceinline__ double warp_sum_d(double v) {
   return v;
 }
 
-// Fused F + gradient sweep over the flattened pair list. Each thread owns one
-// chunk of E consecutive pairs (usually one or two source points j). Per pair
-// and candidate: d = x - q exactly in fixed point (IADD + FADD via the 1.5*2^23
-// magic), r^2, w = ex2(r^2 kappa + log2 c) on MUFU, W += w, S += w d. At every
-// change of j: torque += q_j x S_j (gw = sum_j q_j x S_j, since q x x =
-// q x (x - q)). Per virtual block (2048 pairs) the 7*M totals are reduced in
-// FP64 in a fixed order; the last block of a request reduces the virtual
-// block partials in a fixed order, so results are bitwise reproducible and
-// independent of the physical grid.
+// Fused F + gradient sweep over the sliced-ELL pair list. Work unit = one tile
+// of 32 consecutive sources x kUnitSteps degree steps: lane l owns source
+// j = 32 t + l, so per-j moments stay in registers, pair loads are coalesced
+// (slot = tile_off + 32 k + l) and the x gathers of neighbouring sources hit
+// the same lines. Units are cut into nblk = ceil(U / kUnitsPerBlock) work
+// blocks (a function of the pair list only, so results do not depend on the
+// physical grid or on batch composition); warp w of a work block takes units
+// w, w+8, ... Per pair and candidate: d = x - q exactly in fixed point (IADD +
+// FADD via the 1.5*2^23 magic), r^2, w = ex2(r^2 kappa + log2 c) on MUFU,
+// W += w, S += w d; per unit: torque += q_j x S_j (gw = sum_j q_j x S_j since
+// q x x = q x (x - q)). The 7*M totals of a work block are reduced in FP64 in
+// a fixed order; the last block of a request reduces the work-block partials
+// in a fixed order.
+__device__ __forceinline__ long long sweep_work_blocks(long long units) {
+  const long long b = (units + kUnitsPerBlock - 1) / kUnitsPerBlock;
+  return b < 1 ? 1 : (b > kMaxSweepBlocks ? kMaxSweepBlocks : b);
+}
+
+// kUnitSteps degree steps of one sliced-ELL column (lane = source j) for M
+// candidate transforms: loads first (8 coalesced slots, 8 x gathers), then
+// per candidate d = x - q (exact, fixed point), w = ex2(r^2 kappa + log2 c).
+template <int MAXM, bool FULL>
+__device__ __forceinline__ void sweep_steps(const int2* __restrict__ col, int nk, const int4* __restrict__ xq,
+                                            const int4 (&qv)[MAXM], int M, float kappa, float (&W)[MAXM],
+                                            float (&Sx)[MAXM], float (&Sy)[MAXM], float (&Sz)[MAXM]) {
+  int2 pr[kUnitSteps];
+#pragma unroll
+  for (int k = 0; k < kUnitSteps; ++k) pr[k] = (FULL || k < nk) ? __ldg(col + 32 * k) : make_int2(0, 0);
+  int4 xv[kUnitSteps];
+#pragma unroll
+  for (int k = 0; k < kUnitSteps; ++k) xv[k] = (FULL || k < nk) ? __ldg(xq + pr[k].x) : make_int4(0, 0, 0, 0);
+#pragma unroll
+  for (int m = 0; m < MAXM; ++m) {
+    if (m < M) {
+#pragma unroll
+      for (int k = 0; k < kUnitSteps; ++k) {
+        if (FULL || k < nk) {
+          const float dx = __int_as_float((unsigned)xv[k].x + (unsigned)qv[m].x) - 12582912.0f;
+          const float dy = __int_as_float((unsigned)xv[k].y + (unsigned)qv[m].y) - 12582912.0f;
+          const float dz = __int_as_float((unsigned)xv[k].z + (unsigned)qv[m].z) - 12582912.0f;
+          const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+          const float w = ex2_approx(fmaf(r2, kappa, __int_as_float(pr[k].y)));
+          W[m] += w;
+          Sx[m] = fmaf(w, dx, Sx[m]);
+          Sy[m] = fmaf(w, dy, Sy[m]);
+          Sz[m] = fmaf(w, dz, Sz[m]);
+        }
+      }
+    }
+  }
+}
 template <int MAXM>
 __global__ void __launch_bounds__(kSweepThreads) k_sweep(const SweepReq* reqs) {
   const SweepReq& R = reqs[blockIdx.y];
   const int M = R.M;
-  long long P = R.offsets[R.n_z];
-  if (P > R.capacity) P = 0;  // overflowed build: result discarded by the host
-  const long long n_chunks = (P + kPairsPerChunk - 1) / kPairsPerChunk;
-  const long long nvb = (n_chunks + kSweepThreads - 1) / kSweepThreads;
+  // an overflowed build is skipped (its result is discarded by the host)
+  const long long U = R.tile_off[R.n_tiles] <= R.capacity ? (long long)R.unit_off[R.n_tiles] : 0;
+  const long long nblk = sweep_work_blocks(U);
+  const long long upb = (U + nblk - 1) / nblk;
   const float kappa = R.kappa;
   __shared__ double red[kSweepThreads / 32][MAXM * 7];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 
-  for (long long vb = blockIdx.x; vb < nvb; vb += gridDim.x) {
+  if (blockIdx.x < nblk) {
     float acc[MAXM][7];
 #pragma unroll
     for (int m = 0; m < MAXM; ++m)
 #pragma unroll
       for (int c = 0; c < 7; ++c) acc[m][c] = 0.0f;
 
-    const long long chunk = vb * kSweepThreads + threadIdx.x;
-    if (chunk < n_chunks) {
-      const long long e0 = chunk * kPairsPerChunk;
-      const int ne = (int)min((long long)kPairsPerChunk, P - e0);
-      int j = R.chunk_j[chunk];
-      long long jend = R.offsets[j + 1];
-      // pairs of this chunk: 64 B, 16-B aligned vector loads
-      int2 pr[kPairsPerChunk];
-      if (ne == kPairsPerChunk) {
-        const int4* p4 = reinterpret_cast<const int4*>(R.pairs + e0);
+    const long long u0 = blockIdx.x * upb;
+    const long long u1 = min(U, u0 + upb);
+    // warp w takes a contiguous unit range, so consecutive units mostly share
+    // a tile: per-source moments and q stay in registers across them
+    const long long upw = (upb + kSweepThreads / 32 - 1) / (kSweepThreads / 32);
+    const long long wu0 = min(u1, u0 + wid * upw);
+    const long long wu1 = min(u1, wu0 + upw);
+    int t = -1, deg = 0, ubase = 0;
+    bool active = false;
+    long long col0 = 0;
+    int4 qv[MAXM];
+    float W[MAXM], Sx[MAXM], Sy[MAXM], Sz[MAXM];
 #pragma unroll
-        for (int k = 0; k < kPairsPerChunk / 2; ++k) {
-          const int4 v = __ldg(p4 + k);
-          pr[2 * k] = make_int2(v.x, v.y);
-          pr[2 * k + 1] = make_int2(v.z, v.w);
-        }
-      } else {
-#pragma unroll
-        for (int k = 0; k < kPairsPerChunk; ++k) pr[k] = k < ne ? __ldg(R.pairs + e0 + k) : make_int2(0, 0);
-      }
-      int4 xv[kPairsPerChunk];
-#pragma unroll
-      for (int k = 0; k < kPairsPerChunk; ++k) xv[k] = k < ne ? __ldg(R.xq + pr[k].x) : make_int4(0, 0, 0, 0);
-
-      int4 qv[MAXM];
-      float W[MAXM], Sx[MAXM], Sy[MAXM], Sz[MAXM];
-#pragma unroll
-      for (int m = 0; m < MAXM; ++m) {
-        qv[m] = m < M ? __ldg(R.q + (long long)m * R.n_z + j) : make_int4(0, 0, 0, 0);
-        W[m] = Sx[m] = Sy[m] = Sz[m] = 0.0f;
-      }
-      auto flush = [&]() {
+    for (int m = 0; m < MAXM; ++m) {
+      qv[m] = make_int4(0, 0, 0, 0);
+      W[m] = Sx[m] = Sy[m] = Sz[m] = 0.0f;
+    }
+    auto flush_tile = [&]() {
+      if (active) {
 #pragma unroll
         for (int m = 0; m < MAXM; ++m) {
           if (m < M) {
@@ -437,44 +515,37 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(const SweepReq* reqs) {
             acc[m][5] += qz * Sx[m] - qx * Sz[m];
             acc[m][6] += qx * Sy[m] - qy * Sx[m];
           }
-          W[m] = Sx[m] = Sy[m] = Sz[m] = 0.0f;
-        }
-      };
-#pragma unroll
-      for (int k = 0; k < kPairsPerChunk; ++k) {
-        if (k < ne) {
-          const long long e = e0 + k;
-          if (e >= jend) {
-            flush();
-            do {
-              ++j;
-              jend = R.offsets[j + 1];
-            } while (e >= jend);
-#pragma unroll
-            for (int m = 0; m < MAXM; ++m)
-              if (m < M) qv[m] = __ldg(R.q + (long long)m * R.n_z + j);
-          }
-          const float lc = __int_as_float(pr[k].y);
-#pragma unroll
-          for (int m = 0; m < MAXM; ++m) {
-            if (m < M) {
-              const float dx = __int_as_float((unsigned)xv[k].x + (unsigned)qv[m].x) - 12582912.0f;
-              const float dy = __int_as_float((unsigned)xv[k].y + (unsigned)qv[m].y) - 12582912.0f;
-              const float dz = __int_as_float((unsigned)xv[k].z + (unsigned)qv[m].z) - 12582912.0f;
-              const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-              const float w = ex2_approx(fmaf(r2, kappa, lc));
-              W[m] += w;
-              Sx[m] = fmaf(w, dx, Sx[m]);
-              Sy[m] = fmaf(w, dy, Sy[m]);
-              Sz[m] = fmaf(w, dz, Sz[m]);
-            }
-          }
         }
       }
-      flush();
+#pragma unroll
+      for (int m = 0; m < MAXM; ++m) W[m] = Sx[m] = Sy[m] = Sz[m] = 0.0f;
+    };
+    for (long long u = wu0; u < wu1; ++u) {
+      const int tu = R.unit_tile[u];
+      if (tu != t) {
+        flush_tile();
+        t = tu;
+        const int j = t * 32 + lane;
+        active = j < R.n_z;
+        col0 = R.tile_off[t] + lane;
+        deg = R.tile_deg[t];
+        ubase = R.unit_off[t];
+#pragma unroll
+        for (int m = 0; m < MAXM; ++m)
+          qv[m] = (m < M && active) ? __ldg(R.q + (long long)m * R.n_z + j) : make_int4(0, 0, 0, 0);
+      }
+      if (!active) continue;  // only lanes past n_z in the last tile
+      const int k0 = (int)(u - ubase) * kUnitSteps;
+      const int nk = min(kUnitSteps, deg - k0);
+      const int2* col = R.pairs + col0 + 32LL * k0;
+      if (nk == kUnitSteps) {
+        sweep_steps<MAXM, true>(col, kUnitSteps, R.xq, qv, M, kappa, W, Sx, Sy, Sz);
+      } else {
+        sweep_steps<MAXM, false>(col, nk, R.xq, qv, M, kappa, W, Sx, Sy, Sz);
+      }
     }
+    flush_tile();
     // deterministic block reduction in FP64
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
     for (int m = 0; m < MAXM; ++m) {
       if (m < M) {
@@ -489,23 +560,19 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(const SweepReq* reqs) {
     if (threadIdx.x < M * 7) {
       double s = 0.0;
       for (int w = 0; w < kSweepThreads / 32; ++w) s += red[w][threadIdx.x];
-      R.partials[vb * (M * 7) + threadIdx.x] = s;
+      R.partials[blockIdx.x * (M * 7) + threadIdx.x] = s;
+      __threadfence();
     }
-    __syncthreads();
   }
-
-  // last physical block of this request reduces the virtual-block partials
+  // last physical block of this request reduces the work-block partials
   __shared__ bool is_last;
-  __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) is_last = atomicAdd(R.counter, 1u) == gridDim.x - 1;
   __syncthreads();
   if (!is_last) return;
-  __threadfence();
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  // thread t sums a contiguous range of virtual blocks, then fixed-order tree
-  const long long per = (nvb + kSweepThreads - 1) / kSweepThreads;
-  const long long b0 = threadIdx.x * per, b1 = min(nvb, b0 + per);
+  // thread t sums a contiguous range of work blocks, then fixed-order tree
+  const long long per = (nblk + kSweepThreads - 1) / kSweepThreads;
+  const long long b0 = threadIdx.x * per, b1 = min(nblk, b0 + per);
   for (int m = 0; m < M; ++m) {
     double v[7] = {0, 0, 0, 0, 0, 0, 0};
     for (long long b = b0; b < b1; ++b)
@@ -591,12 +658,19 @@ void build_pairs_batched(const BuildReq* h, const BuildReq* d, int n, cudaStream
   k_rank<<<gx, T, 0, st>>>(d);
   const dim3 gz(max(1, (max_nz + 7) / 8), n);
   k_pair_pass<false><<<gz, 256, 0, st>>>(d);
-  const long long z_tiles = (max_nz + kScanTile - 1) / kScanTile;
-  k_scan_tiles<<<dim3((unsigned)max(1LL, z_tiles), n), kScanThreads, 0, st>>>(d, 1);
+  const unsigned z_tiles = (unsigned)max(1, (max_nz + kScanTile - 1) / kScanTile);
+  k_scan_tiles<<<dim3(z_tiles, n), kScanThreads, 0, st>>>(d, 1);
   k_scan_tile_prefix<<<n, 1024, 0, st>>>(d, 1);
-  k_scan_apply<<<dim3((unsigned)max(1LL, z_tiles), n), kScanThreads, 0, st>>>(d, 1);
+  k_scan_apply<<<dim3(z_tiles, n), kScanThreads, 0, st>>>(d, 1);
+  k_tile_sizes<<<dim3(max(1, (max_nz + 255) / 256), n), 256, 0, st>>>(d);
+  for (int mode = 2; mode <= 3; ++mode) {
+    k_scan_tiles<<<dim3(z_tiles, n), kScanThreads, 0, st>>>(d, mode);
+    k_scan_tile_prefix<<<n, 1024, 0, st>>>(d, mode);
+    k_scan_apply<<<dim3(z_tiles, n), kScanThreads, 0, st>>>(d, mode);
+  }
   k_pair_pass<true><<<gz, 256, 0, st>>>(d);
-  count_launch(11);
+  k_unit_tiles<<<dim3(max(1, (max_nz / 32 + 256) / 256), n), 256, 0, st>>>(d);
+  count_launch(19);
 }
 
 void sweep_batched(const SweepReq* h, const SweepReq* d, int n, int blocks_per_req, cudaStream_t st,

@@ -47,6 +47,30 @@ double anneal_step(double lengthscale, const double* hist, int n, const kreg_reg
   return decayed >= c.min_lengthscale ? decayed : lengthscale;
 }
 
+kreg_pairs* acquire_workspace(kreg_ctx* ctx) {
+  kreg_pairs* p = nullptr;
+  if (ctx && !ctx->pool.empty()) {
+    p = ctx->pool.back();
+    ctx->pool.pop_back();
+  } else {
+    p = new kreg_pairs;
+  }
+  p->ctx = ctx;
+  p->X = p->Z = nullptr;
+  p->built_at_lengthscale = 0.0;
+  p->cutoff_radius = 0.0;
+  p->P = 0;
+  return p;
+}
+
+void release_workspace(kreg_ctx* ctx, kreg_pairs* p) {
+  if (ctx && ctx->pool.size() < 512) {
+    ctx->pool.push_back(p);
+  } else {
+    delete p;
+  }
+}
+
 namespace {
 
 int env_int(const char* name, int dflt) {
@@ -59,13 +83,29 @@ struct Memo {
   double out[kreg_dev::kOut];
 };
 
+// Pair-list workspace borrowed from the context pool for one registration.
+struct WsHandle {
+  kreg_ctx* ctx = nullptr;
+  kreg_pairs* p = nullptr;
+  WsHandle() = default;
+  WsHandle(const WsHandle&) = delete;
+  WsHandle& operator=(const WsHandle&) = delete;
+  ~WsHandle() { reset(); }
+  kreg_pairs* get() const { return p; }
+  kreg_pairs* operator->() const { return p; }
+  void reset() {
+    if (p) release_workspace(ctx, p);
+    p = nullptr;
+  }
+};
+
 enum class Phase { kInit, kStartIter, kAwaitEval, kSearchSetup, kSearch, kAwaitCandidates, kDone };
 
 struct Reg {
   RegJob* job = nullptr;
   kreg_registration_config cfg{};
   Params wp;
-  std::unique_ptr<kreg_pairs> pairs;
+  WsHandle pairs;
   double v_scale = 1.0, denom = 1.0;
   double lengthscale = 0.0;
   double T[12];
@@ -407,8 +447,9 @@ void register_many(kreg_ctx* ctx, std::vector<RegJob>& jobs) {
     r->wp.lengthscale = r->lengthscale;
     std::memcpy(r->T, j.initial, sizeof(r->T));
     for (double& d : r->dir) d = 0.0;
-    r->pairs = std::make_unique<kreg_pairs>();
-    r->pairs->expected_pairs = j.expected_pairs;
+    r->pairs.ctx = ctx;
+    r->pairs.p = acquire_workspace(ctx);
+    if (j.expected_pairs > 0) r->pairs->expected_pairs = j.expected_pairs;
     if (j.X->n == 0 || j.Z->n == 0) {
       // empty cloud: build_pairs yields an empty list -> NoOverlapError
       char msg[160];
