@@ -159,6 +159,10 @@ kreg_status kreg_ctx_set_profiling(kreg_ctx* ctx, int32_t enabled);
 /* Host-side round accounting: {rounds, s preparing + launching, s waiting for
  * the device, reserved}. */
 kreg_status kreg_ctx_host_stats(const kreg_ctx* ctx, double out[4]);
+/* All counters: {sweep kernel ms (profiling on), sweep launches, pair-evals
+ * (pairs x candidates), pairs streamed (sum of P per sweep request),
+ * sliced-ELL slots streamed, rounds, s preparing, s waiting}. */
+kreg_status kreg_ctx_stats(const kreg_ctx* ctx, double out[8]);
 kreg_status kreg_ctx_reset_stats(kreg_ctx* ctx);
 
 /* Upload a cloud into device SoA (replaces constructing kreg::PointCloud,
@@ -175,6 +179,9 @@ kreg_status kreg_build_pairs(kreg_ctx* ctx, const kreg_cloud* X, const kreg_clou
                              int64_t* n_pairs);
 kreg_status kreg_pairs_destroy(kreg_pairs* pairs);
 int64_t kreg_pairs_size(const kreg_pairs* pairs);
+/* Device layout statistics: {pairs, sliced-ELL slots incl. padding, tiles,
+ * grid cells}. */
+kreg_status kreg_pairs_info(const kreg_pairs* pairs, int64_t out[4]);
 /* Copy the pair list out in the reference's layout (inner_product.hpp:18-32):
  * CSR grouped by source j (offsets[n_z+1]), target i ascending inside a group,
  * coeff per entry. Debug / parity path. */
@@ -244,6 +251,13 @@ kreg_status kreg_register_batch(kreg_ctx* ctx, int32_t n, const kreg_cloud* cons
                                 const kreg_kernel_params* params,
                                 const kreg_registration_config* config,
                                 kreg_registration_result* results, int32_t* statuses);
+/* End-to-end throughput mode: host views in (uploaded inside the call),
+ * results out; same semantics as kreg_register_batch. */
+kreg_status kreg_register_batch_host(kreg_ctx* ctx, int32_t n, const kreg_cloud_view* X,
+                                     const kreg_cloud_view* Z, const double* initials,
+                                     const kreg_kernel_params* params,
+                                     const kreg_registration_config* config,
+                                     kreg_registration_result* results, int32_t* statuses);
 /* reference registration.hpp:99-100 register_sequence. */
 kreg_status kreg_register_sequence(kreg_ctx* ctx, const kreg_cloud* const* frames,
                                    int32_t n_frames, const kreg_kernel_params* params,

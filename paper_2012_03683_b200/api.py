@@ -21,7 +21,7 @@ from .types import (Isometry, KernelParams, PointCloud, RegistrationConfig, Regi
                     SequenceBuffers, SequenceResult, raise_for)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libkreg_b200.so")
+LIB_PATH = os.environ.get("KREG_LIB") or os.path.join(_HERE, "libkreg_b200.so")
 
 _lib = None
 _lib_lock = threading.Lock()
@@ -54,6 +54,7 @@ def lib():
         L.kreg_ctx_sweep_stats.argtypes = [P, _abi.dptr, _abi.i64ptr, _abi.i64ptr]
         L.kreg_ctx_set_profiling.argtypes = [P, C.c_int32]
         L.kreg_ctx_host_stats.argtypes = [P, _abi.dptr]
+        L.kreg_ctx_stats.argtypes = [P, _abi.dptr]
         L.kreg_ctx_reset_stats.argtypes = [P]
         L.kreg_cloud_create.argtypes = [P, VP, C.POINTER(P)]
         L.kreg_cloud_destroy.argtypes = [P]
@@ -63,6 +64,7 @@ def lib():
         L.kreg_pairs_size.argtypes = [P]
         L.kreg_pairs_size.restype = C.c_int64
         L.kreg_pairs_export.argtypes = [P, P, _abi.i64ptr, _abi.i32ptr, _abi.dptr]
+        L.kreg_pairs_info.argtypes = [P, _abi.i64ptr]
         L.kreg_inner_product.argtypes = [P, P, P, P, _abi.dptr, KP, _abi.dptr]
         L.kreg_objective_and_gradient.argtypes = [P, P, P, P, _abi.dptr, KP, _abi.dptr]
         L.kreg_eval_transforms.argtypes = [P, P, P, P, _abi.dptr, C.c_int32, KP, C.c_uint32, _abi.dptr]
@@ -76,6 +78,7 @@ def lib():
         L.kreg_register_clouds.argtypes = [P, P, P, _abi.dptr, KP, CP, RP]
         L.kreg_register_clouds_host.argtypes = [P, VP, VP, _abi.dptr, KP, CP, RP]
         L.kreg_register_batch.argtypes = [P, C.c_int32, C.POINTER(P), C.POINTER(P), _abi.dptr, KP, CP, RP, _abi.i32ptr]
+        L.kreg_register_batch_host.argtypes = [P, C.c_int32, VP, VP, _abi.dptr, KP, CP, RP, _abi.i32ptr]
         L.kreg_register_sequence.argtypes = [P, C.POINTER(P), C.c_int32, KP, CP, C.POINTER(_abi.kreg_sequence_result)]
         L.kreg_register_sequence_chains.argtypes = [P, C.POINTER(P), C.c_int32, C.c_int32, KP, CP,
                                                     C.POINTER(_abi.kreg_sequence_result)]
@@ -136,11 +139,10 @@ class Context:
         return {"rounds": int(out[0]), "t_prepare_s": float(out[1]), "t_wait_s": float(out[2])}
 
     def sweep_stats(self):
-        ms = np.zeros(1)
-        n = np.zeros(2, dtype=np.int64)
-        _check(lib().kreg_ctx_sweep_stats(self.h, _abi.as_ptr(ms), _abi.as_ptr(n[:1], C.c_int64),
-                                          _abi.as_ptr(n[1:], C.c_int64)))
-        return {"sweep_ms": float(ms[0]), "sweep_rounds": int(n[0]), "pair_evals": int(n[1])}
+        o = np.zeros(8)
+        _check(lib().kreg_ctx_stats(self.h, _abi.as_ptr(o)))
+        return {"sweep_ms": float(o[0]), "sweep_rounds": int(o[1]), "pair_evals": int(o[2]),
+                "pairs_streamed": int(o[3]), "slots_streamed": int(o[4]), "rounds": int(o[5])}
 
 
 _default_ctx = None
@@ -204,6 +206,12 @@ class PairList:
 
     def empty(self) -> bool:
         return self.n == 0
+
+    def info(self) -> dict:
+        """Device layout: pairs, sliced-ELL slots (incl. padding), tiles, grid cells."""
+        out = np.zeros(4, dtype=np.int64)
+        _check(lib().kreg_pairs_info(self.h, _abi.as_ptr(out, C.c_int64)))
+        return {"pairs": int(out[0]), "slots": int(out[1]), "tiles": int(out[2]), "cells": int(out[3])}
 
     def export(self):
         """(offsets, x_index, coeff) in the reference layout."""
@@ -352,6 +360,29 @@ def register_batch(Xs, Zs, initials, params: KernelParams, config: RegistrationC
     cfg = config.cstruct()
     _check(lib().kreg_register_batch(ctx.h, n, xh, zh, _abi.as_ptr(inits), params.cstruct(), C.byref(cfg), res,
                                      _abi.as_ptr(st, C.c_int32)))
+    out = []
+    for k in range(n):
+        bufs[k].struct = res[k]
+        out.append(RegistrationResult.from_buffers(bufs[k]) if st[k] == 0 else None)
+    return out, st[:n].copy()
+
+
+def register_batch_host(Xs, Zs, initials, params: KernelParams, config: RegistrationConfig, ctx=None,
+                        trace_capacity: int | None = None):
+    """End-to-end throughput call: host clouds in (uploaded inside the call).
+    Returns (results, statuses)."""
+    ctx = ctx or default_context()
+    n = len(Xs)
+    xv = (_abi.kreg_cloud_view * max(n, 1))(*[x.view() for x in Xs])
+    zv = (_abi.kreg_cloud_view * max(n, 1))(*[z.view() for z in Zs])
+    inits = np.ascontiguousarray(np.stack([T.as12() if isinstance(T, Isometry) else np.asarray(T, np.float64).reshape(12)
+                                           for T in initials])) if n else np.zeros((0, 12))
+    bufs = [_abi.TraceBuffers(trace_capacity or config.max_iterations) for _ in range(n)]
+    res = (_abi.kreg_registration_result * max(n, 1))(*[b.struct for b in bufs])
+    st = np.zeros(max(n, 1), dtype=np.int32)
+    cfg = config.cstruct()
+    _check(lib().kreg_register_batch_host(ctx.h, n, xv, zv, _abi.as_ptr(inits), params.cstruct(), C.byref(cfg), res,
+                                          _abi.as_ptr(st, C.c_int32)))
     out = []
     for k in range(n):
         bufs[k].struct = res[k]

@@ -35,20 +35,23 @@ def _stale(target: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
-    os.makedirs(OBJ_DIR, exist_ok=True)
+def build(verbose: bool = False, force: bool = False, defines=(), lib: str = LIB, obj_dir: str = OBJ_DIR) -> str:
+    """Compile and link; `defines` (e.g. ["KREG_UNIT_STEPS=4"]) select kernel
+    variants for A/B measurements (written to `lib` / `obj_dir`)."""
+    os.makedirs(obj_dir, exist_ok=True)
+    extra = ["-D" + d for d in defines]
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".hpp", ".cuh", ".h"))]
     headers.append(os.path.join(ROOT, "include", "kreg_b200.h"))
     nvcc = _nvcc()
     objs = []
     for src in SOURCES:
         path = os.path.join(CSRC, src)
-        obj = os.path.join(OBJ_DIR, src + ".o")
+        obj = os.path.join(obj_dir, src + ".o")
         objs.append(obj)
         if force or _stale(obj, [path] + headers):
-            cmd = [nvcc, *ARCH, *NVCC_FLAGS, "-x", "cu" if src.endswith(".cu") else "c++", "-c", path, "-o", obj]
+            cmd = [nvcc, *ARCH, *NVCC_FLAGS, *extra, "-x", "cu" if src.endswith(".cu") else "c++", "-c", path, "-o", obj]
             if src.endswith(".cpp"):
-                cmd = [nvcc, *NVCC_FLAGS, "-x", "c++", "-c", path, "-o", obj]
+                cmd = [nvcc, *NVCC_FLAGS, *extra, "-x", "c++", "-c", path, "-o", obj]
             r = subprocess.run(cmd, capture_output=True, text=True)
             if verbose or r.returncode != 0:
                 sys.stderr.write(r.stdout + r.stderr)
@@ -56,13 +59,20 @@ def build(verbose: bool = False, force: bool = False) -> str:
                 raise RuntimeError(f"nvcc failed on {src}")
             with open(obj + ".log", "w") as f:
                 f.write(r.stdout + r.stderr)
-    if force or _stale(LIB, objs):
-        cmd = [nvcc, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart"]
+    if force or _stale(lib, objs):
+        cmd = [nvcc, *ARCH, "-shared", "-o", lib, *objs, "-lcudart"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError("link failed")
-    return LIB
+    return lib
+
+
+def build_variant(name: str, defines) -> str:
+    """Experimental kernel variant: paper_2012_03683_b200/_variants/<name>.so."""
+    vdir = os.path.join(HERE, "_variants")
+    return build(force=False, defines=defines, lib=os.path.join(vdir, name + ".so"),
+                 obj_dir=os.path.join(vdir, name + "_obj"))
 
 
 if __name__ == "__main__":

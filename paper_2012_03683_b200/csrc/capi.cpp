@@ -252,6 +252,19 @@ kreg_status kreg_ctx_host_stats(const kreg_ctx* ctx, double out[4]) {
   });
 }
 
+kreg_status kreg_ctx_stats(const kreg_ctx* ctx, double out[8]) {
+  return guarded([&] {
+    out[0] = ctx->sweep_ms;
+    out[1] = static_cast<double>(ctx->sweep_launches);
+    out[2] = static_cast<double>(ctx->pair_evals);
+    out[3] = static_cast<double>(ctx->pairs_streamed);
+    out[4] = static_cast<double>(ctx->slots_streamed);
+    out[5] = static_cast<double>(ctx->rounds);
+    out[6] = ctx->t_prepare;
+    out[7] = ctx->t_wait;
+  });
+}
+
 kreg_status kreg_ctx_set_profiling(kreg_ctx* ctx, int32_t enabled) {
   return guarded([&] { ctx->profiling = enabled != 0; });
 }
@@ -261,6 +274,8 @@ kreg_status kreg_ctx_reset_stats(kreg_ctx* ctx) {
     ctx->sweep_ms = 0.0;
     ctx->sweep_launches = 0;
     ctx->pair_evals = 0;
+    ctx->pairs_streamed = 0;
+    ctx->slots_streamed = 0;
     ctx->rounds = 0;
     ctx->t_prepare = ctx->t_wait = ctx->t_total = 0.0;
     ctx->launches_base = kreg_dev::kernel_launch_count();
@@ -296,6 +311,16 @@ kreg_status kreg_pairs_destroy(kreg_pairs* pairs) {
 }
 
 int64_t kreg_pairs_size(const kreg_pairs* pairs) { return pairs ? pairs->P : 0; }
+
+kreg_status kreg_pairs_info(const kreg_pairs* pairs, int64_t out[4]) {
+  return guarded([&] {
+    require(pairs && out, "NULL argument");
+    out[0] = pairs->P;
+    out[1] = pairs->slots;
+    out[2] = pairs->n_tiles;
+    out[3] = pairs->n_cells;
+  });
+}
 
 kreg_status kreg_pairs_export(kreg_ctx* ctx, const kreg_pairs* pairs, int64_t* offsets, int32_t* x_index,
                               double* coeff) {
@@ -488,6 +513,26 @@ kreg_status kreg_register_batch(kreg_ctx* ctx, int32_t n, const kreg_cloud* cons
     require(ctx && (n == 0 || (X && Z && initials && results && statuses)), "NULL argument");
     std::vector<RegJob> jobs(static_cast<size_t>(n));
     for (int k = 0; k < n; ++k) make_jobs(X[k], Z[k], initials + 12 * k, params, config, &results[k], jobs[k]);
+    register_many(ctx, jobs);
+    for (int k = 0; k < n; ++k) statuses[k] = jobs[k].status;
+  });
+}
+
+kreg_status kreg_register_batch_host(kreg_ctx* ctx, int32_t n, const kreg_cloud_view* X, const kreg_cloud_view* Z,
+                                     const double* initials, const kreg_kernel_params* params,
+                                     const kreg_registration_config* config, kreg_registration_result* results,
+                                     int32_t* statuses) {
+  return guarded([&] {
+    require(ctx && (n == 0 || (X && Z && initials && results && statuses)), "NULL argument");
+    std::vector<std::unique_ptr<kreg_cloud>> clouds;
+    std::vector<RegJob> jobs(static_cast<size_t>(n));
+    for (int k = 0; k < n; ++k) {
+      clouds.emplace_back(cloud_create(ctx, &X[k]));
+      const kreg_cloud* cx = clouds.back().get();
+      clouds.emplace_back(cloud_create(ctx, &Z[k]));
+      const kreg_cloud* cz = clouds.back().get();
+      make_jobs(cx, cz, initials + 12 * k, params, config, &results[k], jobs[k]);
+    }
     register_many(ctx, jobs);
     for (int k = 0; k < n; ++k) statuses[k] = jobs[k].status;
   });

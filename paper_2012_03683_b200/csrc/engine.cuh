@@ -26,8 +26,22 @@
 namespace kreg_dev {
 
 constexpr int kSweepThreads = 256;  // threads per (virtual) sweep block
-constexpr int kUnitSteps = 8;          // degree steps per sweep work unit (x 32 lanes)
-constexpr long long kUnitsPerBlock = 32;  // work units per sweep work block (4 per warp)
+#ifndef KREG_UNIT_STEPS
+#define KREG_UNIT_STEPS 8
+#endif
+#ifndef KREG_UNITS_PER_BLOCK
+#define KREG_UNITS_PER_BLOCK 32
+#endif
+#ifndef KREG_SWEEP_MIN_BLOCKS
+#define KREG_SWEEP_MIN_BLOCKS 1
+#endif
+constexpr int kUnitSteps = KREG_UNIT_STEPS;              // degree steps per sweep work unit (x 32 lanes)
+constexpr long long kUnitsPerBlock = KREG_UNITS_PER_BLOCK;  // work units per sweep work block
+constexpr int kSweepMinBlocks = KREG_SWEEP_MIN_BLOCKS;    // __launch_bounds__ occupancy hint
+#ifndef KREG_SWEEP_STAGES
+#define KREG_SWEEP_STAGES 4
+#endif
+constexpr int kSweepStages = KREG_SWEEP_STAGES;  // per-warp TMA ring depth (units in flight)
 constexpr long long kMaxSweepBlocks = 1184;  // 8 x 148 SMs
 constexpr int kMaxChannels = 8;
 constexpr int kMaxCandidates = 8;   // candidate transforms per sweep request
@@ -87,7 +101,8 @@ struct BuildReq {
 };
 
 // One sweep request: M candidate transforms against one pair list.
-struct SweepReq {
+struct alignas(16) SweepReq {
+  long long units;       // sweep work units when known on the host, else -1
   const long long* tile_off;
   const int* unit_off;
   const int* unit_tile;

@@ -264,6 +264,7 @@ static void prepare_build(kreg_ctx* ctx, BuildJob& job, kreg_dev::BuildReq& R) {
   p->cutoff_radius = job.cutoff_multiplier * job.params.lengthscale;
   p->c_min = job.c_min;
   p->sigma = job.params.sigma;
+  p->counts_valid = false;  // until this round's results are read back
   std::memcpy(p->T_build, job.T, sizeof(p->T_build));
 
   std::memset(&R, 0, sizeof(R));
@@ -388,6 +389,8 @@ static void prepare_sweep(kreg_ctx* ctx, EvalJob& job, kreg_dev::SweepReq& R, co
   kreg_pairs* p = job.pairs;
   std::memset(&R, 0, sizeof(R));
   const int nz = p->Z->n;
+  // every sweep unit is exactly 32 * kUnitSteps slots (k_tile_sizes)
+  R.units = p->counts_valid ? p->slots / (32LL * kreg_dev::kUnitSteps) : -1;
   R.tile_off = p->tile_off.ptr;
   R.unit_off = p->unit_off.ptr;
   R.unit_tile = p->unit_tile.ptr;
@@ -481,6 +484,7 @@ void run_round(kreg_ctx* ctx, std::vector<BuildJob>& builds, std::vector<EvalJob
     const double* st = res + static_cast<size_t>(ne) * kreg_dev::kMaxCandidates * kreg_dev::kOut + 4 * b;
     builds[b].pairs->P = static_cast<long long>(st[0]);
     builds[b].pairs->slots = static_cast<long long>(st[2]);
+    builds[b].pairs->counts_valid = st[1] == 0.0;
     if (st[1] != 0.0) {
       builds[b].pairs->expected_pairs = static_cast<long long>(st[2] * 1.15) + 1024;
       redo.push_back(b);
@@ -499,6 +503,8 @@ void run_round(kreg_ctx* ctx, std::vector<BuildJob>& builds, std::vector<EvalJob
     std::memcpy(evals[e].out, res + static_cast<size_t>(e) * kreg_dev::kMaxCandidates * kreg_dev::kOut,
                 sizeof(double) * kreg_dev::kOut * evals[e].M);
     ctx->pair_evals += evals[e].pairs->P * evals[e].M;
+    ctx->pairs_streamed += evals[e].pairs->P;
+    ctx->slots_streamed += evals[e].pairs->slots;
   }
   if (ne) {
     ctx->sweep_launches += 1;

@@ -100,6 +100,8 @@ struct kreg_ctx {
   double sweep_ms = 0.0;
   long long sweep_launches = 0;
   long long pair_evals = 0;
+  long long pairs_streamed = 0;
+  long long slots_streamed = 0;
   long long launches_base = 0;
   // round staging
   kreg_host::DevBuf<kreg_dev::BuildReq> d_build;
@@ -161,6 +163,7 @@ struct kreg_pairs {
   kreg_host::DevBuf<int> tile_deg, tile_slots, tile_units, unit_off, unit_tile;
   int n_tiles = 0;
   long long slots = 0;                     // valid after the build round
+  bool counts_valid = false;               // P / slots known on the host
   kreg_host::DevBuf<int4> xq;
   double anchor[3] = {0, 0, 0};
   double qscale = 1.0;

@@ -335,8 +335,11 @@ __global__ void __launch_bounds__(256) k_pair_pass(const BuildReq* reqs) {
   }
 }
 
-// Per tile of 32 consecutive sources: max degree, sliced-ELL slot count and
-// sweep work units (kUnitSteps degree steps each).
+// Per tile of 32 consecutive sources: column height = max degree rounded up
+// to a whole number of sweep units (kUnitSteps degree steps; >= 1 unit so
+// the sweep also visits isolated sources for their displacement). Every unit
+// is then exactly 32 * kUnitSteps contiguous slots: unit u = slots
+// [u * 32 kUnitSteps, (u + 1) * 32 kUnitSteps).
 __global__ void k_tile_sizes(const BuildReq* reqs) {
   const BuildReq& R = reqs[blockIdx.y];
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
@@ -346,9 +349,10 @@ __global__ void k_tile_sizes(const BuildReq* reqs) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) d = max(d, __shfl_xor_sync(0xffffffffu, d, o));
   if ((threadIdx.x & 31) == 0) {
-    R.tile_deg[t] = d;
-    R.tile_slots[t] = 32 * d;
-    R.tile_units[t] = (d + kUnitSteps - 1) / kUnitSteps;
+    const int units = d > 0 ? (d + kUnitSteps - 1) / kUnitSteps : 1;
+    R.tile_deg[t] = units * kUnitSteps;
+    R.tile_slots[t] = 32 * kUnitSteps * units;
+    R.tile_units[t] = units;
   }
 }
 
@@ -361,49 +365,31 @@ __global__ void k_unit_tiles(const BuildReq* reqs) {
 }
 
 // ------------------------------------------------------------------ K3
-// q = T_m z_j in FP64 -> (magic - fixed point) per candidate; fused max
-// displacement |T_m z - T_b z| (inner_product.cpp:238-246).
-__global__ void k_transform_sources(const SweepReq* reqs) {
-  const SweepReq& R = reqs[blockIdx.y];
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  const bool valid = j < R.n_z;
-  double zx = 0, zy = 0, zz = 0;
-  if (valid) {
-    zx = R.zx[j];
-    zy = R.zy[j];
-    zz = R.zz[j];
-  }
-  double bx, by, bz;
-  apply_T(R.Tb, zx, zy, zz, bx, by, bz);
-  const double lim = 536870912.0;  // 2^29 units; X lies within 2^28 of the anchor
-  __shared__ unsigned long long warp_max[32];
-  for (int m = 0; m < R.M; ++m) {
-    double qx, qy, qz;
-    apply_T(R.T[m], zx, zy, zz, qx, qy, qz);
-    if (valid) {
-      const double fx = fmin(fmax((qx - R.anchor[0]) * R.qscale, -lim), lim);
-      const double fy = fmin(fmax((qy - R.anchor[1]) * R.qscale, -lim), lim);
-      const double fz = fmin(fmax((qz - R.anchor[2]) * R.qscale, -lim), lim);
-      R.q[(long long)m * R.n_z + j] =
-          make_int4((int)(kMagic - (unsigned)__double2int_rn(fx)), (int)(kMagic - (unsigned)__double2int_rn(fy)),
-                    (int)(kMagic - (unsigned)__double2int_rn(fz)), 0);
-    }
-    const double dx = qx - bx, dy = qy - by, dz = qz - bz;
-    unsigned long long d2 = valid ? (unsigned long long)__double_as_longlong(dx * dx + dy * dy + dz * dz) : 0ull;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const unsigned long long other = __shfl_down_sync(0xffffffffu, d2, o);
-      d2 = other > d2 ? other : d2;
-    }
-    if ((threadIdx.x & 31) == 0) warp_max[threadIdx.x >> 5] = d2;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      unsigned long long mx = 0;
-      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) mx = warp_max[w] > mx ? warp_max[w] : mx;
-      if (mx) atomicMax(&R.disp_bits[m], mx);
-    }
-    __syncthreads();
-  }
+// Packed FP32 pairs (sm_100 FFMA2/FADD2/FMUL2): candidate transforms are
+// processed two at a time, one per half of a 64-bit register pair.
+typedef unsigned long long f2_t;
+__device__ __forceinline__ f2_t pk2(float a, float b) {
+  f2_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void upk2(f2_t r, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+__device__ __forceinline__ f2_t fma2(f2_t a, f2_t b, f2_t c) {
+  f2_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ f2_t add2(f2_t a, f2_t b) {
+  f2_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f2_t mul2(f2_t a, f2_t b) {
+  f2_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
 }
 
 __device__ __forceinline__ double warp_sum_d(double v) {
@@ -412,155 +398,264 @@ __device__ __forceinline__ double warp_sum_d(double v) {
   return v;
 }
 
-// Fused F + gradient sweep over the sliced-ELL pair list. Work unit = one tile
-// of 32 consecutive sources x kUnitSteps degree steps: lane l owns source
-// j = 32 t + l, so per-j moments stay in registers, pair loads are coalesced
-// (slot = tile_off + 32 k + l) and the x gathers of neighbouring sources hit
-// the same lines. Units are cut into nblk = ceil(U / kUnitsPerBlock) work
-// blocks (a function of the pair list only, so results do not depend on the
-// physical grid or on batch composition); warp w of a work block takes units
-// w, w+8, ... Per pair and candidate: d = x - q exactly in fixed point (IADD +
-// FADD via the 1.5*2^23 magic), r^2, w = ex2(r^2 kappa + log2 c) on MUFU,
-// W += w, S += w d; per unit: torque += q_j x S_j (gw = sum_j q_j x S_j since
-// q x x = q x (x - q)). The 7*M totals of a work block are reduced in FP64 in
-// a fixed order; the last block of a request reduces the work-block partials
-// in a fixed order.
+// Fused F + gradient + displacement sweep over the sliced-ELL pair list.
+//  * Work unit = one tile of 32 consecutive sources x kUnitSteps degree steps;
+//    lane l owns source j = 32 t + l: per-j moments stay in registers, pair
+//    slots (tile_off + 32 k + l) load coalesced, and the x gathers of
+//    neighbouring sources (Morton order) hit the same lines.
+//  * At every tile change a lane computes q = T_m z_j in FP64 for all M
+//    candidates -> fixed point (kept as magic - q), and the displacement
+//    |T_m z_j - T_b z_j| (inner_product.cpp:238-246); every tile has >= 1 unit.
+//  * Per slot and candidate: d = x - q exactly (IADD + FADD with the 1.5*2^23
+//    magic), r^2, w = ex2(r^2 kappa + log2 c) on MUFU, W += w, S += w d;
+//    candidates run in pairs on FFMA2/FADD2/FMUL2. Per tile: torque +=
+//    q_j x S_j (gw = sum_j q_j x S_j since q x x = q x (x - q)).
+//  * Units are cut into nblk = ceil(U / kUnitsPerBlock) work blocks, a function
+//    of the pair list only; warp w of a work block takes a contiguous unit
+//    range. Work-block totals are reduced in FP64 in a fixed order and the
+//    last block of the request reduces the work-block partials in a fixed
+//    order: bitwise reproducible, independent of grid and batch composition.
 __device__ __forceinline__ long long sweep_work_blocks(long long units) {
   const long long b = (units + kUnitsPerBlock - 1) / kUnitsPerBlock;
   return b < 1 ? 1 : (b > kMaxSweepBlocks ? kMaxSweepBlocks : b);
 }
 
-// kUnitSteps degree steps of one sliced-ELL column (lane = source j) for M
-// candidate transforms: loads first (8 coalesced slots, 8 x gathers), then
-// per candidate d = x - q (exact, fixed point), w = ex2(r^2 kappa + log2 c).
-template <int MAXM, bool FULL>
-__device__ __forceinline__ void sweep_steps(const int2* __restrict__ col, int nk, const int4* __restrict__ xq,
-                                            const int4 (&qv)[MAXM], int M, float kappa, float (&W)[MAXM],
-                                            float (&Sx)[MAXM], float (&Sy)[MAXM], float (&Sz)[MAXM]) {
-  int2 pr[kUnitSteps];
-#pragma unroll
-  for (int k = 0; k < kUnitSteps; ++k) pr[k] = (FULL || k < nk) ? __ldg(col + 32 * k) : make_int2(0, 0);
+// TMA (bulk async copy) + mbarrier helpers: each warp streams its sweep units
+// (32 * kUnitSteps contiguous 8-B slots = 2 KB each) through a private ring of
+// kSweepStages shared-memory stages, so DRAM/L2 latency of the pair stream is
+// hidden behind the x gathers and math of earlier units.
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "KREG_WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra KREG_WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+constexpr int kUnitSlots = 32 * kUnitSteps;
+constexpr unsigned kStageBytes = kUnitSlots * sizeof(int2);
+constexpr size_t kSweepSmem = (size_t)(kSweepThreads / 32) * kSweepStages * kStageBytes +
+                              (size_t)(kSweepThreads / 32) * kSweepStages * sizeof(unsigned long long);
+
+// One unit of one sliced-ELL column (lane = source j) for M candidates: the
+// unit's slots come from shared memory, the x gathers go to L1/L2, then per
+// candidate pair d = x - q (exact, fixed point), w = ex2(r^2 kappa + log2 c).
+template <int NP>
+__device__ __forceinline__ void sweep_unit(const int2 (&pr)[kUnitSteps], const int4* __restrict__ xq,
+                                           const int (&qx)[2 * NP], const int (&qy)[2 * NP],
+                                           const int (&qz)[2 * NP], f2_t kap2, f2_t (&W)[NP], f2_t (&Sx)[NP],
+                                           f2_t (&Sy)[NP], f2_t (&Sz)[NP]) {
   int4 xv[kUnitSteps];
 #pragma unroll
-  for (int k = 0; k < kUnitSteps; ++k) xv[k] = (FULL || k < nk) ? __ldg(xq + pr[k].x) : make_int4(0, 0, 0, 0);
+  for (int k = 0; k < kUnitSteps; ++k) xv[k] = __ldg(xq + pr[k].x);
+  const f2_t nmag = pk2(-12582912.0f, -12582912.0f);
 #pragma unroll
-  for (int m = 0; m < MAXM; ++m) {
-    if (m < M) {
+  for (int k = 0; k < kUnitSteps; ++k) {
+    const float lc = __int_as_float(pr[k].y);
+    const f2_t lc2 = pk2(lc, lc);
 #pragma unroll
-      for (int k = 0; k < kUnitSteps; ++k) {
-        if (FULL || k < nk) {
-          const float dx = __int_as_float((unsigned)xv[k].x + (unsigned)qv[m].x) - 12582912.0f;
-          const float dy = __int_as_float((unsigned)xv[k].y + (unsigned)qv[m].y) - 12582912.0f;
-          const float dz = __int_as_float((unsigned)xv[k].z + (unsigned)qv[m].z) - 12582912.0f;
-          const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-          const float w = ex2_approx(fmaf(r2, kappa, __int_as_float(pr[k].y)));
-          W[m] += w;
-          Sx[m] = fmaf(w, dx, Sx[m]);
-          Sy[m] = fmaf(w, dy, Sy[m]);
-          Sz[m] = fmaf(w, dz, Sz[m]);
-        }
-      }
+    for (int p = 0; p < NP; ++p) {
+      const int a = 2 * p, b = 2 * p + 1;
+      const f2_t dx = add2(pk2(__int_as_float(xv[k].x + qx[a]), __int_as_float(xv[k].x + qx[b])), nmag);
+      const f2_t dy = add2(pk2(__int_as_float(xv[k].y + qy[a]), __int_as_float(xv[k].y + qy[b])), nmag);
+      const f2_t dz = add2(pk2(__int_as_float(xv[k].z + qz[a]), __int_as_float(xv[k].z + qz[b])), nmag);
+      const f2_t r2 = fma2(dz, dz, fma2(dy, dy, mul2(dx, dx)));
+      float e0, e1;
+      upk2(fma2(r2, kap2, lc2), e0, e1);
+      const f2_t w = pk2(ex2_approx(e0), ex2_approx(e1));
+      W[p] = add2(W[p], w);
+      Sx[p] = fma2(w, dx, Sx[p]);
+      Sy[p] = fma2(w, dy, Sy[p]);
+      Sz[p] = fma2(w, dz, Sz[p]);
     }
   }
 }
-template <int MAXM>
-__global__ void __launch_bounds__(kSweepThreads) k_sweep(const SweepReq* reqs) {
-  const SweepReq& R = reqs[blockIdx.y];
+
+template <int NP>
+__global__ void __launch_bounds__(kSweepThreads, kSweepMinBlocks) k_sweep(const SweepReq* reqs) {
+  constexpr int MAXM = 2 * NP;
+  constexpr int NW = kSweepThreads / 32;
+  // the request descriptor (~1 KB) is staged in shared memory once per block
+  __shared__ __align__(16) SweepReq Rs;
+  {
+    const int4* g = reinterpret_cast<const int4*>(reqs + blockIdx.y);
+    int4* s = reinterpret_cast<int4*>(&Rs);
+    for (int k = threadIdx.x; k < (int)(sizeof(SweepReq) / 16); k += blockDim.x) s[k] = g[k];
+  }
+  __syncthreads();
+  const SweepReq& R = Rs;
   const int M = R.M;
-  // an overflowed build is skipped (its result is discarded by the host)
-  const long long U = R.tile_off[R.n_tiles] <= R.capacity ? (long long)R.unit_off[R.n_tiles] : 0;
+  // an overflowed build is skipped (its result is discarded by the host);
+  // the unit count is passed by the host when the pair list was built earlier
+  long long U = R.units;
+  if (U < 0) U = R.tile_off[R.n_tiles] <= R.capacity ? (long long)R.unit_off[R.n_tiles] : 0;
   const long long nblk = sweep_work_blocks(U);
   const long long upb = (U + nblk - 1) / nblk;
-  const float kappa = R.kappa;
-  __shared__ double red[kSweepThreads / 32][MAXM * 7];
+  const f2_t kap2 = pk2(R.kappa, R.kappa);
+  __shared__ double red[NW][MAXM * 7];
+  __shared__ unsigned long long dred[NW][MAXM];
+  extern __shared__ __align__(128) unsigned char dyn_smem[];
+  int2* ring_all = reinterpret_cast<int2*>(dyn_smem);
+  unsigned long long* bar_all =
+      reinterpret_cast<unsigned long long*>(dyn_smem + (size_t)NW * kSweepStages * kStageBytes);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (threadIdx.x < NW * kSweepStages) mbar_init(&bar_all[threadIdx.x], 1);
+  mbar_fence_init();
+  __syncthreads();
 
   if (blockIdx.x < nblk) {
-    float acc[MAXM][7];
+    f2_t acc[NP][7];
+    unsigned long long dmax[MAXM];
 #pragma unroll
-    for (int m = 0; m < MAXM; ++m)
+    for (int p = 0; p < NP; ++p)
 #pragma unroll
-      for (int c = 0; c < 7; ++c) acc[m][c] = 0.0f;
+      for (int c = 0; c < 7; ++c) acc[p][c] = 0ull;
+#pragma unroll
+    for (int m = 0; m < MAXM; ++m) dmax[m] = 0ull;
 
     const long long u0 = blockIdx.x * upb;
     const long long u1 = min(U, u0 + upb);
-    // warp w takes a contiguous unit range, so consecutive units mostly share
-    // a tile: per-source moments and q stay in registers across them
-    const long long upw = (upb + kSweepThreads / 32 - 1) / (kSweepThreads / 32);
+    const long long upw = (upb + NW - 1) / NW;
     const long long wu0 = min(u1, u0 + wid * upw);
-    const long long wu1 = min(u1, wu0 + upw);
-    int t = -1, deg = 0, ubase = 0;
-    bool active = false;
-    long long col0 = 0;
-    int4 qv[MAXM];
-    float W[MAXM], Sx[MAXM], Sy[MAXM], Sz[MAXM];
-#pragma unroll
-    for (int m = 0; m < MAXM; ++m) {
-      qv[m] = make_int4(0, 0, 0, 0);
-      W[m] = Sx[m] = Sy[m] = Sz[m] = 0.0f;
+    const int nunits = (int)(min(u1, wu0 + upw) - wu0);
+    int2* ring = ring_all + (size_t)wid * kSweepStages * kUnitSlots;
+    unsigned long long* bars = bar_all + wid * kSweepStages;
+    const int2* src = R.pairs + wu0 * kUnitSlots;
+    if (lane == 0) {
+      for (int s = 0; s < kSweepStages && s < nunits; ++s) {
+        mbar_expect_tx(&bars[s], kStageBytes);
+        tma_load_1d(ring + s * kUnitSlots, src + (long long)s * kUnitSlots, kStageBytes, &bars[s]);
+      }
     }
+
+    int t = -1;
+    bool active = false;
+    int qx[MAXM], qy[MAXM], qz[MAXM];
+    f2_t W[NP], Sx[NP], Sy[NP], Sz[NP];
+#pragma unroll
+    for (int m = 0; m < MAXM; ++m) qx[m] = qy[m] = qz[m] = (int)kMagic;
+#pragma unroll
+    for (int p = 0; p < NP; ++p) W[p] = Sx[p] = Sy[p] = Sz[p] = 0ull;
+
     auto flush_tile = [&]() {
       if (active) {
 #pragma unroll
-        for (int m = 0; m < MAXM; ++m) {
-          if (m < M) {
-            const float qx = (float)(int)(kMagic - (unsigned)qv[m].x);
-            const float qy = (float)(int)(kMagic - (unsigned)qv[m].y);
-            const float qz = (float)(int)(kMagic - (unsigned)qv[m].z);
-            acc[m][0] += W[m];
-            acc[m][1] += Sx[m];
-            acc[m][2] += Sy[m];
-            acc[m][3] += Sz[m];
-            acc[m][4] += qy * Sz[m] - qz * Sy[m];
-            acc[m][5] += qz * Sx[m] - qx * Sz[m];
-            acc[m][6] += qx * Sy[m] - qy * Sx[m];
-          }
+        for (int p = 0; p < NP; ++p) {
+          const f2_t fqx = pk2((float)(int)(kMagic - (unsigned)qx[2 * p]), (float)(int)(kMagic - (unsigned)qx[2 * p + 1]));
+          const f2_t fqy = pk2((float)(int)(kMagic - (unsigned)qy[2 * p]), (float)(int)(kMagic - (unsigned)qy[2 * p + 1]));
+          const f2_t fqz = pk2((float)(int)(kMagic - (unsigned)qz[2 * p]), (float)(int)(kMagic - (unsigned)qz[2 * p + 1]));
+          const f2_t neg = pk2(-1.0f, -1.0f);
+          acc[p][0] = add2(acc[p][0], W[p]);
+          acc[p][1] = add2(acc[p][1], Sx[p]);
+          acc[p][2] = add2(acc[p][2], Sy[p]);
+          acc[p][3] = add2(acc[p][3], Sz[p]);
+          acc[p][4] = add2(acc[p][4], fma2(mul2(neg, fqz), Sy[p], mul2(fqy, Sz[p])));
+          acc[p][5] = add2(acc[p][5], fma2(mul2(neg, fqx), Sz[p], mul2(fqz, Sx[p])));
+          acc[p][6] = add2(acc[p][6], fma2(mul2(neg, fqy), Sx[p], mul2(fqx, Sy[p])));
         }
       }
 #pragma unroll
-      for (int m = 0; m < MAXM; ++m) W[m] = Sx[m] = Sy[m] = Sz[m] = 0.0f;
+      for (int p = 0; p < NP; ++p) W[p] = Sx[p] = Sy[p] = Sz[p] = 0ull;
     };
-    for (long long u = wu0; u < wu1; ++u) {
-      const int tu = R.unit_tile[u];
+
+    int tiles32 = 0;  // unit -> tile for 32 units at a time, one load per lane
+    for (int i = 0; i < nunits; ++i) {
+      if ((i & 31) == 0) tiles32 = (i + lane < nunits) ? R.unit_tile[wu0 + i + lane] : 0;
+      const int tu = __shfl_sync(0xffffffffu, tiles32, i & 31);
       if (tu != t) {
         flush_tile();
         t = tu;
         const int j = t * 32 + lane;
         active = j < R.n_z;
-        col0 = R.tile_off[t] + lane;
-        deg = R.tile_deg[t];
-        ubase = R.unit_off[t];
+        if (active) {
+          const double zx = R.zx[j], zy = R.zy[j], zz = R.zz[j];
+          double bx, by, bz;
+          apply_T(R.Tb, zx, zy, zz, bx, by, bz);
+          const double lim = 536870912.0;  // 2^29 units; X lies within 2^28 of the anchor
 #pragma unroll
-        for (int m = 0; m < MAXM; ++m)
-          qv[m] = (m < M && active) ? __ldg(R.q + (long long)m * R.n_z + j) : make_int4(0, 0, 0, 0);
-      }
-      if (!active) continue;  // only lanes past n_z in the last tile
-      const int k0 = (int)(u - ubase) * kUnitSteps;
-      const int nk = min(kUnitSteps, deg - k0);
-      const int2* col = R.pairs + col0 + 32LL * k0;
-      if (nk == kUnitSteps) {
-        sweep_steps<MAXM, true>(col, kUnitSteps, R.xq, qv, M, kappa, W, Sx, Sy, Sz);
-      } else {
-        sweep_steps<MAXM, false>(col, nk, R.xq, qv, M, kappa, W, Sx, Sy, Sz);
-      }
-    }
-    flush_tile();
-    // deterministic block reduction in FP64
-#pragma unroll
-    for (int m = 0; m < MAXM; ++m) {
-      if (m < M) {
-#pragma unroll
-        for (int c = 0; c < 7; ++c) {
-          const double s = warp_sum_d((double)acc[m][c]);
-          if (lane == 0) red[wid][m * 7 + c] = s;
+          for (int m = 0; m < MAXM; ++m) {
+            const int mm = m < M ? m : 0;  // padding candidates repeat candidate 0
+            double x, y, z;
+            apply_T(R.T[mm], zx, zy, zz, x, y, z);
+            const double dx = x - bx, dy = y - by, dz = z - bz;
+            const unsigned long long d2 = (unsigned long long)__double_as_longlong(dx * dx + dy * dy + dz * dz);
+            dmax[m] = d2 > dmax[m] ? d2 : dmax[m];
+            qx[m] = (int)(kMagic - (unsigned)__double2int_rn(fmin(fmax((x - R.anchor[0]) * R.qscale, -lim), lim)));
+            qy[m] = (int)(kMagic - (unsigned)__double2int_rn(fmin(fmax((y - R.anchor[1]) * R.qscale, -lim), lim)));
+            qz[m] = (int)(kMagic - (unsigned)__double2int_rn(fmin(fmax((z - R.anchor[2]) * R.qscale, -lim), lim)));
+          }
         }
       }
+      const int s = i % kSweepStages;
+      mbar_wait(&bars[s], (unsigned)((i / kSweepStages) & 1));
+      int2 pr[kUnitSteps];
+#pragma unroll
+      for (int k = 0; k < kUnitSteps; ++k) pr[k] = ring[s * kUnitSlots + 32 * k + lane];
+      __syncwarp();
+      if (lane == 0 && i + kSweepStages < nunits) {  // refill this stage with unit i + stages
+        fence_proxy_async();
+        mbar_expect_tx(&bars[s], kStageBytes);
+        tma_load_1d(ring + s * kUnitSlots, src + (long long)(i + kSweepStages) * kUnitSlots, kStageBytes, &bars[s]);
+      }
+      if (active) sweep_unit<NP>(pr, R.xq, qx, qy, qz, kap2, W, Sx, Sy, Sz);
+    }
+    flush_tile();
+
+    // deterministic block reduction in FP64; displacement max
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+#pragma unroll
+      for (int c = 0; c < 7; ++c) {
+        float a0, a1;
+        upk2(acc[p][c], a0, a1);
+        const double s0 = warp_sum_d((double)a0);
+        const double s1 = warp_sum_d((double)a1);
+        if (lane == 0) {
+          red[wid][(2 * p) * 7 + c] = s0;
+          red[wid][(2 * p + 1) * 7 + c] = s1;
+        }
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < MAXM; ++m) {
+      unsigned long long d = dmax[m];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long other = __shfl_down_sync(0xffffffffu, d, o);
+        d = other > d ? other : d;
+      }
+      if (lane == 0) dred[wid][m] = d;
     }
     __syncthreads();
     if (threadIdx.x < M * 7) {
       double s = 0.0;
       for (int w = 0; w < kSweepThreads / 32; ++w) s += red[w][threadIdx.x];
       R.partials[blockIdx.x * (M * 7) + threadIdx.x] = s;
+      __threadfence();
+    } else if (threadIdx.x >= 64 && threadIdx.x < 64 + M) {
+      const int m = threadIdx.x - 64;
+      unsigned long long d = 0;
+      for (int w = 0; w < kSweepThreads / 32; ++w) d = dred[w][m] > d ? dred[w][m] : d;
+      if (d) atomicMax(&R.disp_bits[m], d);
       __threadfence();
     }
   }
@@ -676,20 +771,22 @@ void build_pairs_batched(const BuildReq* h, const BuildReq* d, int n, cudaStream
 void sweep_batched(const SweepReq* h, const SweepReq* d, int n, int blocks_per_req, cudaStream_t st,
                    cudaEvent_t ev0, cudaEvent_t ev1) {
   if (n == 0) return;
-  int max_nz = 1, max_m = 1;
-  for (int r = 0; r < n; ++r) {
-    max_nz = max(max_nz, h[r].n_z);
-    max_m = max(max_m, h[r].M);
+  int max_m = 1;
+  for (int r = 0; r < n; ++r) max_m = max(max_m, h[r].M);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_sweep<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepSmem);
+    cudaFuncSetAttribute(k_sweep<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepSmem);
+    cudaFuncSetAttribute(k_sweep<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepSmem);
+    attr_set = true;
   }
-  k_transform_sources<<<dim3((max_nz + 255) / 256, n), 256, 0, st>>>(d);
   if (ev0) cudaEventRecord(ev0, st);
   const dim3 g(blocks_per_req, n);
-  if (max_m <= 1) k_sweep<1><<<g, kSweepThreads, 0, st>>>(d);
-  else if (max_m <= 2) k_sweep<2><<<g, kSweepThreads, 0, st>>>(d);
-  else if (max_m <= 4) k_sweep<4><<<g, kSweepThreads, 0, st>>>(d);
-  else k_sweep<8><<<g, kSweepThreads, 0, st>>>(d);
+  if (max_m <= 2) k_sweep<1><<<g, kSweepThreads, kSweepSmem, st>>>(d);
+  else if (max_m <= 4) k_sweep<2><<<g, kSweepThreads, kSweepSmem, st>>>(d);
+  else k_sweep<4><<<g, kSweepThreads, kSweepSmem, st>>>(d);
   if (ev1) cudaEventRecord(ev1, st);
-  count_launch(2);
+  count_launch(1);
 }
 
 void displacement(const double* zx, const double* zy, const double* zz, int n, const double* d_T2,

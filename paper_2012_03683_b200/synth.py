@@ -229,17 +229,26 @@ class _Scene:
     def add_box(self, lo, hi, rgb, cls, freq=1.0):
         self.boxes.append((np.asarray(lo, float), np.asarray(hi, float), np.asarray(rgb, float), cls, freq))
 
-    def raycast(self, origin, dirs):
-        """Nearest hit along each ray (world frame). Returns t, primitive id."""
+    def raycast(self, origin, dirs, forward=None, depth_range=(0.0, np.inf)):
+        """Nearest hit along each ray (world frame). Returns t, primitive id.
+        Boxes entirely outside depth_range along `forward` are culled."""
         n = dirs.shape[0]
         best_t = np.full(n, np.inf)
         best_id = np.full(n, -1, dtype=np.int64)
         inv = 1.0 / np.where(np.abs(dirs) < 1e-12, 1e-12, dirs)
+        ix, iy, iz = (np.ascontiguousarray(inv[:, k]) for k in range(3))
         for b, (lo, hi, _, _, _) in enumerate(self.boxes):
-            t1 = (lo - origin) * inv
-            t2 = (hi - origin) * inv
-            tmin = np.max(np.minimum(t1, t2), axis=1)
-            tmax = np.min(np.maximum(t1, t2), axis=1)
+            if forward is not None:
+                corners = np.array([[x, y, z] for x in (lo[0], hi[0]) for y in (lo[1], hi[1]) for z in (lo[2], hi[2])])
+                depth = (corners - origin) @ forward
+                if depth.max() < depth_range[0] or depth.min() > depth_range[1]:
+                    continue
+            # slab test per axis on contiguous columns (same arithmetic as before)
+            ax = (lo[0] - origin[0]) * ix, (hi[0] - origin[0]) * ix
+            ay = (lo[1] - origin[1]) * iy, (hi[1] - origin[1]) * iy
+            az = (lo[2] - origin[2]) * iz, (hi[2] - origin[2]) * iz
+            tmin = np.maximum(np.maximum(np.minimum(*ax), np.minimum(*ay)), np.minimum(*az))
+            tmax = np.minimum(np.minimum(np.maximum(*ax), np.maximum(*ay)), np.maximum(*az))
             t = np.where(tmin > 1e-6, tmin, tmax)  # camera inside the box → exit face
             hit = (tmax >= np.maximum(tmin, 1e-6)) & (t > 1e-6) & (t < best_t)
             best_t = np.where(hit, t, best_t)
@@ -322,7 +331,7 @@ def _render(scene: _Scene, pose: Isometry, intr: dict, n_points: int, depth_nois
         v = rng.uniform(intr["skip_top"], intr["height"], m)
         d_cam = np.stack([(u - cx) / fx, (v - cy) / fy, np.ones(m)], axis=1)
         d_w = d_cam @ pose.rotation.T
-        t, ids = scene.raycast(pose.translation, d_w)
+        t, ids = scene.raycast(pose.translation, d_w, pose.rotation[:, 2], (0.0, intr["max_depth"]))
         z = t  # depth along the optical axis (d_cam.z = 1)
         ok = np.isfinite(t) & (z >= intr["min_depth"]) & (z <= intr["max_depth"])
         z = z[ok]
