@@ -156,9 +156,13 @@ int64_t kreg_ctx_kernel_launches(const kreg_ctx* ctx);
 kreg_status kreg_ctx_sweep_stats(const kreg_ctx* ctx, double* sweep_ms, int64_t* sweep_launches,
                                  int64_t* pair_evals);
 kreg_status kreg_ctx_set_profiling(kreg_ctx* ctx, int32_t enabled);
+/* Throughput mode: at most `n` registrations in flight at once (0 = all);
+ * a finished registration is replaced by the next one immediately. */
+kreg_status kreg_ctx_set_max_active(kreg_ctx* ctx, int32_t n);
 /* Host-side round accounting: {rounds, s preparing + launching, s waiting for
- * the device, reserved}. */
-kreg_status kreg_ctx_host_stats(const kreg_ctx* ctx, double out[4]);
+ * the device, s preparing builds, s preparing sweeps, s in the solver state
+ * machines, device allocations so far (process), bytes allocated}. */
+kreg_status kreg_ctx_host_stats(const kreg_ctx* ctx, double out[8]);
 /* All counters: {sweep kernel ms (profiling on), sweep launches, pair-evals
  * (pairs x candidates), pairs streamed (sum of P per sweep request),
  * sliced-ELL slots streamed, rounds, s preparing, s waiting}. */

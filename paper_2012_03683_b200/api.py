@@ -53,6 +53,7 @@ def lib():
         L.kreg_ctx_kernel_launches.restype = C.c_int64
         L.kreg_ctx_sweep_stats.argtypes = [P, _abi.dptr, _abi.i64ptr, _abi.i64ptr]
         L.kreg_ctx_set_profiling.argtypes = [P, C.c_int32]
+        L.kreg_ctx_set_max_active.argtypes = [P, C.c_int32]
         L.kreg_ctx_host_stats.argtypes = [P, _abi.dptr]
         L.kreg_ctx_stats.argtypes = [P, _abi.dptr]
         L.kreg_ctx_reset_stats.argtypes = [P]
@@ -133,10 +134,16 @@ class Context:
     def reset_stats(self):
         _check(lib().kreg_ctx_reset_stats(self.h))
 
+    def set_max_active(self, n: int):
+        """Lockstep window of register_batch (0 = all registrations at once)."""
+        _check(lib().kreg_ctx_set_max_active(self.h, int(n)))
+
     def host_stats(self):
-        out = np.zeros(4)
+        out = np.zeros(8)
         _check(lib().kreg_ctx_host_stats(self.h, _abi.as_ptr(out)))
-        return {"rounds": int(out[0]), "t_prepare_s": float(out[1]), "t_wait_s": float(out[2])}
+        return {"rounds": int(out[0]), "t_prepare_s": float(out[1]), "t_wait_s": float(out[2]),
+                "t_build_prep_s": float(out[3]), "t_sweep_prep_s": float(out[4]), "t_solver_s": float(out[5]),
+                "device_allocs": int(out[6]), "device_alloc_bytes": int(out[7])}
 
     def sweep_stats(self):
         o = np.zeros(8)

@@ -243,12 +243,16 @@ kreg_status kreg_ctx_sweep_stats(const kreg_ctx* ctx, double* sweep_ms, int64_t*
   });
 }
 
-kreg_status kreg_ctx_host_stats(const kreg_ctx* ctx, double out[4]) {
+kreg_status kreg_ctx_host_stats(const kreg_ctx* ctx, double out[8]) {
   return guarded([&] {
     out[0] = static_cast<double>(ctx->rounds);
     out[1] = ctx->t_prepare;
     out[2] = ctx->t_wait;
-    out[3] = ctx->t_total;
+    out[3] = ctx->t_build_prep;
+    out[4] = ctx->t_sweep_prep;
+    out[5] = ctx->t_total;
+    out[6] = static_cast<double>(g_device_allocs);
+    out[7] = static_cast<double>(g_device_alloc_bytes);
   });
 }
 
@@ -265,6 +269,13 @@ kreg_status kreg_ctx_stats(const kreg_ctx* ctx, double out[8]) {
   });
 }
 
+kreg_status kreg_ctx_set_max_active(kreg_ctx* ctx, int32_t n) {
+  return guarded([&] {
+    require(ctx != nullptr && n >= 0, "invalid argument");
+    ctx->max_active = n;
+  });
+}
+
 kreg_status kreg_ctx_set_profiling(kreg_ctx* ctx, int32_t enabled) {
   return guarded([&] { ctx->profiling = enabled != 0; });
 }
@@ -278,6 +289,7 @@ kreg_status kreg_ctx_reset_stats(kreg_ctx* ctx) {
     ctx->slots_streamed = 0;
     ctx->rounds = 0;
     ctx->t_prepare = ctx->t_wait = ctx->t_total = 0.0;
+    ctx->t_build_prep = ctx->t_sweep_prep = 0.0;
     ctx->launches_base = kreg_dev::kernel_launch_count();
   });
 }

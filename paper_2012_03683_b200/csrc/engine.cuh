@@ -12,12 +12,12 @@
 //     plus cell-ordered FP64 copies cx/cy/cz for coalesced candidate tests.
 //   Pair list (per build): sliced ELL over tiles of 32 consecutive sources:
 //     tile t holds 32 columns (one per source j = 32 t + l) of tile_deg[t]
-//     slots; slot (t, k, l) = tile_off[t] + 32 k + l; a slot is int2
-//     {i, float_as_int(log2 c)} = 8 B, padding {0, -inf}. CSR offsets
-//     (int64[n_z+1]) record the true degrees; xq int4[n_x] = X in fixed
-//     point (2^-k m units around the X bbox centre).
-//   Sweep scratch: q int4[M][n_z] (magic - fixed-point T z) per candidate;
-//     per-work-block FP64 partials; per-request completion counters.
+//     slots (a multiple of kUnitSteps); slot (t, k, l) = tile_off[t] + 32 k
+//     + l; a slot is int4 {x_i in fixed point (2^-k m around the X bbox
+//     centre), float_as_int(log2 c)} = 16 B, so the sweep streams slots with
+//     TMA and never gathers; padding {0,0,0,-inf}. slot_i[] keeps the target
+//     index (export only); CSR offsets (int64[n_z+1]) record true degrees.
+//   Sweep scratch: per-work-block FP64 partials; per-request counters.
 #pragma once
 
 #include <cstdint>
@@ -33,13 +33,13 @@ constexpr int kSweepThreads = 256;  // threads per (virtual) sweep block
 #define KREG_UNITS_PER_BLOCK 32
 #endif
 #ifndef KREG_SWEEP_MIN_BLOCKS
-#define KREG_SWEEP_MIN_BLOCKS 1
+#define KREG_SWEEP_MIN_BLOCKS 2
 #endif
 constexpr int kUnitSteps = KREG_UNIT_STEPS;              // degree steps per sweep work unit (x 32 lanes)
 constexpr long long kUnitsPerBlock = KREG_UNITS_PER_BLOCK;  // work units per sweep work block
 constexpr int kSweepMinBlocks = KREG_SWEEP_MIN_BLOCKS;    // __launch_bounds__ occupancy hint
 #ifndef KREG_SWEEP_STAGES
-#define KREG_SWEEP_STAGES 4
+#define KREG_SWEEP_STAGES 2
 #endif
 constexpr int kSweepStages = KREG_SWEEP_STAGES;  // per-warp TMA ring depth (units in flight)
 constexpr long long kMaxSweepBlocks = 1184;  // 8 x 148 SMs
@@ -89,7 +89,8 @@ struct BuildReq {
   long long* tile_off;   // n_tiles + 1: sliced-ELL slot offsets
   int* unit_off;         // n_tiles + 1: sweep work-unit offsets
   int* unit_tile;        // capacity / 256 + n_tiles + 1: tile of every work unit
-  int2* pairs;           // capacity slots {i, float_as_int(log2 c)}
+  int4* slots;           // capacity slots {x_i fixed point (3 x int32), float_as_int(log2 c)}
+  int* slot_i;           // capacity: target index i of every slot (export / debug only)
   long long capacity;
   double* status;        // {P, slots > capacity, slots}
   int4* xq;              // n_x fixed-point X
@@ -108,11 +109,10 @@ struct alignas(16) SweepReq {
   const int* unit_tile;
   const int* tile_deg;
   int n_tiles;
-  const int2* pairs;
-  long long capacity;    // pairs capacity (an overflowed build is skipped)
-  const int4* xq;
+  const int4* slots;
+  long long capacity;    // slot capacity (an overflowed build is skipped)
+  int grad;              // 0: F (+ displacement) only, 1: F + gradient
   const double* zx; const double* zy; const double* zz;  // source, sorted
-  int4* q;               // M x n_z scratch
   int n_z;
   int M;
   double T[kMaxCandidates][12];

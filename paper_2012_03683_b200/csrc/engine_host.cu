@@ -325,8 +325,11 @@ static void prepare_build(kreg_ctx* ctx, BuildJob& job, kreg_dev::BuildReq& R) {
   p->xq.ensure(nx + 1);
   R.scan_stride = std::max<long long>(R.n_cells, nz) / kreg_dev::kScanTile + 4;
   p->scan_tiles.ensure(static_cast<size_t>(4 * R.scan_stride));
-  long long want = p->expected_pairs > 0 ? p->expected_pairs : static_cast<long long>(nz) * 48 + 1024;
-  if (p->pairs.cap < static_cast<size_t>(want)) p->pairs.ensure(static_cast<size_t>(want));
+  long long want = p->expected_pairs > 0 ? p->expected_pairs : static_cast<long long>(nz) * 96 + 4096;
+  if (p->slot_buf.cap < static_cast<size_t>(want)) {
+    p->slot_buf.ensure(static_cast<size_t>(want), false, 1.5);
+    p->slot_i.ensure(p->slot_buf.cap, false, 1.0);
+  }
   const int n_tiles = (nz + 31) / 32;
   p->n_tiles = n_tiles;
   p->tile_deg.ensure(n_tiles + 1);
@@ -334,7 +337,7 @@ static void prepare_build(kreg_ctx* ctx, BuildJob& job, kreg_dev::BuildReq& R) {
   p->tile_units.ensure(n_tiles + 1);
   p->tile_off.ensure(n_tiles + 2);
   p->unit_off.ensure(n_tiles + 2);
-  p->unit_tile.ensure(p->pairs.cap / (32 * kreg_dev::kUnitSteps) + n_tiles + 2);
+  p->unit_tile.ensure(p->slot_buf.cap / (32 * kreg_dev::kUnitSteps) + n_tiles + 2);
   R.unit_tile = p->unit_tile.ptr;
   R.n_tiles = n_tiles;
   R.tile_deg = p->tile_deg.ptr;
@@ -351,8 +354,9 @@ static void prepare_build(kreg_ctx* ctx, BuildJob& job, kreg_dev::BuildReq& R) {
   R.cx = p->cx.ptr; R.cy = p->cy.ptr; R.cz = p->cz.ptr;
   R.count = p->count.ptr;
   R.offsets = p->offsets.ptr;
-  R.pairs = p->pairs.ptr;
-  R.capacity = static_cast<long long>(p->pairs.cap);
+  R.slots = p->slot_buf.ptr;
+  R.slot_i = p->slot_i.ptr;
+  R.capacity = static_cast<long long>(p->slot_buf.cap);
   R.xq = p->xq.ptr;
   R.scan_tiles = p->scan_tiles.ptr;
 
@@ -374,33 +378,35 @@ static void prepare_build(kreg_ctx* ctx, BuildJob& job, kreg_dev::BuildReq& R) {
 // Scratch of request e lives in per-round arenas of the context (several
 // requests of one round may sweep the same pair list).
 struct SweepScratch {
-  size_t q_off = 0, part_off = 0;
+  size_t part_off = 0;
 };
 
+static long long sweep_units(const kreg_pairs* p) {
+  // every sweep unit is exactly 32 * kUnitSteps slots (k_tile_sizes); before
+  // the build round has been read back use the capacity bound
+  if (p->counts_valid) return p->slots / (32LL * kreg_dev::kUnitSteps);
+  return static_cast<long long>(p->slot_buf.cap) / (32 * kreg_dev::kUnitSteps) + p->n_tiles + 1;
+}
+
 static size_t sweep_nvb_cap(const EvalJob& job) {
-  // units <= slots / (32 kUnitSteps) + n_tiles
-  const long long units = static_cast<long long>(job.pairs->pairs.cap) / (32 * kreg_dev::kUnitSteps) +
-                          job.pairs->n_tiles + 1;
-  const long long b = units / kreg_dev::kUnitsPerBlock + 2;
-  return static_cast<size_t>(std::min(b, kreg_dev::kMaxSweepBlocks));
+  const long long b = sweep_units(job.pairs) / kreg_dev::kUnitsPerBlock + 1;
+  return static_cast<size_t>(std::max(1LL, std::min(b, kreg_dev::kMaxSweepBlocks)));
 }
 
 static void prepare_sweep(kreg_ctx* ctx, EvalJob& job, kreg_dev::SweepReq& R, const SweepScratch& s, int e) {
   kreg_pairs* p = job.pairs;
   std::memset(&R, 0, sizeof(R));
   const int nz = p->Z->n;
-  // every sweep unit is exactly 32 * kUnitSteps slots (k_tile_sizes)
-  R.units = p->counts_valid ? p->slots / (32LL * kreg_dev::kUnitSteps) : -1;
+  R.units = p->counts_valid ? sweep_units(p) : -1;
   R.tile_off = p->tile_off.ptr;
   R.unit_off = p->unit_off.ptr;
   R.unit_tile = p->unit_tile.ptr;
   R.tile_deg = p->tile_deg.ptr;
   R.n_tiles = p->n_tiles;
-  R.pairs = p->pairs.ptr;
-  R.capacity = static_cast<long long>(p->pairs.cap);
-  R.xq = p->xq.ptr;
+  R.slots = p->slot_buf.ptr;
+  R.capacity = static_cast<long long>(p->slot_buf.cap);
+  R.grad = job.grad ? 1 : 0;
   R.zx = p->Z->x.ptr; R.zy = p->Z->y.ptr; R.zz = p->Z->z.ptr;
-  R.q = ctx->q_arena.ptr + s.q_off;
   R.n_z = nz;
   R.M = job.M;
   for (int m = 0; m < job.M; ++m) std::memcpy(R.T[m], job.T[m], sizeof(double) * 12);
@@ -435,18 +441,19 @@ void run_round(kreg_ctx* ctx, std::vector<BuildJob>& builds, std::vector<EvalJob
     prepare_build(ctx, builds[b], ctx->h_build.ptr[b]);
     ctx->h_build.ptr[b].status = ctx->d_results.ptr + static_cast<size_t>(ne) * kreg_dev::kMaxCandidates * kreg_dev::kOut + 4 * b;
   }
+  const auto tb = clk::now();
+  ctx->t_build_prep += std::chrono::duration<double>(tb - t0).count();
   long long max_nvb_est = 1;
+  // gradient requests first, F-only requests after (one launch per group)
+  std::stable_partition(evals.begin(), evals.end(), [](const EvalJob& e) { return e.grad; });
   std::vector<SweepScratch> scratch(static_cast<size_t>(ne));
-  size_t q_total = 0, part_total = 0;
+  size_t part_total = 0;
   for (int e = 0; e < ne; ++e) {
-    scratch[e].q_off = q_total;
     scratch[e].part_off = part_total;
-    q_total += static_cast<size_t>(evals[e].M) * (evals[e].pairs->Z->n + 1);
     part_total += sweep_nvb_cap(evals[e]) * evals[e].M * 7;
   }
   if (ne) {
-    ctx->q_arena.ensure(q_total + 1);
-    ctx->part_arena.ensure(part_total + 1);
+    ctx->part_arena.ensure(part_total + 1, false, 1.5);
     ctx->counter_arena.ensure(ne + 1, /*zero=*/true);
     ctx->disp_arena.ensure(static_cast<size_t>(ne + 1) * kreg_dev::kMaxCandidates, /*zero=*/true);
   }
@@ -455,6 +462,8 @@ void run_round(kreg_ctx* ctx, std::vector<BuildJob>& builds, std::vector<EvalJob
     ctx->h_sweep.ptr[e].out = ctx->d_results.ptr + static_cast<size_t>(e) * kreg_dev::kMaxCandidates * kreg_dev::kOut;
     max_nvb_est = std::max<long long>(max_nvb_est, static_cast<long long>(sweep_nvb_cap(evals[e])));
   }
+  const auto ts = clk::now();
+  ctx->t_sweep_prep += std::chrono::duration<double>(ts - tb).count();
   if (nb)
     KREG_CUDA(cudaMemcpyAsync(ctx->d_build.ptr, ctx->h_build.ptr, sizeof(kreg_dev::BuildReq) * nb,
                               cudaMemcpyHostToDevice, ctx->stream));
@@ -540,14 +549,18 @@ void pairs_export(kreg_ctx* ctx, const kreg_pairs* p, int64_t* offsets, int32_t*
   const int nz = p->Z ? p->Z->n : 0;
   std::vector<long long> off(static_cast<size_t>(nz) + 1, 0);
   std::vector<long long> toff(static_cast<size_t>(p->n_tiles) + 1, 0);
-  std::vector<int2> pr(static_cast<size_t>(p->slots));
+  std::vector<int4> sl(static_cast<size_t>(p->slots));
+  std::vector<int> si(static_cast<size_t>(p->slots));
   if (nz) {
     KREG_CUDA(cudaMemcpyAsync(off.data(), p->offsets.ptr, sizeof(long long) * (nz + 1), cudaMemcpyDeviceToHost,
                               ctx->stream));
     KREG_CUDA(cudaMemcpyAsync(toff.data(), p->tile_off.ptr, sizeof(long long) * (p->n_tiles + 1),
                               cudaMemcpyDeviceToHost, ctx->stream));
-    if (p->slots)
-      KREG_CUDA(cudaMemcpyAsync(pr.data(), p->pairs.ptr, sizeof(int2) * p->slots, cudaMemcpyDeviceToHost, ctx->stream));
+    if (p->slots) {
+      KREG_CUDA(cudaMemcpyAsync(sl.data(), p->slot_buf.ptr, sizeof(int4) * p->slots, cudaMemcpyDeviceToHost,
+                                ctx->stream));
+      KREG_CUDA(cudaMemcpyAsync(si.data(), p->slot_i.ptr, sizeof(int) * p->slots, cudaMemcpyDeviceToHost, ctx->stream));
+    }
     KREG_CUDA(cudaStreamSynchronize(ctx->stream));
   }
   std::vector<long long> cnt(static_cast<size_t>(nz), 0);
@@ -560,10 +573,10 @@ void pairs_export(kreg_ctx* ctx, const kreg_pairs* p, int64_t* offsets, int32_t*
     tmp.clear();
     const long long col = toff[static_cast<size_t>(js >> 5)] + (js & 31);  // sliced-ELL column of js
     for (long long k = 0; k < off[js + 1] - off[js]; ++k) {
-      const int2 s = pr[static_cast<size_t>(col + 32 * k)];
+      const size_t at = static_cast<size_t>(col + 32 * k);
       float lc;
-      std::memcpy(&lc, &s.y, sizeof(float));
-      tmp.push_back({p->X->order[s.x], std::exp2(static_cast<double>(lc))});
+      std::memcpy(&lc, &sl[at].w, sizeof(float));
+      tmp.push_back({p->X->order[si[at]], std::exp2(static_cast<double>(lc))});
     }
     std::sort(tmp.begin(), tmp.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
     long long at = offsets[j];

@@ -28,6 +28,10 @@ struct Error : std::runtime_error {
     if (e_ != cudaSuccess) ::kreg_host::throw_cuda(e_, #call); \
   } while (0)
 
+// device allocation accounting (count, bytes) — cudaMalloc/cudaFree synchronise
+inline long long g_device_allocs = 0;
+inline long long g_device_alloc_bytes = 0;
+
 template <typename T>
 struct DevBuf {
   T* ptr = nullptr;
@@ -46,6 +50,8 @@ struct DevBuf {
     if (n <= cap && ptr) return;
     release();
     size_t want = n < 16 ? 16 : static_cast<size_t>(static_cast<double>(n) * slack);
+    ++g_device_allocs;
+    g_device_alloc_bytes += static_cast<long long>(want * sizeof(T));
     cudaError_t e = cudaMalloc(&ptr, want * sizeof(T));
     if (e != cudaSuccess) {
       cudaGetLastError();
@@ -113,15 +119,16 @@ struct kreg_ctx {
   kreg_host::DevBuf<double> d_T2;
   kreg_host::DevBuf<unsigned long long> d_disp;
   // per-round sweep scratch arenas (one slice per request)
-  kreg_host::DevBuf<int4> q_arena;
   kreg_host::DevBuf<double> part_arena;
   kreg_host::DevBuf<unsigned int> counter_arena;        // self-resetting, zero between rounds
   kreg_host::DevBuf<unsigned long long> disp_arena;    // self-resetting, zero between rounds
   // pair-list workspaces kept across registrations (device buffers keep capacity)
   std::vector<kreg_pairs*> pool;
+  int max_active = 0;  // lockstep window of kreg_register_batch (0 = all at once)
   // host-side round accounting (seconds)
   long long rounds = 0;
   double t_prepare = 0.0, t_wait = 0.0, t_total = 0.0;
+  double t_build_prep = 0.0, t_sweep_prep = 0.0;
   ~kreg_ctx();
 };
 
@@ -159,7 +166,8 @@ struct kreg_pairs {
   kreg_host::DevBuf<int> cell_count, cell_start, cell_of, tmp_items, cell_items, count;
   kreg_host::DevBuf<double> cx, cy, cz;
   kreg_host::DevBuf<long long> offsets, scan_tiles, tile_off;
-  kreg_host::DevBuf<int2> pairs;           // sliced-ELL slots
+  kreg_host::DevBuf<int4> slot_buf;        // sliced-ELL slots {x fixed point, log2 c}
+  kreg_host::DevBuf<int> slot_i;           // target index per slot (export only)
   kreg_host::DevBuf<int> tile_deg, tile_slots, tile_units, unit_off, unit_tile;
   int n_tiles = 0;
   long long slots = 0;                     // valid after the build round
@@ -202,6 +210,7 @@ struct EvalJob {
   double T[kreg_dev::kMaxCandidates][12];
   double lengthscale;  // kernel lengthscale of the evaluation
   double* out;         // host, M x 8 {F, omega, v, disp}; filled after run_round
+  bool grad = true;    // false: F + displacement only (gradient left zero)
 };
 
 // Executes builds (then, in stream order, evaluations) as batched launches,

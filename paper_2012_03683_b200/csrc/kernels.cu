@@ -319,7 +319,10 @@ __global__ void __launch_bounds__(256) k_pair_pass(const BuildReq* reqs) {
           const unsigned m = __ballot_sync(0xffffffffu, keep);
           if (EMIT && keep) {
             const int pos = __popc(m & ((1u << lane) - 1u));
-            R.pairs[out + 32LL * (cnt + pos)] = make_int2(i, __float_as_int(lc));
+            const long long at = out + 32LL * (cnt + pos);
+            const int4 x = R.xq[i];
+            R.slots[at] = make_int4(x.x, x.y, x.z, __float_as_int(lc));
+            R.slot_i[at] = i;
           }
           cnt += __popc(m);
         }
@@ -329,9 +332,12 @@ __global__ void __launch_bounds__(256) k_pair_pass(const BuildReq* reqs) {
   if (!EMIT) {
     if (lane == 0) R.count[j] = cnt;
   } else {
-    // pad the column to the tile's max degree: w = ex2(-inf) = 0
+    // pad the column to the tile's (unit-rounded) max degree: w = ex2(-inf) = 0
     const int dmax = R.tile_deg[j >> 5];
-    for (int k = cnt + lane; k < dmax; k += 32) R.pairs[out + 32LL * k] = make_int2(0, __float_as_int(-INFINITY));
+    for (int k = cnt + lane; k < dmax; k += 32) {
+      R.slots[out + 32LL * k] = make_int4(0, 0, 0, __float_as_int(-INFINITY));
+      R.slot_i[out + 32LL * k] = -1;
+    }
   }
 }
 
@@ -452,47 +458,48 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phas
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 constexpr int kUnitSlots = 32 * kUnitSteps;
-constexpr unsigned kStageBytes = kUnitSlots * sizeof(int2);
+constexpr unsigned kStageBytes = kUnitSlots * sizeof(int4);
 constexpr size_t kSweepSmem = (size_t)(kSweepThreads / 32) * kSweepStages * kStageBytes +
                               (size_t)(kSweepThreads / 32) * kSweepStages * sizeof(unsigned long long);
 
-// One unit of one sliced-ELL column (lane = source j) for M candidates: the
-// unit's slots come from shared memory, the x gathers go to L1/L2, then per
-// candidate pair d = x - q (exact, fixed point), w = ex2(r^2 kappa + log2 c).
-template <int NP>
-__device__ __forceinline__ void sweep_unit(const int2 (&pr)[kUnitSteps], const int4* __restrict__ xq,
-                                           const int (&qx)[2 * NP], const int (&qy)[2 * NP],
-                                           const int (&qz)[2 * NP], f2_t kap2, f2_t (&W)[NP], f2_t (&Sx)[NP],
-                                           f2_t (&Sy)[NP], f2_t (&Sz)[NP]) {
-  int4 xv[kUnitSteps];
-#pragma unroll
-  for (int k = 0; k < kUnitSteps; ++k) xv[k] = __ldg(xq + pr[k].x);
+// One unit of one sliced-ELL column (lane = source j) for M candidates. The
+// unit's 16-B slots {x fixed point, log2 c} are in shared memory (TMA);
+// per candidate pair d = x - q (exact, fixed point), w = ex2(r^2 kappa +
+// log2 c), W += w and (GRAD) S += w d on FFMA2/FADD2/FMUL2 + 2 MUFU.EX2.
+template <int NP, bool GRAD>
+__device__ __forceinline__ void sweep_unit(const int4* __restrict__ stage, int lane, const int (&qx)[2 * NP],
+                                           const int (&qy)[2 * NP], const int (&qz)[2 * NP], f2_t kap2,
+                                           f2_t (&W)[NP], f2_t (&Sx)[NP], f2_t (&Sy)[NP], f2_t (&Sz)[NP]) {
   const f2_t nmag = pk2(-12582912.0f, -12582912.0f);
 #pragma unroll
   for (int k = 0; k < kUnitSteps; ++k) {
-    const float lc = __int_as_float(pr[k].y);
+    const int4 sl = stage[32 * k + lane];  // conflict-free LDS.128
+    const float lc = __int_as_float(sl.w);
     const f2_t lc2 = pk2(lc, lc);
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
       const int a = 2 * p, b = 2 * p + 1;
-      const f2_t dx = add2(pk2(__int_as_float(xv[k].x + qx[a]), __int_as_float(xv[k].x + qx[b])), nmag);
-      const f2_t dy = add2(pk2(__int_as_float(xv[k].y + qy[a]), __int_as_float(xv[k].y + qy[b])), nmag);
-      const f2_t dz = add2(pk2(__int_as_float(xv[k].z + qz[a]), __int_as_float(xv[k].z + qz[b])), nmag);
+      const f2_t dx = add2(pk2(__int_as_float(sl.x + qx[a]), __int_as_float(sl.x + qx[b])), nmag);
+      const f2_t dy = add2(pk2(__int_as_float(sl.y + qy[a]), __int_as_float(sl.y + qy[b])), nmag);
+      const f2_t dz = add2(pk2(__int_as_float(sl.z + qz[a]), __int_as_float(sl.z + qz[b])), nmag);
       const f2_t r2 = fma2(dz, dz, fma2(dy, dy, mul2(dx, dx)));
       float e0, e1;
       upk2(fma2(r2, kap2, lc2), e0, e1);
       const f2_t w = pk2(ex2_approx(e0), ex2_approx(e1));
       W[p] = add2(W[p], w);
-      Sx[p] = fma2(w, dx, Sx[p]);
-      Sy[p] = fma2(w, dy, Sy[p]);
-      Sz[p] = fma2(w, dz, Sz[p]);
+      if (GRAD) {
+        Sx[p] = fma2(w, dx, Sx[p]);
+        Sy[p] = fma2(w, dy, Sy[p]);
+        Sz[p] = fma2(w, dz, Sz[p]);
+      }
     }
   }
 }
 
-template <int NP>
+template <int NP, bool GRAD>
 __global__ void __launch_bounds__(kSweepThreads, kSweepMinBlocks) k_sweep(const SweepReq* reqs) {
   constexpr int MAXM = 2 * NP;
+  constexpr int NV = GRAD ? 7 : 1;  // reduced values per candidate
   constexpr int NW = kSweepThreads / 32;
   // the request descriptor (~1 KB) is staged in shared memory once per block
   __shared__ __align__(16) SweepReq Rs;
@@ -514,7 +521,7 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMinBlocks) k_sweep(const 
   __shared__ double red[NW][MAXM * 7];
   __shared__ unsigned long long dred[NW][MAXM];
   extern __shared__ __align__(128) unsigned char dyn_smem[];
-  int2* ring_all = reinterpret_cast<int2*>(dyn_smem);
+  int4* ring_all = reinterpret_cast<int4*>(dyn_smem);
   unsigned long long* bar_all =
       reinterpret_cast<unsigned long long*>(dyn_smem + (size_t)NW * kSweepStages * kStageBytes);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -537,9 +544,9 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMinBlocks) k_sweep(const 
     const long long upw = (upb + NW - 1) / NW;
     const long long wu0 = min(u1, u0 + wid * upw);
     const int nunits = (int)(min(u1, wu0 + upw) - wu0);
-    int2* ring = ring_all + (size_t)wid * kSweepStages * kUnitSlots;
+    int4* ring = ring_all + (size_t)wid * kSweepStages * kUnitSlots;
     unsigned long long* bars = bar_all + wid * kSweepStages;
-    const int2* src = R.pairs + wu0 * kUnitSlots;
+    const int4* src = R.slots + wu0 * kUnitSlots;
     if (lane == 0) {
       for (int s = 0; s < kSweepStages && s < nunits; ++s) {
         mbar_expect_tx(&bars[s], kStageBytes);
@@ -565,12 +572,14 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMinBlocks) k_sweep(const 
           const f2_t fqz = pk2((float)(int)(kMagic - (unsigned)qz[2 * p]), (float)(int)(kMagic - (unsigned)qz[2 * p + 1]));
           const f2_t neg = pk2(-1.0f, -1.0f);
           acc[p][0] = add2(acc[p][0], W[p]);
-          acc[p][1] = add2(acc[p][1], Sx[p]);
-          acc[p][2] = add2(acc[p][2], Sy[p]);
-          acc[p][3] = add2(acc[p][3], Sz[p]);
-          acc[p][4] = add2(acc[p][4], fma2(mul2(neg, fqz), Sy[p], mul2(fqy, Sz[p])));
-          acc[p][5] = add2(acc[p][5], fma2(mul2(neg, fqx), Sz[p], mul2(fqz, Sx[p])));
-          acc[p][6] = add2(acc[p][6], fma2(mul2(neg, fqy), Sx[p], mul2(fqx, Sy[p])));
+          if (GRAD) {
+            acc[p][1] = add2(acc[p][1], Sx[p]);
+            acc[p][2] = add2(acc[p][2], Sy[p]);
+            acc[p][3] = add2(acc[p][3], Sz[p]);
+            acc[p][4] = add2(acc[p][4], fma2(mul2(neg, fqz), Sy[p], mul2(fqy, Sz[p])));
+            acc[p][5] = add2(acc[p][5], fma2(mul2(neg, fqx), Sz[p], mul2(fqz, Sx[p])));
+            acc[p][6] = add2(acc[p][6], fma2(mul2(neg, fqy), Sx[p], mul2(fqx, Sy[p])));
+          }
         }
       }
 #pragma unroll
@@ -607,16 +616,13 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMinBlocks) k_sweep(const 
       }
       const int s = i % kSweepStages;
       mbar_wait(&bars[s], (unsigned)((i / kSweepStages) & 1));
-      int2 pr[kUnitSteps];
-#pragma unroll
-      for (int k = 0; k < kUnitSteps; ++k) pr[k] = ring[s * kUnitSlots + 32 * k + lane];
+      if (active) sweep_unit<NP, GRAD>(ring + s * kUnitSlots, lane, qx, qy, qz, kap2, W, Sx, Sy, Sz);
       __syncwarp();
       if (lane == 0 && i + kSweepStages < nunits) {  // refill this stage with unit i + stages
         fence_proxy_async();
         mbar_expect_tx(&bars[s], kStageBytes);
         tma_load_1d(ring + s * kUnitSlots, src + (long long)(i + kSweepStages) * kUnitSlots, kStageBytes, &bars[s]);
       }
-      if (active) sweep_unit<NP>(pr, R.xq, qx, qy, qz, kap2, W, Sx, Sy, Sz);
     }
     flush_tile();
 
@@ -625,10 +631,10 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMinBlocks) k_sweep(const 
     for (int p = 0; p < NP; ++p) {
 #pragma unroll
       for (int c = 0; c < 7; ++c) {
-        float a0, a1;
-        upk2(acc[p][c], a0, a1);
-        const double s0 = warp_sum_d((double)a0);
-        const double s1 = warp_sum_d((double)a1);
+        float a0 = 0.0f, a1 = 0.0f;
+        if (c < NV) upk2(acc[p][c], a0, a1);
+        const double s0 = c < NV ? warp_sum_d((double)a0) : 0.0;
+        const double s1 = c < NV ? warp_sum_d((double)a1) : 0.0;
         if (lane == 0) {
           red[wid][(2 * p) * 7 + c] = s0;
           red[wid][(2 * p + 1) * 7 + c] = s1;
@@ -771,22 +777,39 @@ void build_pairs_batched(const BuildReq* h, const BuildReq* d, int n, cudaStream
 void sweep_batched(const SweepReq* h, const SweepReq* d, int n, int blocks_per_req, cudaStream_t st,
                    cudaEvent_t ev0, cudaEvent_t ev1) {
   if (n == 0) return;
-  int max_m = 1;
-  for (int r = 0; r < n; ++r) max_m = max(max_m, h[r].M);
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(k_sweep<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepSmem);
-    cudaFuncSetAttribute(k_sweep<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepSmem);
-    cudaFuncSetAttribute(k_sweep<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepSmem);
+    cudaFuncSetAttribute(k_sweep<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepSmem);
+    cudaFuncSetAttribute(k_sweep<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepSmem);
+    cudaFuncSetAttribute(k_sweep<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepSmem);
+    cudaFuncSetAttribute(k_sweep<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepSmem);
+    cudaFuncSetAttribute(k_sweep<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepSmem);
+    cudaFuncSetAttribute(k_sweep<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepSmem);
     attr_set = true;
   }
   if (ev0) cudaEventRecord(ev0, st);
-  const dim3 g(blocks_per_req, n);
-  if (max_m <= 2) k_sweep<1><<<g, kSweepThreads, kSweepSmem, st>>>(d);
-  else if (max_m <= 4) k_sweep<2><<<g, kSweepThreads, kSweepSmem, st>>>(d);
-  else k_sweep<4><<<g, kSweepThreads, kSweepSmem, st>>>(d);
+  // requests arrive grouped: gradient requests first, then F-only ones
+  int n_grad = 0;
+  while (n_grad < n && h[n_grad].grad) ++n_grad;
+  for (int grp = 0; grp < 2; ++grp) {
+    const int r0 = grp == 0 ? 0 : n_grad, r1 = grp == 0 ? n_grad : n;
+    if (r1 <= r0) continue;
+    int max_m = 1;
+    for (int r = r0; r < r1; ++r) max_m = max(max_m, h[r].M);
+    const dim3 g(blocks_per_req, r1 - r0);
+    const SweepReq* dr = d + r0;
+    if (grp == 0) {
+      if (max_m <= 2) k_sweep<1, true><<<g, kSweepThreads, kSweepSmem, st>>>(dr);
+      else if (max_m <= 4) k_sweep<2, true><<<g, kSweepThreads, kSweepSmem, st>>>(dr);
+      else k_sweep<4, true><<<g, kSweepThreads, kSweepSmem, st>>>(dr);
+    } else {
+      if (max_m <= 2) k_sweep<1, false><<<g, kSweepThreads, kSweepSmem, st>>>(dr);
+      else if (max_m <= 4) k_sweep<2, false><<<g, kSweepThreads, kSweepSmem, st>>>(dr);
+      else k_sweep<4, false><<<g, kSweepThreads, kSweepSmem, st>>>(dr);
+    }
+    count_launch(1);
+  }
   if (ev1) cudaEventRecord(ev1, st);
-  count_launch(1);
 }
 
 void displacement(const double* zx, const double* zy, const double* zz, int n, const double* d_T2,

@@ -19,6 +19,7 @@
 //    a halved step, registration.cpp:154).
 #include <algorithm>
 #include <cfloat>
+#include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -80,6 +81,7 @@ int env_int(const char* name, int dflt) {
 
 struct Memo {
   double eps;
+  bool grad;  // out[1..6] holds the gradient
   double out[kreg_dev::kOut];
 };
 
@@ -126,6 +128,7 @@ struct Reg {
   double cand_T[24][12];
   double cand_eps[24];
   double cand_out[24][kreg_dev::kOut];
+  bool cand_grad = true;     // the in-flight candidates carry their gradient
   // outputs
   std::vector<double> tr_obj, tr_ind, tr_l, tr_step, tr_tn;
   std::vector<long long> tr_pc;
@@ -161,7 +164,7 @@ void finish(Reg& r) {
 
 // End of one reference iteration (registration.cpp:145-182).
 void end_iteration(Reg& r, bool searched, bool accepted, int backtracks, double eps, const double* cand_T,
-                   const double* cand_out) {
+                   const double* cand_out, bool cand_has_grad = true) {
   const kreg_registration_config& c = r.cfg;
   double accepted_step = 0.0, twist_norm = 0.0, f_now = r.ev[0];
   if (searched) {
@@ -175,8 +178,10 @@ void end_iteration(Reg& r, bool searched, bool accepted, int backtracks, double 
                    std::sqrt(applied[3] * applied[3] + applied[4] * applied[4] + applied[5] * applied[5]) / r.v_scale;
       r.step_factor = backtracks == 0 ? std::min(r.step_factor * c.step_grow, 1e3)
                                       : std::max(r.step_factor * std::pow(c.step_shrink, backtracks), 1e-6);
-      std::memcpy(r.ev, cand_out, sizeof(r.ev));  // F, grad and displacement at the new T
-      r.have_eval = true;
+      // F, grad and displacement at the new T (an F-only candidate leaves the
+      // gradient to a fresh evaluation at the start of the next iteration)
+      std::memcpy(r.ev, cand_out, sizeof(r.ev));
+      r.have_eval = cand_has_grad;
       r.memo.clear();
     } else {
       r.step_factor = std::max(r.step_factor * c.step_shrink, 1e-6);
@@ -236,7 +241,7 @@ void schedule_build_eval(Reg& r, std::vector<BuildJob>& builds, std::vector<Eval
 
 // Advance host-only logic until the registration needs device work.
 void plan(Reg& r, std::vector<BuildJob>& builds, std::vector<EvalJob>& evals, std::vector<Reg*>& owners,
-          int k_first) {
+          int k_first, bool fail_grad) {
   const kreg_registration_config& c = r.cfg;
   for (;;) {
     switch (r.phase) {
@@ -322,7 +327,7 @@ void plan(Reg& r, std::vector<BuildJob>& builds, std::vector<EvalJob>& evals, st
           kreg_se3::compose(E, r.T, cand);
           if (hit && n_new == 0) {
             if (hit->out[0] > r.ev[0]) {
-              end_iteration(r, true, true, k, eps, cand, hit->out);
+              end_iteration(r, true, true, k, eps, cand, hit->out, hit->grad);
               resolved = true;
               break;
             }
@@ -346,6 +351,9 @@ void plan(Reg& r, std::vector<BuildJob>& builds, std::vector<EvalJob>& evals, st
           }
           break;  // continue searching (more memo hits or new candidates)
         }
+        // the first batch carries gradients (its accepted candidate's gradient
+        // is the next iteration's); the failure-path batches evaluate F only
+        r.cand_grad = k0 == 0 || fail_grad;
         for (int b = 0; b < n_new; b += kreg_dev::kMaxCandidates) {
           EvalJob e;
           e.pairs = r.pairs.get();
@@ -353,6 +361,7 @@ void plan(Reg& r, std::vector<BuildJob>& builds, std::vector<EvalJob>& evals, st
           for (int m = 0; m < e.M; ++m) std::memcpy(e.T[m], r.cand_T[b + m], sizeof(double) * 12);
           e.lengthscale = r.lengthscale;
           e.out = &r.cand_out[b][0];
+          e.grad = r.cand_grad;
           evals.push_back(e);
           owners.push_back(&r);
           ++r.sweeps;
@@ -393,6 +402,7 @@ void consume(Reg& r) {
     for (int m = 0; m < r.pending; ++m) {
       Memo mm;
       mm.eps = r.cand_eps[m];
+      mm.grad = r.cand_grad;
       std::memcpy(mm.out, r.cand_out[m], sizeof(mm.out));
       r.memo.push_back(mm);
     }
@@ -402,7 +412,7 @@ void consume(Reg& r) {
         double T[12], out[kreg_dev::kOut];
         std::memcpy(T, r.cand_T[m], sizeof(T));
         std::memcpy(out, r.cand_out[m], sizeof(out));
-        end_iteration(r, true, true, k, r.cand_eps[m], T, out);
+        end_iteration(r, true, true, k, r.cand_eps[m], T, out, r.cand_grad);
         return;
       }
     }
@@ -420,6 +430,7 @@ void consume(Reg& r) {
 
 void register_many(kreg_ctx* ctx, std::vector<RegJob>& jobs) {
   const int k_first = std::max(1, std::min(8, env_int("KREG_K_FIRST", 2)));
+  const bool fail_grad = env_int("KREG_FAIL_GRAD", 0) != 0;
   std::vector<std::unique_ptr<Reg>> regs;
   for (RegJob& j : jobs) {
     j.status = KREG_OK;
@@ -447,9 +458,6 @@ void register_many(kreg_ctx* ctx, std::vector<RegJob>& jobs) {
     r->wp.lengthscale = r->lengthscale;
     std::memcpy(r->T, j.initial, sizeof(r->T));
     for (double& d : r->dir) d = 0.0;
-    r->pairs.ctx = ctx;
-    r->pairs.p = acquire_workspace(ctx);
-    if (j.expected_pairs > 0) r->pairs->expected_pairs = j.expected_pairs;
     if (j.X->n == 0 || j.Z->n == 0) {
       // empty cloud: build_pairs yields an empty list -> NoOverlapError
       char msg[160];
@@ -465,13 +473,36 @@ void register_many(kreg_ctx* ctx, std::vector<RegJob>& jobs) {
   std::vector<BuildJob> builds;
   std::vector<EvalJob> evals;
   std::vector<Reg*> owners;
+  using clk = std::chrono::steady_clock;
+  // At most `window` registrations are in flight; a finished one is replaced
+  // by the next job at once (dynamic refill), so one slow registration does
+  // not hold the batch. Results do not depend on the window: every sweep
+  // request is evaluated independently of what else shares its launch.
+  const size_t window = ctx && ctx->max_active > 0 ? static_cast<size_t>(ctx->max_active) : regs.size();
+  size_t started = 0;
+  std::vector<Reg*> active;
   for (;;) {
+    const auto t0 = clk::now();
+    active.erase(std::remove_if(active.begin(), active.end(), [](Reg* r) { return r->phase == Phase::kDone; }),
+                 active.end());
+    while (active.size() < window && started < regs.size()) {
+      Reg* r = regs[started++].get();
+      r->pairs.ctx = ctx;
+      r->pairs.p = acquire_workspace(ctx);
+      if (r->job->expected_pairs > 0) r->pairs->expected_pairs = r->job->expected_pairs;
+      active.push_back(r);
+    }
     builds.clear();
     evals.clear();
     owners.clear();
-    for (auto& r : regs) plan(*r, builds, evals, owners, k_first);
-    if (builds.empty() && evals.empty()) break;
+    for (Reg* r : active) plan(*r, builds, evals, owners, k_first, fail_grad);
+    if (builds.empty() && evals.empty()) {
+      if (started >= regs.size()) break;
+      continue;  // all active registrations finished this round: refill
+    }
+    const auto t1 = clk::now();
     run_round(ctx, builds, evals);
+    const auto t2 = clk::now();
     // each registration consumes once per round
     Reg* last = nullptr;
     for (Reg* r : owners) {
@@ -479,6 +510,9 @@ void register_many(kreg_ctx* ctx, std::vector<RegJob>& jobs) {
       last = r;
       consume(*r);
     }
+    if (ctx)
+      ctx->t_total += std::chrono::duration<double>(t1 - t0).count() +
+                      std::chrono::duration<double>(clk::now() - t2).count();
   }
 }
 
