@@ -44,15 +44,16 @@ def measured_peaks():
 
 
 def make_workload(rank: int, batch: int, n_points: int, seed: int = 2012036830):
-    """B frame pairs from one street sequence (frame k -> k+1), per rank."""
-    frames, poses = synth.kitti_sequence(seed + 1009 * rank, batch + 1, n_points)
-    from paper_2012_03683_b200.types import compose, inverse
+    """B independent KITTI-shaped frame pairs per rank: each
+    pair is its own ray-cast street, second frame 1.0 m forward + 0.5 deg yaw,
+    initial guess = true motion composed with a small error."""
     Xs, Zs, inits = [], [], []
     for k in range(batch):
-        Xs.append(frames[k])
-        Zs.append(frames[k + 1])
-        truth = compose(inverse(poses[k]), poses[k + 1])
-        inits.append(synth.perturbed(truth, seed + 7919 * rank + k))
+        s = synth.SplitMix64.derive(seed, 100003 * rank + k) & 0x7FFFFFFF
+        X, Z, T = synth.kitti_pair(s, n_points, start=float(k % 7) * 9.0)
+        Xs.append(X)
+        Zs.append(Z)
+        inits.append(synth.perturbed(T, s))
     return Xs, Zs, inits
 
 
@@ -209,6 +210,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--batch", type=int, default=32, help="frame pairs per step per GPU")
+    ap.add_argument("--window", type=int, default=0, help="registrations in flight (0 = whole batch)")
     ap.add_argument("--points", type=int, default=40000)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -222,6 +224,7 @@ def main():
 
     from paper_2012_03683_b200 import api
     ctx = api.Context(local)
+    ctx.set_max_active(args.window)
     params, cfg = synth.kitti_params(), synth.kitti_subsequent_config()
     B = args.batch
     Xs, Zs, inits = make_workload(rank, B, args.points)
