@@ -168,6 +168,13 @@ kreg_status kreg_ctx_host_stats(const kreg_ctx* ctx, double out[8]);
  * sliced-ELL slots streamed, rounds, s preparing, s waiting}. */
 kreg_status kreg_ctx_stats(const kreg_ctx* ctx, double out[8]);
 kreg_status kreg_ctx_reset_stats(kreg_ctx* ctx);
+/* Candidate-list skin: a full build searches the grid at R_s = cutoff (1 +
+ * skin) and later builds filter that list while max_j |T z_j - T_s z_j| <=
+ * R_s - cutoff (exact: same FP64 predicate); 0 = always search the grid.
+ * Default 0.25 (env KREG_SKIN). Engine extension, no reference counterpart. */
+kreg_status kreg_ctx_set_candidate_skin(kreg_ctx* ctx, double skin);
+/* Builds so far: {grid searches, candidate-list filters}. */
+kreg_status kreg_ctx_build_stats(const kreg_ctx* ctx, int64_t out[2]);
 
 /* Upload a cloud into device SoA (replaces constructing kreg::PointCloud,
  * point_cloud.cpp:49-59; same validation and messages). */
@@ -181,6 +188,13 @@ kreg_status kreg_build_pairs(kreg_ctx* ctx, const kreg_cloud* X, const kreg_clou
                              const double T[12], const kreg_kernel_params* params,
                              double cutoff_multiplier, double c_min, kreg_pairs** out,
                              int64_t* n_pairs);
+/* build_pairs again into an existing list (the reference loop's rebuild,
+ * registration.cpp:111/126: pairs = build_pairs(X, Z, T, ...)): reuses the
+ * list's candidate list when it provably covers the new list (see
+ * kreg_ctx_set_candidate_skin), else searches the grid. Same result either way. */
+kreg_status kreg_rebuild_pairs(kreg_ctx* ctx, kreg_pairs* pairs, const double T[12],
+                               const kreg_kernel_params* params, double cutoff_multiplier,
+                               double c_min, int64_t* n_pairs);
 kreg_status kreg_pairs_destroy(kreg_pairs* pairs);
 int64_t kreg_pairs_size(const kreg_pairs* pairs);
 /* Device layout statistics: {pairs, sliced-ELL slots incl. padding, tiles,

@@ -57,6 +57,9 @@ def lib():
         L.kreg_ctx_host_stats.argtypes = [P, _abi.dptr]
         L.kreg_ctx_stats.argtypes = [P, _abi.dptr]
         L.kreg_ctx_reset_stats.argtypes = [P]
+        L.kreg_ctx_set_candidate_skin.argtypes = [P, D]
+        L.kreg_ctx_build_stats.argtypes = [P, _abi.i64ptr]
+        L.kreg_rebuild_pairs.argtypes = [P, P, _abi.dptr, KP, D, D, _abi.i64ptr]
         L.kreg_cloud_create.argtypes = [P, VP, C.POINTER(P)]
         L.kreg_cloud_destroy.argtypes = [P]
         L.kreg_cloud_size.argtypes = [P]
@@ -138,6 +141,15 @@ class Context:
         """Lockstep window of register_batch (0 = all registrations at once)."""
         _check(lib().kreg_ctx_set_max_active(self.h, int(n)))
 
+    def set_candidate_skin(self, skin: float):
+        """Candidate-list radius R_s = cutoff * (1 + skin); 0 = grid search every build."""
+        _check(lib().kreg_ctx_set_candidate_skin(self.h, float(skin)))
+
+    def build_stats(self):
+        out = np.zeros(2, dtype=np.int64)
+        _check(lib().kreg_ctx_build_stats(self.h, _abi.as_ptr(out, C.c_int64)))
+        return {"grid_builds": int(out[0]), "filter_builds": int(out[1])}
+
     def host_stats(self):
         out = np.zeros(8)
         _check(lib().kreg_ctx_host_stats(self.h, _abi.as_ptr(out)))
@@ -213,6 +225,20 @@ class PairList:
 
     def empty(self) -> bool:
         return self.n == 0
+
+    def rebuild(self, T, params: KernelParams, cutoff_multiplier: float, c_min: float) -> "PairList":
+        """build_pairs(X, Z, T, ...) into this list (registration.cpp:126), reusing
+        its candidate list when that provably covers the new list."""
+        t, tp = _t12(T)
+        n = C.c_int64()
+        _check(lib().kreg_rebuild_pairs(self.X.ctx.h, self.h, tp, params.cstruct(), cutoff_multiplier, c_min,
+                                        C.byref(n)))
+        self.n = n.value
+        self.built_at_lengthscale = params.lengthscale
+        self.cutoff_radius = cutoff_multiplier * params.lengthscale
+        self.c_min = c_min
+        self.build_transform = T if isinstance(T, Isometry) else Isometry.from12(T)
+        return self
 
     def info(self) -> dict:
         """Device layout: pairs, sliced-ELL slots (incl. padding), tiles, grid cells."""

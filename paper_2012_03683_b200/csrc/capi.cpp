@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -208,7 +209,24 @@ kreg_status kreg_ctx_create(int32_t device, kreg_ctx** out) {
     KREG_CUDA(cudaEventCreate(&ctx->ev_sweep0));
     KREG_CUDA(cudaEventCreate(&ctx->ev_sweep1));
     ctx->launches_base = kreg_dev::kernel_launch_count();
+    if (const char* sk = std::getenv("KREG_SKIN")) ctx->skin = std::atof(sk);
     *out = ctx.release();
+  });
+}
+
+kreg_status kreg_ctx_set_candidate_skin(kreg_ctx* ctx, double skin) {
+  return guarded([&] {
+    require(ctx != nullptr, "ctx must not be NULL");
+    require(skin >= 0.0 && skin <= 4.0, "candidate skin must lie in [0, 4]");
+    ctx->skin = skin;
+  });
+}
+
+kreg_status kreg_ctx_build_stats(const kreg_ctx* ctx, int64_t out[2]) {
+  return guarded([&] {
+    require(ctx != nullptr && out != nullptr, "NULL argument");
+    out[0] = ctx->full_builds;
+    out[1] = ctx->filter_builds;
   });
 }
 
@@ -291,6 +309,7 @@ kreg_status kreg_ctx_reset_stats(kreg_ctx* ctx) {
     ctx->t_prepare = ctx->t_wait = ctx->t_total = 0.0;
     ctx->t_build_prep = ctx->t_sweep_prep = 0.0;
     ctx->launches_base = kreg_dev::kernel_launch_count();
+    ctx->full_builds = ctx->filter_builds = 0;
   });
 }
 
@@ -315,6 +334,37 @@ kreg_status kreg_build_pairs(kreg_ctx* ctx, const kreg_cloud* X, const kreg_clou
     kreg_pairs* p = build(ctx, X, Z, T, to_params(params), cutoff_multiplier, c_min);
     *out = p;
     if (n_pairs) *n_pairs = p->P;
+  });
+}
+
+kreg_status kreg_rebuild_pairs(kreg_ctx* ctx, kreg_pairs* pairs, const double T[12],
+                               const kreg_kernel_params* params, double cutoff_multiplier, double c_min,
+                               int64_t* n_pairs) {
+  return guarded([&] {
+    require(ctx && pairs && T && params, "NULL argument");
+    require(pairs->X && pairs->Z, "pair list has no clouds");
+    const Params p = to_params(params);
+    check_build_args(pairs->X, pairs->Z, p, cutoff_multiplier, c_min);
+    if (pairs->X->n > 0 && pairs->Z->n > 0) {
+      std::vector<BuildJob> builds(1);
+      builds[0].pairs = pairs;
+      builds[0].X = pairs->X;
+      builds[0].Z = pairs->Z;
+      std::memcpy(builds[0].T, T, sizeof(double) * 12);
+      builds[0].params = p;
+      builds[0].cutoff_multiplier = cutoff_multiplier;
+      builds[0].c_min = c_min;
+      builds[0].disp_hint =
+          pairs->counts_valid ? max_point_displacement_dev(ctx, pairs->Z, pairs->T_build, T) : -1.0;
+      std::vector<EvalJob> none;
+      run_round(ctx, builds, none);
+    } else {
+      pairs->built_at_lengthscale = p.lengthscale;
+      pairs->cutoff_radius = cutoff_multiplier * p.lengthscale;
+      std::memcpy(pairs->T_build, T, sizeof(double) * 12);
+      pairs->P = 0;
+    }
+    if (n_pairs) *n_pairs = pairs->P;
   });
 }
 

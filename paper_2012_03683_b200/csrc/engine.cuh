@@ -64,42 +64,55 @@ struct CoeffParams {
   ChannelDev ch[kMaxChannels];
 };
 
-// One pair-list build (K1 grid + K2 pairs) for one registration.
+// One pair-list build for one registration, in two stages:
+//  candidate stage (full = 1 only): grid over X + 27-cell search at the
+//    enlarged radius R_s = cutoff (1 + skin) around Ts z_j, c_ij and the
+//    c > c_min test -> candidate list {i, log2 c} (sliced ELL, 8 B entries);
+//  filter stage (always): the reference predicate |x_i - T z_j|^2 <= cutoff^2
+//    (inner_product.cpp:69) over the candidate list -> sweep list.
+// The filter is exact while max_j |T z_j - Ts z_j| <= R_s - cutoff (triangle
+// inequality); the kernel checks that bound and flags the build otherwise.
 struct BuildReq {
   const double* xx; const double* xy; const double* xz; const float* xfeat; int n_x;
   const double* zx; const double* zy; const double* zz; const float* zfeat; int n_z;
   double T[12];          // build transform, row-major 3x4
+  int full;              // run the candidate stage first
+  int n_tiles;           // ceil(n_z / 32)
+  // candidate stage
+  double Ts[12];         // candidate-list transform
   double origin[3];      // grid origin (componentwise min of X)
   double inv_h;          // 1 / cell size
   int gx, gy, gz;        // grid dims
   long long n_cells;
-  double cutoff_sq;
+  double sup_cutoff_sq;  // R_s^2
   int* cell_count;       // n_cells (all zero between builds)
   int* cell_start;       // n_cells + 1
   int* cell_of;          // n_x
   int* tmp_items;        // n_x
   int* cell_items;       // n_x
   double* cx; double* cy; double* cz;  // n_x cell-ordered positions
+  long long* scan_tiles; // cell-scan workspace (tile sums)
+  int* sup_count;        // n_z: candidates of every source
+  long long* sup_off;    // n_tiles + 1: candidate tile offsets (entries)
+  int2* sup;             // sup_capacity entries {i, float_as_int(log2 c)}
+  long long sup_capacity;
+  CoeffParams cp;
+  // filter stage
+  double cutoff_sq;
+  double filter_limit_sq;  // (R_s - cutoff)^2 (minus rounding margin)
   int* count;            // n_z: degree of every source
-  long long* offsets;    // n_z + 1: CSR offsets (pair count, export)
-  int n_tiles;           // ceil(n_z / 32)
-  int* tile_deg;         // n_tiles: max degree in the tile
-  int* tile_slots;       // n_tiles: 32 * tile_deg
-  int* tile_units;       // n_tiles: ceil(tile_deg / kUnitSteps)
   long long* tile_off;   // n_tiles + 1: sliced-ELL slot offsets
   int* unit_off;         // n_tiles + 1: sweep work-unit offsets
   int* unit_tile;        // capacity / 256 + n_tiles + 1: tile of every work unit
   int4* slots;           // capacity slots {x_i fixed point (3 x int32), float_as_int(log2 c)}
   int* slot_i;           // capacity: target index i of every slot (export / debug only)
   long long capacity;
-  double* status;        // {P, slots > capacity, slots}
-  int4* xq;              // n_x fixed-point X
   double anchor[3];
   double qscale;         // 2^k
-  long long* scan_tiles; // scan workspace (tile sums), 4 modes x scan_stride
-  long long scan_stride;
-  CoeffParams cp;
+  unsigned long long* disp_blk;   // ceil(n_z / 8): per filter block max |T z - Ts z|^2 (bits)
+  double* status;        // kBuildStatus: {P, slots > cap, slots, cand > cap, cand, |T-Ts| disp, invalid, -}
 };
+constexpr int kBuildStatus = 8;
 
 // One sweep request: M candidate transforms against one pair list.
 struct alignas(16) SweepReq {
@@ -107,7 +120,6 @@ struct alignas(16) SweepReq {
   const long long* tile_off;
   const int* unit_off;
   const int* unit_tile;
-  const int* tile_deg;
   int n_tiles;
   const int4* slots;
   long long capacity;    // slot capacity (an overflowed build is skipped)

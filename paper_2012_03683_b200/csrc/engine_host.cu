@@ -253,48 +253,123 @@ kreg_cloud* cloud_create(kreg_ctx* ctx, const kreg_cloud_view* v) {
 }
 
 // ------------------------------------------------------------ build setup
+static void fill_coeff_params(const BuildJob& job, const kreg_cloud* X, kreg_dev::CoeffParams& cp) {
+  // kernels.cpp:18-53; c_ij does not depend on the geometric lengthscale, so
+  // a candidate list stays valid across annealing levels
+  std::memset(&cp, 0, sizeof(cp));
+  cp.n_channels = static_cast<int>(job.params.per_channel.size());
+  cp.fstride = X->fstride;
+  cp.c_min = static_cast<float>(job.c_min);
+  for (int k = 0; k < cp.n_channels; ++k) {
+    const kreg_channel_params& pc = job.params.per_channel[static_cast<size_t>(k)];
+    kreg_dev::ChannelDev& ch = cp.ch[k];
+    ch.offset = X->chan_off[static_cast<size_t>(k)];
+    ch.dim = X->schema[static_cast<size_t>(k)].dim;
+    ch.linear = pc.form == KREG_FORM_LINEAR ? 1 : 0;
+    ch.kappa = static_cast<float>(-1.4426950408889634 / (2.0 * pc.lengthscale * pc.lengthscale));
+    ch.sigma2 = static_cast<float>(pc.sigma * pc.sigma);
+  }
+}
+
 static void prepare_build(kreg_ctx* ctx, BuildJob& job, kreg_dev::BuildReq& R) {
   kreg_pairs* p = job.pairs;
   const kreg_cloud* X = job.X;
   const kreg_cloud* Z = job.Z;
+  std::memset(&R, 0, sizeof(R));
+  fill_coeff_params(job, X, R.cp);
+  const double cutoff = job.cutoff_multiplier * job.params.lengthscale;
+
+  // Reuse the resident candidate list when it provably contains every pair
+  // of the new list: max_j |T z_j - Ts z_j| <= sup_disp + disp_hint (triangle
+  // inequality over the list being replaced) and that must fit in R_s - cutoff.
+  const double margin = 1e-9 * p->sup_radius;
+  const bool reuse = !job.force_full && ctx->skin > 0.0 && p->sup_valid && p->sup_X == X && p->sup_Z == Z &&
+                     std::memcmp(&p->sup_cp, &R.cp, sizeof(R.cp)) == 0 && job.disp_hint >= 0.0 &&
+                     p->sup_disp + job.disp_hint + cutoff <= p->sup_radius - 2.0 * margin;
+
   p->ctx = ctx;
   p->X = X;
   p->Z = Z;
   p->built_at_lengthscale = job.params.lengthscale;
-  p->cutoff_radius = job.cutoff_multiplier * job.params.lengthscale;
+  p->cutoff_radius = cutoff;
   p->c_min = job.c_min;
   p->sigma = job.params.sigma;
   p->counts_valid = false;  // until this round's results are read back
   std::memcpy(p->T_build, job.T, sizeof(p->T_build));
 
-  std::memset(&R, 0, sizeof(R));
   R.xx = X->x.ptr; R.xy = X->y.ptr; R.xz = X->z.ptr; R.xfeat = X->feat.ptr; R.n_x = X->n;
   R.zx = Z->x.ptr; R.zy = Z->y.ptr; R.zz = Z->z.ptr; R.zfeat = Z->feat.ptr; R.n_z = Z->n;
   std::memcpy(R.T, job.T, sizeof(R.T));
-  const double cutoff = p->cutoff_radius;
   R.cutoff_sq = cutoff * cutoff;  // inner_product.cpp:59
+  const int nx = X->n, nz = Z->n;
+  const int n_tiles = (nz + 31) / 32;
+  p->n_tiles = n_tiles;
+  R.n_tiles = n_tiles;
 
-  // dense grid over X's bbox; cell >= cutoff (margin keeps the 27-cell
-  // stencil a superset of the FP64 cutoff ball under rounding)
-  double h = cutoff * (1.0 + 1e-7);
-  long long g[3];
-  for (;;) {
-    long long cells = 1;
-    for (int k = 0; k < 3; ++k) {
-      g[k] = X->n ? static_cast<long long>(std::floor((X->hi[k] - X->lo[k]) / h)) + 1 : 1;
-      cells *= g[k];
+  if (!reuse) {
+    R.full = 1;
+    ++ctx->full_builds;
+    ++p->full_builds;
+    const double rs = cutoff * (1.0 + std::max(0.0, ctx->skin));
+    p->sup_valid = false;  // until this round's results are read back
+    p->sup_X = X;
+    p->sup_Z = Z;
+    p->sup_cp = R.cp;
+    p->sup_radius = rs;
+    std::memcpy(p->sup_T, job.T, sizeof(p->sup_T));
+    R.sup_cutoff_sq = rs * rs;
+    // dense grid over X's bbox; cell >= R_s (margin keeps the 27-cell
+    // stencil a superset of the FP64 ball under rounding)
+    double h = rs * (1.0 + 1e-7);
+    long long g[3];
+    for (;;) {
+      long long cells = 1;
+      for (int k = 0; k < 3; ++k) {
+        g[k] = X->n ? static_cast<long long>(std::floor((X->hi[k] - X->lo[k]) / h)) + 1 : 1;
+        cells *= g[k];
+      }
+      if (cells <= kMaxCells) break;
+      h *= 1.25;
     }
-    if (cells <= kMaxCells) break;
-    h *= 1.25;
+    for (int k = 0; k < 3; ++k) R.origin[k] = X->lo[k];
+    R.inv_h = 1.0 / h;
+    R.gx = static_cast<int>(g[0]);
+    R.gy = static_cast<int>(g[1]);
+    R.gz = static_cast<int>(g[2]);
+    R.n_cells = g[0] * g[1] * g[2];
+    p->n_cells = R.n_cells;
+    p->gx = R.gx; p->gy = R.gy; p->gz = R.gz;
+    p->cell_count.ensure(static_cast<size_t>(R.n_cells) + 1, /*zero=*/true);
+    p->cell_start.ensure(static_cast<size_t>(R.n_cells) + 1);
+    p->cell_of.ensure(nx + 1);
+    p->tmp_items.ensure(nx + 1);
+    p->cell_items.ensure(nx + 1);
+    p->cx.ensure(nx + 1);
+    p->cy.ensure(nx + 1);
+    p->cz.ensure(nx + 1);
+    p->scan_tiles.ensure(static_cast<size_t>(R.n_cells / kreg_dev::kScanTile + 4));
+    const long long want = p->expected_sup > 0 ? p->expected_sup : static_cast<long long>(nz) * 160 + 4096;
+    if (p->sup.cap < static_cast<size_t>(want)) p->sup.ensure(static_cast<size_t>(want), false, 1.25);
+    R.cell_count = p->cell_count.ptr;
+    R.cell_start = p->cell_start.ptr;
+    R.cell_of = p->cell_of.ptr;
+    R.tmp_items = p->tmp_items.ptr;
+    R.cell_items = p->cell_items.ptr;
+    R.cx = p->cx.ptr; R.cy = p->cy.ptr; R.cz = p->cz.ptr;
+    R.scan_tiles = p->scan_tiles.ptr;
+  } else {
+    ++ctx->filter_builds;
+    ++p->filter_builds;
   }
-  for (int k = 0; k < 3; ++k) R.origin[k] = X->lo[k];
-  R.inv_h = 1.0 / h;
-  R.gx = static_cast<int>(g[0]);
-  R.gy = static_cast<int>(g[1]);
-  R.gz = static_cast<int>(g[2]);
-  R.n_cells = g[0] * g[1] * g[2];
-  p->n_cells = R.n_cells;
-  p->gx = R.gx; p->gy = R.gy; p->gz = R.gz;
+  p->sup_count.ensure(nz + 1);
+  p->sup_off.ensure(n_tiles + 2);
+  std::memcpy(R.Ts, p->sup_T, sizeof(R.Ts));
+  R.sup_count = p->sup_count.ptr;
+  R.sup_off = p->sup_off.ptr;
+  R.sup = p->sup.ptr;
+  R.sup_capacity = static_cast<long long>(p->sup.cap);
+  const double limit = p->sup_radius - cutoff - margin;
+  R.filter_limit_sq = limit > 0.0 ? limit * limit : 0.0;
 
   // fixed point for the sweep: 2^22 units >= 8.5 l (kernel < 2e-16 beyond,
   // where the 1.5*2^23 conversion saturates) and |x - anchor| < 2^28 units
@@ -310,69 +385,25 @@ static void prepare_build(kreg_ctx* ctx, BuildJob& job, kreg_dev::BuildReq& R) {
   for (int k = 0; k < 3; ++k) R.anchor[k] = p->anchor[k];
   R.qscale = p->qscale;
 
-  // buffers
-  const int nx = X->n, nz = Z->n;
-  p->cell_count.ensure(static_cast<size_t>(R.n_cells) + 1, /*zero=*/true);
-  p->cell_start.ensure(static_cast<size_t>(R.n_cells) + 1);
-  p->cell_of.ensure(nx + 1);
-  p->tmp_items.ensure(nx + 1);
-  p->cell_items.ensure(nx + 1);
-  p->cx.ensure(nx + 1);
-  p->cy.ensure(nx + 1);
-  p->cz.ensure(nx + 1);
+  // sweep-list buffers
   p->count.ensure(nz + 1);
-  p->offsets.ensure(nz + 2);
-  p->xq.ensure(nx + 1);
-  R.scan_stride = std::max<long long>(R.n_cells, nz) / kreg_dev::kScanTile + 4;
-  p->scan_tiles.ensure(static_cast<size_t>(4 * R.scan_stride));
-  long long want = p->expected_pairs > 0 ? p->expected_pairs : static_cast<long long>(nz) * 96 + 4096;
+  const long long want = p->expected_pairs > 0 ? p->expected_pairs : static_cast<long long>(nz) * 96 + 4096;
   if (p->slot_buf.cap < static_cast<size_t>(want)) {
     p->slot_buf.ensure(static_cast<size_t>(want), false, 1.5);
     p->slot_i.ensure(p->slot_buf.cap, false, 1.0);
   }
-  const int n_tiles = (nz + 31) / 32;
-  p->n_tiles = n_tiles;
-  p->tile_deg.ensure(n_tiles + 1);
-  p->tile_slots.ensure(n_tiles + 1);
-  p->tile_units.ensure(n_tiles + 1);
   p->tile_off.ensure(n_tiles + 2);
   p->unit_off.ensure(n_tiles + 2);
   p->unit_tile.ensure(p->slot_buf.cap / (32 * kreg_dev::kUnitSteps) + n_tiles + 2);
-  R.unit_tile = p->unit_tile.ptr;
-  R.n_tiles = n_tiles;
-  R.tile_deg = p->tile_deg.ptr;
-  R.tile_slots = p->tile_slots.ptr;
-  R.tile_units = p->tile_units.ptr;
+  p->disp_blk.ensure(nz / 8 + 2);
+  R.count = p->count.ptr;
   R.tile_off = p->tile_off.ptr;
   R.unit_off = p->unit_off.ptr;
-
-  R.cell_count = p->cell_count.ptr;
-  R.cell_start = p->cell_start.ptr;
-  R.cell_of = p->cell_of.ptr;
-  R.tmp_items = p->tmp_items.ptr;
-  R.cell_items = p->cell_items.ptr;
-  R.cx = p->cx.ptr; R.cy = p->cy.ptr; R.cz = p->cz.ptr;
-  R.count = p->count.ptr;
-  R.offsets = p->offsets.ptr;
+  R.unit_tile = p->unit_tile.ptr;
   R.slots = p->slot_buf.ptr;
   R.slot_i = p->slot_i.ptr;
   R.capacity = static_cast<long long>(p->slot_buf.cap);
-  R.xq = p->xq.ptr;
-  R.scan_tiles = p->scan_tiles.ptr;
-
-  // coefficient params (kernels.cpp:18-53)
-  R.cp.n_channels = static_cast<int>(job.params.per_channel.size());
-  R.cp.fstride = X->fstride;
-  R.cp.c_min = static_cast<float>(job.c_min);
-  for (int k = 0; k < R.cp.n_channels; ++k) {
-    const kreg_channel_params& cp = job.params.per_channel[static_cast<size_t>(k)];
-    kreg_dev::ChannelDev& ch = R.cp.ch[k];
-    ch.offset = X->chan_off[static_cast<size_t>(k)];
-    ch.dim = X->schema[static_cast<size_t>(k)].dim;
-    ch.linear = cp.form == KREG_FORM_LINEAR ? 1 : 0;
-    ch.kappa = static_cast<float>(-1.4426950408889634 / (2.0 * cp.lengthscale * cp.lengthscale));
-    ch.sigma2 = static_cast<float>(cp.sigma * cp.sigma);
-  }
+  R.disp_blk = p->disp_blk.ptr;
 }
 
 // Scratch of request e lives in per-round arenas of the context (several
@@ -401,7 +432,6 @@ static void prepare_sweep(kreg_ctx* ctx, EvalJob& job, kreg_dev::SweepReq& R, co
   R.tile_off = p->tile_off.ptr;
   R.unit_off = p->unit_off.ptr;
   R.unit_tile = p->unit_tile.ptr;
-  R.tile_deg = p->tile_deg.ptr;
   R.n_tiles = p->n_tiles;
   R.slots = p->slot_buf.ptr;
   R.capacity = static_cast<long long>(p->slot_buf.cap);
@@ -433,13 +463,14 @@ void run_round(kreg_ctx* ctx, std::vector<BuildJob>& builds, std::vector<EvalJob
   ctx->d_build.ensure(nb + 1);
   ctx->h_sweep.ensure(ne + 1);
   ctx->d_sweep.ensure(ne + 1);
-  const size_t n_res = static_cast<size_t>(ne) * kreg_dev::kMaxCandidates * kreg_dev::kOut + 4 * nb + 4;
+  const size_t n_res = static_cast<size_t>(ne) * kreg_dev::kMaxCandidates * kreg_dev::kOut + kreg_dev::kBuildStatus * (nb + 1);
   ctx->d_results.ensure(n_res);
   ctx->h_results.ensure(n_res);
 
   for (int b = 0; b < nb; ++b) {
     prepare_build(ctx, builds[b], ctx->h_build.ptr[b]);
-    ctx->h_build.ptr[b].status = ctx->d_results.ptr + static_cast<size_t>(ne) * kreg_dev::kMaxCandidates * kreg_dev::kOut + 4 * b;
+    ctx->h_build.ptr[b].status = ctx->d_results.ptr + static_cast<size_t>(ne) * kreg_dev::kMaxCandidates * kreg_dev::kOut +
+                                    kreg_dev::kBuildStatus * b;
   }
   const auto tb = clk::now();
   ctx->t_build_prep += std::chrono::duration<double>(tb - t0).count();
@@ -490,19 +521,47 @@ void run_round(kreg_ctx* ctx, std::vector<BuildJob>& builds, std::vector<EvalJob
   const double* res = ctx->h_results.ptr;
   std::vector<int> redo;
   for (int b = 0; b < nb; ++b) {
-    const double* st = res + static_cast<size_t>(ne) * kreg_dev::kMaxCandidates * kreg_dev::kOut + 4 * b;
-    builds[b].pairs->P = static_cast<long long>(st[0]);
-    builds[b].pairs->slots = static_cast<long long>(st[2]);
-    builds[b].pairs->counts_valid = st[1] == 0.0;
+    const double* st =
+        res + static_cast<size_t>(ne) * kreg_dev::kMaxCandidates * kreg_dev::kOut + kreg_dev::kBuildStatus * b;
+    BuildJob& job = builds[b];
+    kreg_pairs* p = job.pairs;
+    const bool full = ctx->h_build.ptr[b].full != 0;
+    bool ok = true;
+    if (full) {
+      p->sup_entries = static_cast<long long>(st[4]);
+      if (st[3] != 0.0) {  // candidate list overflowed: grow, rebuild from the grid
+        p->expected_sup = static_cast<long long>(st[4] * 1.15) + 4096;
+        job.force_full = true;
+        ok = false;
+      } else {
+        p->sup_valid = true;
+        p->sup_disp = 0.0;  // built at T: a re-run may filter it
+        job.disp_hint = 0.0;
+        p->expected_sup = std::max(p->expected_sup, p->sup_entries);
+      }
+    }
+    if (ok && st[6] != 0.0) {  // candidate radius did not cover the move (rounding guard)
+      p->sup_valid = false;
+      job.force_full = true;
+      ok = false;
+    }
+    p->P = static_cast<long long>(st[0]);
+    p->slots = static_cast<long long>(st[2]);
     if (st[1] != 0.0) {
-      builds[b].pairs->expected_pairs = static_cast<long long>(st[2] * 1.15) + 1024;
-      redo.push_back(b);
+      p->expected_pairs = static_cast<long long>(st[2] * 1.15) + 1024;
+      ok = false;
     } else {
-      builds[b].pairs->expected_pairs = std::max(builds[b].pairs->expected_pairs, builds[b].pairs->slots);
+      p->expected_pairs = std::max(p->expected_pairs, p->slots);
+    }
+    p->counts_valid = ok;
+    if (ok) {
+      p->sup_disp = st[5];
+    } else {
+      redo.push_back(b);
     }
   }
   if (!redo.empty()) {
-    // grow and re-run the overflowed builds and every evaluation in this round
+    // grow and re-run the failed builds and every evaluation in this round
     std::vector<BuildJob> b2;
     for (int b : redo) b2.push_back(builds[b]);
     run_round(ctx, b2, evals);
@@ -547,13 +606,12 @@ double max_point_displacement_dev(kreg_ctx* ctx, const kreg_cloud* Z, const doub
 void pairs_export(kreg_ctx* ctx, const kreg_pairs* p, int64_t* offsets, int32_t* x_index, double* coeff) {
   // reference layout: CSR by ORIGINAL source index j, ascending ORIGINAL i
   const int nz = p->Z ? p->Z->n : 0;
-  std::vector<long long> off(static_cast<size_t>(nz) + 1, 0);
+  std::vector<int> deg(static_cast<size_t>(nz) + 1, 0);
   std::vector<long long> toff(static_cast<size_t>(p->n_tiles) + 1, 0);
   std::vector<int4> sl(static_cast<size_t>(p->slots));
   std::vector<int> si(static_cast<size_t>(p->slots));
   if (nz) {
-    KREG_CUDA(cudaMemcpyAsync(off.data(), p->offsets.ptr, sizeof(long long) * (nz + 1), cudaMemcpyDeviceToHost,
-                              ctx->stream));
+    KREG_CUDA(cudaMemcpyAsync(deg.data(), p->count.ptr, sizeof(int) * nz, cudaMemcpyDeviceToHost, ctx->stream));
     KREG_CUDA(cudaMemcpyAsync(toff.data(), p->tile_off.ptr, sizeof(long long) * (p->n_tiles + 1),
                               cudaMemcpyDeviceToHost, ctx->stream));
     if (p->slots) {
@@ -564,7 +622,7 @@ void pairs_export(kreg_ctx* ctx, const kreg_pairs* p, int64_t* offsets, int32_t*
     KREG_CUDA(cudaStreamSynchronize(ctx->stream));
   }
   std::vector<long long> cnt(static_cast<size_t>(nz), 0);
-  for (int js = 0; js < nz; ++js) cnt[static_cast<size_t>(p->Z->order[js])] = off[js + 1] - off[js];
+  for (int js = 0; js < nz; ++js) cnt[static_cast<size_t>(p->Z->order[js])] = deg[js];
   offsets[0] = 0;
   for (int j = 0; j < nz; ++j) offsets[j + 1] = offsets[j] + cnt[static_cast<size_t>(j)];
   std::vector<std::pair<int, double>> tmp;
@@ -572,7 +630,7 @@ void pairs_export(kreg_ctx* ctx, const kreg_pairs* p, int64_t* offsets, int32_t*
     const int j = p->Z->order[js];
     tmp.clear();
     const long long col = toff[static_cast<size_t>(js >> 5)] + (js & 31);  // sliced-ELL column of js
-    for (long long k = 0; k < off[js + 1] - off[js]; ++k) {
+    for (long long k = 0; k < deg[js]; ++k) {
       const size_t at = static_cast<size_t>(col + 32 * k);
       float lc;
       std::memcpy(&lc, &sl[at].w, sizeof(float));

@@ -125,6 +125,9 @@ struct kreg_ctx {
   // pair-list workspaces kept across registrations (device buffers keep capacity)
   std::vector<kreg_pairs*> pool;
   int max_active = 0;  // lockstep window of kreg_register_batch (0 = all at once)
+  // candidate-list radius R_s = cutoff (1 + skin); 0 disables reuse
+  double skin = 0.25;
+  long long full_builds = 0, filter_builds = 0;
   // host-side round accounting (seconds)
   long long rounds = 0;
   double t_prepare = 0.0, t_wait = 0.0, t_total = 0.0;
@@ -160,22 +163,40 @@ struct kreg_pairs {
   double T_build[12] = {1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1, 0};
   long long P = 0;           // valid after the build round completed
   double sigma = 1.0;
-  // grid
+  // grid (candidate stage)
   long long n_cells = 0;
   int gx = 0, gy = 0, gz = 0;
-  kreg_host::DevBuf<int> cell_count, cell_start, cell_of, tmp_items, cell_items, count;
+  kreg_host::DevBuf<int> cell_count, cell_start, cell_of, tmp_items, cell_items;
   kreg_host::DevBuf<double> cx, cy, cz;
-  kreg_host::DevBuf<long long> offsets, scan_tiles, tile_off;
+  kreg_host::DevBuf<long long> scan_tiles;
+  // candidate list: pairs within R_s = cutoff (1 + skin) of Ts z_j with c > c_min
+  kreg_host::DevBuf<int2> sup;             // per tile: 32 rows of H_t entries {i, log2 c}
+  kreg_host::DevBuf<int> sup_count;
+  kreg_host::DevBuf<long long> sup_off;
+  bool sup_valid = false;                  // a complete candidate list is resident
+  const kreg_cloud* sup_X = nullptr;
+  const kreg_cloud* sup_Z = nullptr;
+  kreg_dev::CoeffParams sup_cp{};          // coefficient parameters it was built with
+  double sup_T[12] = {1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1, 0};
+  double sup_radius = 0.0;                 // R_s
+  double sup_disp = 0.0;                   // max_j |T_build z_j - sup_T z_j|
+  long long sup_entries = 0;
+  long long expected_sup = 0;              // capacity hint
+  // sweep list
+  kreg_host::DevBuf<int> count;            // degree per source (sorted order)
+  kreg_host::DevBuf<long long> tile_off;
   kreg_host::DevBuf<int4> slot_buf;        // sliced-ELL slots {x fixed point, log2 c}
   kreg_host::DevBuf<int> slot_i;           // target index per slot (export only)
-  kreg_host::DevBuf<int> tile_deg, tile_slots, tile_units, unit_off, unit_tile;
+  kreg_host::DevBuf<int> unit_off, unit_tile;
+  kreg_host::DevBuf<unsigned long long> disp_blk;
   int n_tiles = 0;
   long long slots = 0;                     // valid after the build round
   bool counts_valid = false;               // P / slots known on the host
-  kreg_host::DevBuf<int4> xq;
   double anchor[3] = {0, 0, 0};
   double qscale = 1.0;
   long long expected_pairs = 0;  // capacity hint
+  // statistics
+  long long full_builds = 0, filter_builds = 0;
 };
 
 namespace kreg_host {
@@ -201,6 +222,10 @@ struct BuildJob {
   Params params;       // lengthscale = the build lengthscale
   double cutoff_multiplier;
   double c_min;
+  // max_j |T z_j - T_build z_j| against the list being replaced (< 0:
+  // unknown); lets the build reuse the resident candidate list
+  double disp_hint = -1.0;
+  bool force_full = false;
 };
 
 // One evaluation request: M (<= 8) transforms against a built pair list.

@@ -73,11 +73,14 @@ __device__ V block_excl_scan(V v, V* total) {
 }
 
 // ------------------------------------------------------------------ K1
-// Cell id + occupancy count + fixed-point copy of X for the sweep.
+constexpr int kUnitSlots = 32 * kUnitSteps;  // slots per sweep work unit
+
+// Candidate stage, grid over X (requests with full == 0 exit at once).
+// Cell id + occupancy count.
 __global__ void k_cell_assign(const BuildReq* reqs) {
   const BuildReq& R = reqs[blockIdx.y];
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= R.n_x) return;
+  if (!R.full || i >= R.n_x) return;
   const double x = R.xx[i], y = R.xy[i], z = R.xz[i];
   // hash_grid.hpp:41-43: floor((p - origin) / cell)
   long long cx = (long long)floor((x - R.origin[0]) * R.inv_h);
@@ -89,9 +92,6 @@ __global__ void k_cell_assign(const BuildReq* reqs) {
   const int cell = (int)((cz * R.gy + cy) * R.gx + cx);
   R.cell_of[i] = cell;
   atomicAdd(&R.cell_count[cell], 1);
-  R.xq[i] = make_int4(__double2int_rn((x - R.anchor[0]) * R.qscale),
-                      __double2int_rn((y - R.anchor[1]) * R.qscale),
-                      __double2int_rn((z - R.anchor[2]) * R.qscale), 0);
 }
 
 // Scatter into cell ranges (arbitrary order inside a cell); the count array
@@ -99,7 +99,7 @@ __global__ void k_cell_assign(const BuildReq* reqs) {
 __global__ void k_scatter(const BuildReq* reqs) {
   const BuildReq& R = reqs[blockIdx.y];
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= R.n_x) return;
+  if (!R.full || i >= R.n_x) return;
   const int cell = R.cell_of[i];
   const int slot = atomicSub(&R.cell_count[cell], 1) - 1;
   R.tmp_items[R.cell_start[cell] + slot] = i;
@@ -109,7 +109,7 @@ __global__ void k_scatter(const BuildReq* reqs) {
 __global__ void k_rank(const BuildReq* reqs) {
   const BuildReq& R = reqs[blockIdx.y];
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= R.n_x) return;
+  if (!R.full || s >= R.n_x) return;
   const int i = R.tmp_items[s];
   const int cell = R.cell_of[i];
   const int b = R.cell_start[cell], e = R.cell_start[cell + 1];
@@ -122,100 +122,61 @@ __global__ void k_rank(const BuildReq* reqs) {
   R.cz[dst] = R.xz[i];
 }
 
-// --------------------------------------------------- batched exclusive scan
-// mode 0: cell_count (int32, n_cells) -> cell_start (int32, n_cells + 1)
-// mode 1: count      (int32, n_z)     -> offsets    (int64, n_z + 1)
-// mode 2: tile_slots (int32, n_tiles) -> tile_off   (int64, n_tiles + 1)
-// mode 3: tile_units (int32, n_tiles) -> unit_off   (int32, n_tiles + 1)
-struct ScanView {
-  const int* in;
-  long long n;
-  int* out32;
-  long long* out64;
-  long long* tiles;
-};
-
-__device__ __forceinline__ ScanView scan_view(const BuildReq& R, int mode) {
-  ScanView v;
-  v.out32 = nullptr;
-  v.out64 = nullptr;
-  if (mode == 0) {
-    v.in = R.cell_count; v.n = R.n_cells; v.out32 = R.cell_start;
-  } else if (mode == 1) {
-    v.in = R.count; v.n = R.n_z; v.out64 = R.offsets;
-  } else if (mode == 2) {
-    v.in = R.tile_slots; v.n = R.n_tiles; v.out64 = R.tile_off;
-  } else {
-    v.in = R.tile_units; v.n = R.n_tiles; v.out32 = R.unit_off;
-  }
-  v.tiles = R.scan_tiles + (long long)mode * R.scan_stride;
-  return v;
-}
-
+// ---------------------------------------- exclusive scan of the cell counts
+// cell_count (int32, n_cells) -> cell_start (int32, n_cells + 1), three
+// launches (tile sums, tile prefix, apply) over 2048-cell tiles.
 constexpr int kScanThreads = 256;
 constexpr int kScanPerThread = kScanTile / kScanThreads;
 
-__global__ void k_scan_tiles(const BuildReq* reqs, int mode) {
-  const ScanView v = scan_view(reqs[blockIdx.y], mode);
+__global__ void k_scan_tiles(const BuildReq* reqs) {
+  const BuildReq& R = reqs[blockIdx.y];
   const long long base = (long long)blockIdx.x * kScanTile;
-  if (base >= v.n) return;
+  if (!R.full || base >= R.n_cells) return;
   long long s = 0;
   for (int k = 0; k < kScanPerThread; ++k) {
     const long long idx = base + (long long)k * kScanThreads + threadIdx.x;
-    if (idx < v.n) s += v.in[idx];
+    if (idx < R.n_cells) s += R.cell_count[idx];
   }
   long long tot;
   block_excl_scan<long long>(s, &tot);
-  if (threadIdx.x == 0) v.tiles[blockIdx.x] = tot;
+  if (threadIdx.x == 0) R.scan_tiles[blockIdx.x] = tot;
 }
 
-__global__ void k_scan_tile_prefix(const BuildReq* reqs, int mode) {
-  const ScanView v = scan_view(reqs[blockIdx.x], mode);
-  const long long nt = (v.n + kScanTile - 1) / kScanTile;
+__global__ void k_scan_tile_prefix(const BuildReq* reqs) {
+  const BuildReq& R = reqs[blockIdx.x];
+  if (!R.full) return;
+  const long long nt = (R.n_cells + kScanTile - 1) / kScanTile;
   long long carry = 0;
   for (long long b = 0; b < nt; b += blockDim.x) {
     const long long t = b + threadIdx.x;
-    const long long val = t < nt ? v.tiles[t] : 0;
+    const long long val = t < nt ? R.scan_tiles[t] : 0;
     long long tot;
     const long long ex = block_excl_scan<long long>(val, &tot);
-    if (t < nt) v.tiles[t] = carry + ex;
+    if (t < nt) R.scan_tiles[t] = carry + ex;
     carry += tot;
   }
-  if (threadIdx.x == 0) {
-    const BuildReq& R = reqs[blockIdx.x];
-    if (v.out32) v.out32[v.n] = (int)carry;
-    else v.out64[v.n] = carry;
-    if (mode == 1) R.status[0] = (double)carry;  // pairs
-    if (mode == 2) {                               // sliced-ELL slots (incl. padding)
-      R.status[1] = carry > R.capacity ? 1.0 : 0.0;
-      R.status[2] = (double)carry;
-    }
-  }
+  if (threadIdx.x == 0) R.cell_start[R.n_cells] = (int)carry;
 }
 
-__global__ void k_scan_apply(const BuildReq* reqs, int mode) {
-  const ScanView v = scan_view(reqs[blockIdx.y], mode);
+__global__ void k_scan_apply(const BuildReq* reqs) {
+  const BuildReq& R = reqs[blockIdx.y];
   const long long base = (long long)blockIdx.x * kScanTile;
-  if (base >= v.n) return;
-  // thread-contiguous segment of kScanPerThread elements
+  if (!R.full || base >= R.n_cells) return;
   const long long seg = base + (long long)threadIdx.x * kScanPerThread;
-  long long vals[kScanPerThread];
+  int vals[kScanPerThread];
   long long s = 0;
 #pragma unroll
   for (int k = 0; k < kScanPerThread; ++k) {
     const long long idx = seg + k;
-    vals[k] = idx < v.n ? v.in[idx] : 0;
+    vals[k] = idx < R.n_cells ? R.cell_count[idx] : 0;
     s += vals[k];
   }
   long long tot;
-  long long run = block_excl_scan<long long>(s, &tot) + v.tiles[blockIdx.x];
+  long long run = block_excl_scan<long long>(s, &tot) + R.scan_tiles[blockIdx.x];
 #pragma unroll
   for (int k = 0; k < kScanPerThread; ++k) {
     const long long idx = seg + k;
-    if (idx < v.n) {
-      if (v.out32) v.out32[idx] = (int)run;
-      else v.out64[idx] = run;
-    }
+    if (idx < R.n_cells) R.cell_start[idx] = (int)run;
     run += vals[k];
   }
 }
@@ -261,18 +222,20 @@ __device__ __forceinline__ bool coefficient(const CoeffParams& cp, const float* 
 
 constexpr int kMaxFeat = 64;  // max padded feature row handled in registers/smem
 
-// One warp per source point j: 27-cell stencil = 9 contiguous x-rows of the
-// dense grid; lanes stride over candidates (coalesced FP64 loads), FP64
-// distance test (kernels.hpp:37-42, inner_product.cpp:69), c_ij, c > c_min.
-// EMIT=false writes count[j]; EMIT=true writes j's pairs in stencil order
-// into its sliced-ELL column: slot(k) = tile_off[j/32] + 32 k + (j%32), and
-// pads the column to the tile's max degree with {0, -inf} (w = 0).
+// Candidate search, one warp per source point j: the 27-cell stencil around
+// Ts z_j is 9 contiguous x-rows of the dense grid; lanes stride over the
+// candidates (coalesced FP64 loads), FP64 distance test against R_s
+// (kernels.hpp:37-42, inner_product.cpp:69), c_ij, c > c_min (:73).
+// EMIT=false writes sup_count[j]; EMIT=true writes j's candidates in stencil
+// order, contiguously: tile t = j/32 owns 32 rows of H_t entries (H_t = max
+// candidates in the tile), entry(j, k) = sup_off[t] + (j%32) H_t + k.
 template <bool EMIT>
 __global__ void __launch_bounds__(256) k_pair_pass(const BuildReq* reqs) {
   const BuildReq& R = reqs[blockIdx.y];
   const int lane = threadIdx.x & 31;
   const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (j >= R.n_z) return;
+  if (!R.full || j >= R.n_z) return;
+  if (EMIT && R.sup_off[R.n_tiles] > R.sup_capacity) return;  // host grows and re-runs
   __shared__ __align__(16) float zf_s[8][kMaxFeat];
   float* zf = zf_s[threadIdx.x >> 5];
   const int fs = R.cp.fstride;
@@ -280,15 +243,15 @@ __global__ void __launch_bounds__(256) k_pair_pass(const BuildReq* reqs) {
   __syncwarp();
 
   double qx, qy, qz;
-  apply_T(R.T, R.zx[j], R.zy[j], R.zz[j], qx, qy, qz);
+  apply_T(R.Ts, R.zx[j], R.zy[j], R.zz[j], qx, qy, qz);
   const long long cxl = (long long)floor((qx - R.origin[0]) * R.inv_h);
   const long long cyl = (long long)floor((qy - R.origin[1]) * R.inv_h);
   const long long czl = (long long)floor((qz - R.origin[2]) * R.inv_h);
 
   long long out = 0;
   if (EMIT) {
-    if (R.tile_off[R.n_tiles] > R.capacity) return;  // host grows and re-runs
-    out = R.tile_off[j >> 5] + (j & 31);
+    const long long t0 = R.sup_off[j >> 5], H = (R.sup_off[(j >> 5) + 1] - t0) >> 5;
+    out = t0 + (j & 31) * H;
   }
   int cnt = 0;
   const bool geo = R.cp.n_channels == 0;
@@ -311,7 +274,7 @@ __global__ void __launch_bounds__(256) k_pair_pass(const BuildReq* reqs) {
           int i = 0;
           if (s < s1) {
             const double dx = R.cx[s] - qx, dy2 = R.cy[s] - qy, dz2 = R.cz[s] - qz;
-            if (dx * dx + dy2 * dy2 + dz2 * dz2 <= R.cutoff_sq) {
+            if (dx * dx + dy2 * dy2 + dz2 * dz2 <= R.sup_cutoff_sq) {
               i = R.cell_items[s];
               keep = geo ? true : coefficient(R.cp, R.xfeat + (long long)i * fs, zf, &lc);
             }
@@ -319,55 +282,171 @@ __global__ void __launch_bounds__(256) k_pair_pass(const BuildReq* reqs) {
           const unsigned m = __ballot_sync(0xffffffffu, keep);
           if (EMIT && keep) {
             const int pos = __popc(m & ((1u << lane) - 1u));
-            const long long at = out + 32LL * (cnt + pos);
-            const int4 x = R.xq[i];
-            R.slots[at] = make_int4(x.x, x.y, x.z, __float_as_int(lc));
-            R.slot_i[at] = i;
+            R.sup[out + cnt + pos] = make_int2(i, __float_as_int(lc));
           }
           cnt += __popc(m);
         }
       }
     }
   }
+  if (!EMIT && lane == 0) R.sup_count[j] = cnt;
+}
+
+// Tile offsets, one block per request (grid.x = requests):
+//  SUP:  candidate list, column height = max candidates in the tile
+//        -> sup_off = 32 x prefix; status[3, 4] = {overflow, entries}.
+//  !SUP: sweep list, column height = max degree rounded up to whole sweep
+//        units of kUnitSteps steps (>= 1 unit so the sweep also visits
+//        isolated sources for their displacement) -> unit_off, tile_off =
+//        kUnitSlots x unit_off, unit_tile[], status {P, overflow, slots,
+//        |T - Ts| displacement, invalid}; resets disp_bits.
+template <bool SUP>
+__global__ void __launch_bounds__(1024) k_tile_offsets(const BuildReq* reqs) {
+  const BuildReq& R = reqs[blockIdx.x];
+  if (SUP && !R.full) return;
+  const int* cnt = SUP ? R.sup_count : R.count;
+  const int nt = R.n_tiles;
+  long long carry = 0, pairs = 0;
+  for (int b = 0; b < nt; b += blockDim.x) {
+    const int t = b + threadIdx.x;
+    long long v = 0;
+    if (t < nt) {
+      const int j0 = 32 * t, j1 = min(R.n_z, j0 + 32);
+      int d = 0;
+      for (int j = j0; j < j1; ++j) {
+        const int c = cnt[j];
+        d = max(d, c);
+        pairs += c;
+      }
+      v = SUP ? d : (d > 0 ? (d + kUnitSteps - 1) / kUnitSteps : 1);
+    }
+    long long tot;
+    const long long ex = carry + block_excl_scan<long long>(v, &tot);
+    if (t < nt) {
+      if (SUP) {
+        R.sup_off[t] = 32 * ex;
+      } else {
+        R.unit_off[t] = (int)ex;
+        R.tile_off[t] = ex * kUnitSlots;
+      }
+    }
+    carry += tot;
+  }
+  long long P;
+  block_excl_scan<long long>(pairs, &P);
+  __shared__ unsigned long long dmax_s;
+  if (!SUP) {  // max |T z - Ts z|^2 over the filter blocks (bit patterns of non-negative doubles)
+    if (threadIdx.x == 0) dmax_s = 0;
+    __syncthreads();
+    unsigned long long d = 0;
+    for (int b = threadIdx.x; b < (R.n_z + 7) / 8; b += blockDim.x) d = R.disp_blk[b] > d ? R.disp_blk[b] : d;
+    atomicMax(&dmax_s, d);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    if (SUP) {
+      R.sup_off[nt] = 32 * carry;
+      R.status[3] = 32 * carry > R.sup_capacity ? 1.0 : 0.0;
+      R.status[4] = (double)(32 * carry);
+    } else {
+      R.unit_off[nt] = (int)carry;
+      R.tile_off[nt] = carry * kUnitSlots;
+      R.status[0] = (double)P;
+      R.status[1] = carry * kUnitSlots > R.capacity ? 1.0 : 0.0;
+      R.status[2] = (double)(carry * kUnitSlots);
+      R.status[5] = sqrt(__longlong_as_double((long long)dmax_s));
+      R.status[6] = __longlong_as_double((long long)dmax_s) > R.filter_limit_sq ? 1.0 : 0.0;
+    }
+  }
+  if (!SUP && carry * kUnitSlots <= R.capacity) {
+    __syncthreads();
+    for (int t = threadIdx.x; t < nt; t += blockDim.x)
+      for (int u = R.unit_off[t]; u < R.unit_off[t + 1]; ++u) R.unit_tile[u] = t;
+  }
+}
+
+// Filter stage, one warp per source j (lanes over its candidate row,
+// coalesced 8-B entries + gathers of x_i from the L2-resident cloud). Applies
+// the reference predicate |x_i - T z_j|^2 <= cutoff^2 in FP64
+// (inner_product.cpp:69) with the same operations as a direct search, so the
+// kept set is exactly the direct build's set whenever the candidate radius
+// covers cutoff + |T z_j - Ts z_j| (checked: COUNT writes the block's max
+// displacement to disp_blk[], k_tile_offsets flags a violation).
+// EMIT=false: count[j]. EMIT=true: j's slots {x_i fixed point, log2 c} in
+// candidate order into its sliced-ELL column (slot(k) = tile_off[t] + 32 k +
+// j%32), padded to the tile's unit-rounded column height.
+template <bool EMIT>
+__global__ void __launch_bounds__(256) k_filter(const BuildReq* reqs) {
+  const BuildReq& R = reqs[blockIdx.y];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int j = blockIdx.x * 8 + wid;
+  const bool sup_ok = R.sup_off[R.n_tiles] <= R.sup_capacity;
+  if (EMIT && (!sup_ok || R.tile_off[R.n_tiles] > R.capacity)) return;  // host grows and re-runs
+  const bool active = j < R.n_z;
+  double qx = 0, qy = 0, qz = 0;
+  if (active) apply_T(R.T, R.zx[j], R.zy[j], R.zz[j], qx, qy, qz);
+  if (!EMIT) {
+    __shared__ unsigned long long dblk[8];
+    unsigned long long d2 = 0;
+    if (active) {
+      double sx, sy, sz;
+      apply_T(R.Ts, R.zx[j], R.zy[j], R.zz[j], sx, sy, sz);
+      const double dx = qx - sx, dy = qy - sy, dz = qz - sz;
+      d2 = (unsigned long long)__double_as_longlong(dx * dx + dy * dy + dz * dz);
+    }
+    if (lane == 0) dblk[wid] = d2;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long m = 0;
+      for (int w = 0; w < 8; ++w) m = dblk[w] > m ? dblk[w] : m;
+      R.disp_blk[blockIdx.x] = m;
+    }
+  }
+  if (!active) return;
+  const int t = j >> 5;
+  int ds = 0;
+  const int2* row = R.sup;
+  if (sup_ok) {
+    ds = R.sup_count[j];
+    const long long t0 = R.sup_off[t], H = (R.sup_off[t + 1] - t0) >> 5;
+    row = R.sup + t0 + (j & 31) * H;
+  }
+  const long long out = EMIT ? R.tile_off[t] + (j & 31) : 0;
+  const double c2 = R.cutoff_sq;
+  int cnt = 0;
+  for (int sb = 0; sb < ds; sb += 32) {
+    const int k = sb + lane;
+    bool keep = false;
+    int2 e = make_int2(0, 0);
+    double x = 0, y = 0, z = 0;
+    if (k < ds) {
+      e = row[k];
+      x = R.xx[e.x];
+      y = R.xy[e.x];
+      z = R.xz[e.x];
+      const double dx = x - qx, dy = y - qy, dz = z - qz;
+      keep = dx * dx + dy * dy + dz * dz <= c2;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    if (EMIT && keep) {
+      const long long at = out + 32LL * (cnt + __popc(m & ((1u << lane) - 1u)));
+      R.slots[at] = make_int4(__double2int_rn((x - R.anchor[0]) * R.qscale),
+                              __double2int_rn((y - R.anchor[1]) * R.qscale),
+                              __double2int_rn((z - R.anchor[2]) * R.qscale), e.y);
+      R.slot_i[at] = e.x;
+    }
+    cnt += __popc(m);
+  }
   if (!EMIT) {
     if (lane == 0) R.count[j] = cnt;
   } else {
-    // pad the column to the tile's (unit-rounded) max degree: w = ex2(-inf) = 0
-    const int dmax = R.tile_deg[j >> 5];
-    for (int k = cnt + lane; k < dmax; k += 32) {
+    // pad the column to the tile's unit-rounded height: w = ex2(-inf) = 0
+    const int height = (R.unit_off[t + 1] - R.unit_off[t]) * kUnitSteps;
+    for (int k = cnt + lane; k < height; k += 32) {
       R.slots[out + 32LL * k] = make_int4(0, 0, 0, __float_as_int(-INFINITY));
       R.slot_i[out + 32LL * k] = -1;
     }
   }
-}
-
-// Per tile of 32 consecutive sources: column height = max degree rounded up
-// to a whole number of sweep units (kUnitSteps degree steps; >= 1 unit so
-// the sweep also visits isolated sources for their displacement). Every unit
-// is then exactly 32 * kUnitSteps contiguous slots: unit u = slots
-// [u * 32 kUnitSteps, (u + 1) * 32 kUnitSteps).
-__global__ void k_tile_sizes(const BuildReq* reqs) {
-  const BuildReq& R = reqs[blockIdx.y];
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  const int t = j >> 5;
-  if (t >= R.n_tiles) return;
-  int d = j < R.n_z ? R.count[j] : 0;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) d = max(d, __shfl_xor_sync(0xffffffffu, d, o));
-  if ((threadIdx.x & 31) == 0) {
-    const int units = d > 0 ? (d + kUnitSteps - 1) / kUnitSteps : 1;
-    R.tile_deg[t] = units * kUnitSteps;
-    R.tile_slots[t] = 32 * kUnitSteps * units;
-    R.tile_units[t] = units;
-  }
-}
-
-// unit -> tile table for the sweep
-__global__ void k_unit_tiles(const BuildReq* reqs) {
-  const BuildReq& R = reqs[blockIdx.y];
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= R.n_tiles || R.tile_off[R.n_tiles] > R.capacity) return;
-  for (int u = R.unit_off[t]; u < R.unit_off[t + 1]; ++u) R.unit_tile[u] = t;
 }
 
 // ------------------------------------------------------------------ K3
@@ -457,7 +536,6 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phas
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-constexpr int kUnitSlots = 32 * kUnitSteps;
 constexpr unsigned kStageBytes = kUnitSlots * sizeof(int4);
 constexpr size_t kSweepSmem = (size_t)(kSweepThreads / 32) * kSweepStages * kStageBytes +
                               (size_t)(kSweepThreads / 32) * kSweepStages * sizeof(unsigned long long);
@@ -740,38 +818,38 @@ __global__ void k_displacement(const double* zx, const double* zy, const double*
 
 // -------------------------------------------------------------- launchers
 void build_pairs_batched(const BuildReq* h, const BuildReq* d, int n, cudaStream_t st) {
-  int max_nx = 0, max_nz = 0;
+  if (n == 0) return;
+  int max_nx = 0, max_nz = 0, n_full = 0;
   long long max_cells = 0;
   for (int r = 0; r < n; ++r) {
-    max_nx = max(max_nx, h[r].n_x);
     max_nz = max(max_nz, h[r].n_z);
+    if (!h[r].full) continue;
+    ++n_full;
+    max_nx = max(max_nx, h[r].n_x);
     max_cells = max(max_cells, h[r].n_cells);
   }
-  if (n == 0) return;
-  const int T = 256;
-  const dim3 gx(max(1, (max_nx + T - 1) / T), n);
-  k_cell_assign<<<gx, T, 0, st>>>(d);
-  const long long cell_tiles = (max_cells + kScanTile - 1) / kScanTile;
-  k_scan_tiles<<<dim3((unsigned)cell_tiles, n), kScanThreads, 0, st>>>(d, 0);
-  k_scan_tile_prefix<<<n, 1024, 0, st>>>(d, 0);
-  k_scan_apply<<<dim3((unsigned)cell_tiles, n), kScanThreads, 0, st>>>(d, 0);
-  k_scatter<<<gx, T, 0, st>>>(d);
-  k_rank<<<gx, T, 0, st>>>(d);
-  const dim3 gz(max(1, (max_nz + 7) / 8), n);
-  k_pair_pass<false><<<gz, 256, 0, st>>>(d);
-  const unsigned z_tiles = (unsigned)max(1, (max_nz + kScanTile - 1) / kScanTile);
-  k_scan_tiles<<<dim3(z_tiles, n), kScanThreads, 0, st>>>(d, 1);
-  k_scan_tile_prefix<<<n, 1024, 0, st>>>(d, 1);
-  k_scan_apply<<<dim3(z_tiles, n), kScanThreads, 0, st>>>(d, 1);
-  k_tile_sizes<<<dim3(max(1, (max_nz + 255) / 256), n), 256, 0, st>>>(d);
-  for (int mode = 2; mode <= 3; ++mode) {
-    k_scan_tiles<<<dim3(z_tiles, n), kScanThreads, 0, st>>>(d, mode);
-    k_scan_tile_prefix<<<n, 1024, 0, st>>>(d, mode);
-    k_scan_apply<<<dim3(z_tiles, n), kScanThreads, 0, st>>>(d, mode);
+  int launches = 0;
+  if (n_full) {  // candidate stage (requests with full == 0 exit at once)
+    const int T = 256;
+    const dim3 gx(max(1, (max_nx + T - 1) / T), n);
+    k_cell_assign<<<gx, T, 0, st>>>(d);
+    const unsigned cell_tiles = (unsigned)max(1LL, (max_cells + kScanTile - 1) / kScanTile);
+    k_scan_tiles<<<dim3(cell_tiles, n), kScanThreads, 0, st>>>(d);
+    k_scan_tile_prefix<<<n, 1024, 0, st>>>(d);
+    k_scan_apply<<<dim3(cell_tiles, n), kScanThreads, 0, st>>>(d);
+    k_scatter<<<gx, T, 0, st>>>(d);
+    k_rank<<<gx, T, 0, st>>>(d);
+    const dim3 gz(max(1, (max_nz + 7) / 8), n);
+    k_pair_pass<false><<<gz, 256, 0, st>>>(d);
+    k_tile_offsets<true><<<n, 1024, 0, st>>>(d);
+    k_pair_pass<true><<<gz, 256, 0, st>>>(d);
+    launches += 9;
   }
-  k_pair_pass<true><<<gz, 256, 0, st>>>(d);
-  k_unit_tiles<<<dim3(max(1, (max_nz / 32 + 256) / 256), n), 256, 0, st>>>(d);
-  count_launch(19);
+  const dim3 gt(max(1, (max_nz + 7) / 8), n);  // warp per source
+  k_filter<false><<<gt, 256, 0, st>>>(d);
+  k_tile_offsets<false><<<n, 1024, 0, st>>>(d);
+  k_filter<true><<<gt, 256, 0, st>>>(d);
+  count_launch(launches + 3);
 }
 
 void sweep_batched(const SweepReq* h, const SweepReq* d, int n, int blocks_per_req, cudaStream_t st,

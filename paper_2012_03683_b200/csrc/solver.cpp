@@ -61,6 +61,7 @@ kreg_pairs* acquire_workspace(kreg_ctx* ctx) {
   p->built_at_lengthscale = 0.0;
   p->cutoff_radius = 0.0;
   p->P = 0;
+  p->sup_valid = false;
   return p;
 }
 
@@ -223,6 +224,9 @@ void schedule_build_eval(Reg& r, std::vector<BuildJob>& builds, std::vector<Eval
   b.params = r.wp;
   b.cutoff_multiplier = r.cfg.cutoff_multiplier;
   b.c_min = r.cfg.c_min;
+  // displacement of T from the current list's build transform (from the
+  // sweep that evaluated T); lets the engine filter its candidate list
+  b.disp_hint = r.phase == Phase::kInit ? -1.0 : r.ev[7];
   builds.push_back(b);
   EvalJob e;
   e.pairs = r.pairs.get();

@@ -149,6 +149,43 @@ def test_kitti_full_size_pairs_and_eval_vs_reference(ctx, ref):
             assert_eval_close([ev.value, *ev.grad], ref.objective_and_gradient(r, X, Z, T, pl))
 
 
+def test_candidate_list_rebuild_is_exact(ctx, ref):
+    """A rebuild that filters the resident candidate list (R_s = cutoff (1 +
+    skin) around the earlier transform) yields exactly the list a grid search
+    at the new transform yields, and the reference's set."""
+    X, Z, Ts = synth.kitti_pair(7, 40000)
+    p = synth.kitti_params()
+    init = synth.perturbed(Ts, 3)
+    c = api.default_context()
+    c.reset_stats()
+    g = api.build_pairs(X, Z, init, p, 3.0, 1e-4)
+    first = c.build_stats()  # (a capacity overflow re-runs the grid search)
+    assert first["grid_builds"] >= 1 and first["filter_builds"] == 0
+    rng = synth.SplitMix64(11)
+    T1 = compose(synth.random_isometry(rng, math.radians(0.05), 0.01), init)  # moves < R_s - cutoff
+    p1 = p.with_lengthscale(0.098)
+    g.rebuild(T1, p1, 3.0, 1e-4)
+    st = c.build_stats()
+    assert st["grid_builds"] == first["grid_builds"] and st["filter_builds"] >= 1
+    fresh = api.build_pairs(X, Z, T1, p1, 3.0, 1e-4)
+    a, b = g.export(), fresh.export()
+    assert g.size() == fresh.size()
+    for u, v in zip(a, b):
+        assert np.array_equal(u, v)
+    r = ref.build_pairs(X, Z, T1, p1, 3.0, 1e-4)
+    assert_pairs_match(a, (r.offsets, r.x_index, r.coeff), X, Z, T1, p1, 3.0, 1e-4)
+    ev_g = api.objective_and_gradient(g, X, Z, T1, p1)
+    assert_eval_close([ev_g.value, *ev_g.grad], ref.objective_and_gradient(r, X, Z, T1, p1))
+    # a move beyond the skin falls back to a grid search
+    T2 = compose(synth.random_isometry(rng, math.radians(2.0), 0.5), T1)
+    before = c.build_stats()
+    g.rebuild(T2, p1, 3.0, 1e-4)
+    assert c.build_stats()["grid_builds"] == before["grid_builds"] + 1
+    fresh2 = api.build_pairs(X, Z, T2, p1, 3.0, 1e-4)
+    for u, v in zip(g.export(), fresh2.export()):
+        assert np.array_equal(u, v)
+
+
 def test_tum_shaped_eval_vs_reference(ctx, ref):
     X, Z, Ts = synth.tum_pair(3, 20000)
     p = synth.tum_params()
