@@ -586,15 +586,15 @@ kreg_status kreg_register_batch_host(kreg_ctx* ctx, int32_t n, const kreg_cloud_
                                      int32_t* statuses) {
   return guarded([&] {
     require(ctx && (n == 0 || (X && Z && initials && results && statuses)), "NULL argument");
-    std::vector<std::unique_ptr<kreg_cloud>> clouds;
-    std::vector<RegJob> jobs(static_cast<size_t>(n));
+    std::vector<const kreg_cloud_view*> views;
     for (int k = 0; k < n; ++k) {
-      clouds.emplace_back(cloud_create(ctx, &X[k]));
-      const kreg_cloud* cx = clouds.back().get();
-      clouds.emplace_back(cloud_create(ctx, &Z[k]));
-      const kreg_cloud* cz = clouds.back().get();
-      make_jobs(cx, cz, initials + 12 * k, params, config, &results[k], jobs[k]);
+      views.push_back(&X[k]);
+      views.push_back(&Z[k]);
     }
+    std::vector<std::unique_ptr<kreg_cloud>> clouds = cloud_create_many(ctx, views.data(), 2 * n);
+    std::vector<RegJob> jobs(static_cast<size_t>(n));
+    for (int k = 0; k < n; ++k)
+      make_jobs(clouds[2 * k].get(), clouds[2 * k + 1].get(), initials + 12 * k, params, config, &results[k], jobs[k]);
     register_many(ctx, jobs);
     for (int k = 0; k < n; ++k) statuses[k] = jobs[k].status;
   });

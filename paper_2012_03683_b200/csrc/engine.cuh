@@ -25,29 +25,24 @@
 
 namespace kreg_dev {
 
-constexpr int kSweepThreads = 256;  // threads per (virtual) sweep block
+constexpr int kSweepThreads = 256;  // threads per persistent sweep CTA (2 CTAs per SM)
 #ifndef KREG_UNIT_STEPS
-#define KREG_UNIT_STEPS 8
+#define KREG_UNIT_STEPS 2
 #endif
-#ifndef KREG_UNITS_PER_BLOCK
-#define KREG_UNITS_PER_BLOCK 32
-#endif
-#ifndef KREG_SWEEP_MIN_BLOCKS
-#define KREG_SWEEP_MIN_BLOCKS 2
-#endif
-constexpr int kUnitSteps = KREG_UNIT_STEPS;              // degree steps per sweep work unit (x 32 lanes)
-constexpr long long kUnitsPerBlock = KREG_UNITS_PER_BLOCK;  // work units per sweep work block
-constexpr int kSweepMinBlocks = KREG_SWEEP_MIN_BLOCKS;    // __launch_bounds__ occupancy hint
 #ifndef KREG_SWEEP_STAGES
-#define KREG_SWEEP_STAGES 2
+#define KREG_SWEEP_STAGES 3
 #endif
-constexpr int kSweepStages = KREG_SWEEP_STAGES;  // per-warp TMA ring depth (units in flight)
-constexpr long long kMaxSweepBlocks = 1184;  // 8 x 148 SMs
+constexpr int kUnitSteps = KREG_UNIT_STEPS;      // degree steps per sweep unit (x 32 lanes x 16 B)
+constexpr int kStageUnits = 4;                   // units per TMA stage (4 KB at 2 steps)
+constexpr int kSweepStages = KREG_SWEEP_STAGES;  // per-warp TMA ring depth (stages)
+constexpr int kMaxChunks = 1184;                 // chunks per request (8 x 148)
+constexpr int kMinChunkUnits = 8;                // >= 2 stages per chunk
+constexpr int kQueueDepth = 8;                   // chunks a warp may hold in its prefetch queue
+constexpr int kMaxSweepReqs = kSweepThreads;     // requests per sweep launch
 constexpr int kMaxChannels = 8;
 constexpr int kMaxCandidates = 8;   // candidate transforms per sweep request
 constexpr int kOut = 8;             // {F, omega[3], v[3], max displacement}
 constexpr int kScanTile = 2048;     // elements per scan tile
-constexpr unsigned kMagic = 0x4B400000u;  // bits of 1.5 * 2^23
 
 struct ChannelDev {
   int offset;     // float offset inside the feature row
@@ -62,6 +57,16 @@ struct CoeffParams {
   int fstride;
   float c_min;
   ChannelDev ch[kMaxChannels];
+};
+
+// Sweep chunk record (written at build time, TMA-loaded with the chunk's
+// first stage): the tile holding the chunk's first unit, the unit where that
+// tile ends, and its 32 sources (degree-sorted order) in FP32.
+struct alignas(16) ChunkRec {
+  int t0;
+  int t0_end;
+  int pad[2];
+  float x[32], y[32], z[32];
 };
 
 // One pair-list build for one registration, in two stages:
@@ -101,14 +106,16 @@ struct BuildReq {
   double cutoff_sq;
   double filter_limit_sq;  // (R_s - cutoff)^2 (minus rounding margin)
   int* count;            // n_z: degree of every source
+  int* perm;             // n_z: source at degree-sorted position p
+  int* pos;              // n_z: degree-sorted position of source j
+  int* deg_s;            // n_z: degree at position p
   long long* tile_off;   // n_tiles + 1: sliced-ELL slot offsets
   int* unit_off;         // n_tiles + 1: sweep work-unit offsets
-  int* unit_tile;        // capacity / 256 + n_tiles + 1: tile of every work unit
-  int4* slots;           // capacity slots {x_i fixed point (3 x int32), float_as_int(log2 c)}
+  float4* zs;            // n_z: sources in degree-sorted order (FP32)
+  ChunkRec* chunks;      // kMaxChunks sweep chunk records
+  int4* slots;           // capacity slots {x_i - T_b z_j (3 x FP32), log2 c (FP32)}
   int* slot_i;           // capacity: target index i of every slot (export / debug only)
   long long capacity;
-  double anchor[3];
-  double qscale;         // 2^k
   unsigned long long* disp_blk;   // ceil(n_z / 8): per filter block max |T z - Ts z|^2 (bits)
   double* status;        // kBuildStatus: {P, slots > cap, slots, cand > cap, cand, |T-Ts| disp, invalid, -}
 };
@@ -119,7 +126,8 @@ struct alignas(16) SweepReq {
   long long units;       // sweep work units when known on the host, else -1
   const long long* tile_off;
   const int* unit_off;
-  const int* unit_tile;
+  const float4* zs;      // sources in degree-sorted order (FP32)
+  const ChunkRec* chunks;
   int n_tiles;
   const int4* slots;
   long long capacity;    // slot capacity (an overflowed build is skipped)
@@ -129,20 +137,22 @@ struct alignas(16) SweepReq {
   int M;
   double T[kMaxCandidates][12];
   double Tb[12];         // pair-list build transform (displacement reference)
+  float Td[kMaxCandidates][12];  // {R_m - R_b, t_m - t_b}: source displacement (T_m - T_b) z
+  float Ta[kMaxCandidates][12];  // {R_m, t_m - anchor}: T_m z - anchor (torque arm)
   double anchor[3];
-  double qscale;         // 2^k
-  float kappa;           // -log2(e) / (2 l^2 qscale^2): ex2 argument per unit^2
+  float kappa;           // -log2(e) / (2 l^2): ex2 argument per m^2
   double sigma2;
   double inv_l2;
-  double* partials;      // kMaxSweepBlocks x M x 7
-  unsigned int* counter; // per request, self-resetting
+  double* partials;      // kMaxChunks x M x (7 | 1)
   unsigned long long* disp_bits;  // M, max squared displacement (self-resetting)
   double* out;           // M x kOut
 };
 
 // All launches go to `stream`; d_reqs are device copies of h_reqs.
 void build_pairs_batched(const BuildReq* h_reqs, const BuildReq* d_reqs, int n, cudaStream_t stream);
-void sweep_batched(const SweepReq* h_reqs, const SweepReq* d_reqs, int n, int blocks_per_req,
+// d_ctl: 2 x ceil(n / kMaxSweepReqs) chunk counters, zero between launches
+// (reset by the reduction kernel).
+void sweep_batched(const SweepReq* h_reqs, const SweepReq* d_reqs, int n, int sm_count, unsigned* d_ctl,
                    cudaStream_t stream, cudaEvent_t sweep_begin, cudaEvent_t sweep_end);
 void displacement(const double* zx, const double* zy, const double* zz, int n, const double* d_T2,
                   unsigned long long* d_out, cudaStream_t stream);

@@ -6,6 +6,7 @@
 #include <cstring>
 #include <numeric>
 #include <sstream>
+#include <thread>
 
 #include "engine_host.hpp"
 
@@ -150,7 +151,8 @@ static uint64_t spread3(uint64_t v) {
   return v;
 }
 
-kreg_cloud* cloud_create(kreg_ctx* ctx, const kreg_cloud_view* v) {
+// Validation + metadata (schema, padded device row layout, diameter, bbox).
+kreg_cloud* cloud_describe(kreg_ctx* ctx, const kreg_cloud_view* v) {
   if (v->n < 0) throw Error(KREG_INVALID_ARGUMENT, "PointCloud: negative point count");
   int total = 0;
   for (int k = 0; k < v->n_channels; ++k) {
@@ -169,37 +171,36 @@ kreg_cloud* cloud_create(kreg_ctx* ctx, const kreg_cloud_view* v) {
        << v->n << " points requires " << static_cast<long long>(v->n) * total;
     throw Error(KREG_INVALID_ARGUMENT, os.str());
   }
-  auto* c = new kreg_cloud;
+  auto c = std::make_unique<kreg_cloud>();
   c->ctx = ctx;
   c->n = v->n;
   c->dim = total;
   // device rows: every channel 16-B aligned and zero-padded to 4k floats
   int padded = 0;
-  std::vector<int> src_off;
-  int so = 0;
   for (int k = 0; k < v->n_channels; ++k) {
     c->schema.push_back({v->channels[k].name, v->channels[k].dim, v->channels[k].kind});
     c->chan_off.push_back(padded);
-    src_off.push_back(so);
     padded += (v->channels[k].dim + 3) / 4 * 4;
-    so += v->channels[k].dim;
   }
   c->fstride = padded;
-  if (padded > 64) {
-    delete c;
-    throw Error(KREG_INVALID_ARGUMENT, "PointCloud: padded feature row > 64 floats is not supported");
-  }
-  const int n = v->n;
-  c->diam = diameter_host(v->xyz, n);
-  if (n > 0) {
+  if (padded > 64) throw Error(KREG_INVALID_ARGUMENT, "PointCloud: padded feature row > 64 floats is not supported");
+  c->diam = diameter_host(v->xyz, v->n);
+  if (v->n > 0) {
     for (int k = 0; k < 3; ++k) c->lo[k] = c->hi[k] = v->xyz[k];
-    for (int i = 1; i < n; ++i)
+    for (int i = 1; i < v->n; ++i)
       for (int k = 0; k < 3; ++k) {
         c->lo[k] = std::min(c->lo[k], v->xyz[3 * i + k]);
         c->hi[k] = std::max(c->hi[k], v->xyz[3 * i + k]);
       }
   }
-  // spatial (Morton) order so that index locality is spatial locality
+  return c.release();
+}
+
+// Host staging: spatial (Morton) order so that index locality is spatial
+// locality; SoA FP64 positions and padded FP32 feature rows written to
+// sx/sy/sz/sf (n, n, n, n * fstride elements; pinned memory for fast DMA).
+void cloud_stage(const kreg_cloud_view* v, kreg_cloud* c, double* sx, double* sy, double* sz, float* sf) {
+  const int n = v->n;
   std::vector<std::pair<uint64_t, int>> keys(static_cast<size_t>(n));
   double span = 0.0;
   for (int k = 0; k < 3; ++k) span = std::max(span, c->hi[k] - c->lo[k]);
@@ -216,40 +217,115 @@ kreg_cloud* cloud_create(kreg_ctx* ctx, const kreg_cloud_view* v) {
   std::sort(keys.begin(), keys.end());
   c->order.resize(static_cast<size_t>(n));
   c->rank.resize(static_cast<size_t>(n));
-  std::vector<double> hx(static_cast<size_t>(n)), hy(static_cast<size_t>(n)), hz(static_cast<size_t>(n));
-  std::vector<float> hf(static_cast<size_t>(n) * c->fstride, 0.0f);
+  std::vector<int> src_off;
+  int so = 0;
+  for (int k = 0; k < v->n_channels; ++k) {
+    src_off.push_back(so);
+    so += v->channels[k].dim;
+  }
+  const int fs = c->fstride, dim = c->dim;
   for (int r = 0; r < n; ++r) {
     const int i = keys[static_cast<size_t>(r)].second;
     c->order[static_cast<size_t>(r)] = i;
     c->rank[static_cast<size_t>(i)] = r;
-    hx[static_cast<size_t>(r)] = v->xyz[3 * i];
-    hy[static_cast<size_t>(r)] = v->xyz[3 * i + 1];
-    hz[static_cast<size_t>(r)] = v->xyz[3 * i + 2];
+    sx[r] = v->xyz[3 * i];
+    sy[r] = v->xyz[3 * i + 1];
+    sz[r] = v->xyz[3 * i + 2];
+    float* row = sf + static_cast<size_t>(r) * fs;
+    for (int d = 0; d < fs; ++d) row[d] = 0.0f;
     for (int k = 0; k < v->n_channels; ++k)
       for (int d = 0; d < v->channels[k].dim; ++d)
-        hf[static_cast<size_t>(r) * c->fstride + c->chan_off[k] + d] =
-            static_cast<float>(v->features[static_cast<size_t>(i) * total + src_off[k] + d]);
+        row[c->chan_off[k] + d] = static_cast<float>(v->features[static_cast<size_t>(i) * dim + src_off[k] + d]);
   }
-  try {
-    KREG_CUDA(cudaSetDevice(ctx->device));
+}
+
+size_t cloud_stage_doubles(const kreg_cloud* c) { return 3 * static_cast<size_t>(c->n); }
+size_t cloud_stage_floats(const kreg_cloud* c) { return static_cast<size_t>(c->n) * c->fstride + 4; }
+
+// Device copies (async on the context stream) into dx/dy/dz/df, or into
+// buffers owned by the cloud when dx == nullptr.
+void cloud_upload(kreg_ctx* ctx, kreg_cloud* c, const double* sx, const double* sy, const double* sz, const float* sf,
+                  double* dx, double* dy, double* dz, float* df) {
+  const int n = c->n;
+  if (dx) {
+    c->x.borrow(dx, n);
+    c->y.borrow(dy, n);
+    c->z.borrow(dz, n);
+    c->feat.borrow(df, cloud_stage_floats(c));
+  } else {
     c->x.ensure(n, false, 1.0);
     c->y.ensure(n, false, 1.0);
     c->z.ensure(n, false, 1.0);
-    c->feat.ensure(static_cast<size_t>(n) * c->fstride + 4, false, 1.0);
-    if (n) {
-      KREG_CUDA(cudaMemcpyAsync(c->x.ptr, hx.data(), sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
-      KREG_CUDA(cudaMemcpyAsync(c->y.ptr, hy.data(), sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
-      KREG_CUDA(cudaMemcpyAsync(c->z.ptr, hz.data(), sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
-      if (c->fstride)
-        KREG_CUDA(cudaMemcpyAsync(c->feat.ptr, hf.data(), sizeof(float) * hf.size(), cudaMemcpyHostToDevice,
-                                  ctx->stream));
-      KREG_CUDA(cudaStreamSynchronize(ctx->stream));  // host staging vectors go out of scope
-    }
-  } catch (...) {
-    delete c;
-    throw;
+    c->feat.ensure(cloud_stage_floats(c), false, 1.0);
   }
-  return c;
+  if (n) {
+    KREG_CUDA(cudaMemcpyAsync(c->x.ptr, sx, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+    KREG_CUDA(cudaMemcpyAsync(c->y.ptr, sy, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+    KREG_CUDA(cudaMemcpyAsync(c->z.ptr, sz, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+    if (c->fstride)
+      KREG_CUDA(cudaMemcpyAsync(c->feat.ptr, sf, sizeof(float) * static_cast<size_t>(n) * c->fstride,
+                                cudaMemcpyHostToDevice, ctx->stream));
+  }
+}
+
+kreg_cloud* cloud_create(kreg_ctx* ctx, const kreg_cloud_view* v) {
+  std::unique_ptr<kreg_cloud> c(cloud_describe(ctx, v));
+  KREG_CUDA(cudaSetDevice(ctx->device));
+  std::vector<double> h(cloud_stage_doubles(c.get()));
+  std::vector<float> f(cloud_stage_floats(c.get()));
+  const int n = c->n;
+  cloud_stage(v, c.get(), h.data(), h.data() + n, h.data() + 2 * n, f.data());
+  cloud_upload(ctx, c.get(), h.data(), h.data() + n, h.data() + 2 * n, f.data(), nullptr, nullptr, nullptr, nullptr);
+  KREG_CUDA(cudaStreamSynchronize(ctx->stream));  // host staging vectors go out of scope
+  return c.release();
+}
+
+// Many clouds at once (end-to-end calls): validation and staging run on host
+// worker threads into pinned context memory, device copies go into one
+// context arena (no per-cloud allocation), all on the context stream.
+std::vector<std::unique_ptr<kreg_cloud>> cloud_create_many(kreg_ctx* ctx, const kreg_cloud_view* const* views,
+                                                           int n) {
+  std::vector<std::unique_ptr<kreg_cloud>> out(static_cast<size_t>(n));
+  for (int k = 0; k < n; ++k) out[k].reset(cloud_describe(ctx, views[k]));
+  std::vector<size_t> doff(static_cast<size_t>(n) + 1, 0), foff(static_cast<size_t>(n) + 1, 0);
+  for (int k = 0; k < n; ++k) {
+    doff[k + 1] = doff[k] + (cloud_stage_doubles(out[k].get()) + 1) / 2 * 2;  // 16-B aligned slices
+    foff[k + 1] = foff[k] + (cloud_stage_floats(out[k].get()) + 3) / 4 * 4;
+  }
+  KREG_CUDA(cudaSetDevice(ctx->device));
+  KREG_CUDA(cudaStreamSynchronize(ctx->stream));  // staging / arena may still be in use
+  ctx->stage_d.ensure(doff[n] + 2);
+  ctx->stage_f.ensure(foff[n] + 4);
+  ctx->arena_d.ensure(doff[n] + 2, false, 1.25);
+  ctx->arena_f.ensure(foff[n] + 4, false, 1.25);
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const int workers = static_cast<int>(std::min<unsigned>(std::min<unsigned>(hw, 32u), static_cast<unsigned>(n)));
+  std::vector<std::exception_ptr> err(static_cast<size_t>(std::max(workers, 1)));
+  auto work = [&](int w) {
+    try {
+      for (int k = w; k < n; k += workers) {
+        const int m = out[k]->n;
+        double* d = ctx->stage_d.ptr + doff[k];
+        cloud_stage(views[k], out[k].get(), d, d + m, d + 2 * m, ctx->stage_f.ptr + foff[k]);
+      }
+    } catch (...) {
+      err[static_cast<size_t>(w)] = std::current_exception();
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int w = 1; w < workers; ++w) pool.emplace_back(work, w);
+  if (workers > 0) work(0);
+  for (auto& t : pool) t.join();
+  for (auto& e : err)
+    if (e) std::rethrow_exception(e);
+  for (int k = 0; k < n; ++k) {
+    const int m = out[k]->n;
+    const double* d = ctx->stage_d.ptr + doff[k];
+    double* a = ctx->arena_d.ptr + doff[k];
+    cloud_upload(ctx, out[k].get(), d, d + m, d + 2 * m, ctx->stage_f.ptr + foff[k], a, a + m, a + 2 * m,
+                 ctx->arena_f.ptr + foff[k]);
+  }
+  return out;
 }
 
 // ------------------------------------------------------------ build setup
@@ -348,7 +424,7 @@ static void prepare_build(kreg_ctx* ctx, BuildJob& job, kreg_dev::BuildReq& R) {
     p->cy.ensure(nx + 1);
     p->cz.ensure(nx + 1);
     p->scan_tiles.ensure(static_cast<size_t>(R.n_cells / kreg_dev::kScanTile + 4));
-    const long long want = p->expected_sup > 0 ? p->expected_sup : static_cast<long long>(nz) * 160 + 4096;
+    const long long want = p->expected_sup > 0 ? p->expected_sup : static_cast<long long>(nz) * 256 + 4096;
     if (p->sup.cap < static_cast<size_t>(want)) p->sup.ensure(static_cast<size_t>(want), false, 1.25);
     R.cell_count = p->cell_count.ptr;
     R.cell_start = p->cell_start.ptr;
@@ -371,22 +447,21 @@ static void prepare_build(kreg_ctx* ctx, BuildJob& job, kreg_dev::BuildReq& R) {
   const double limit = p->sup_radius - cutoff - margin;
   R.filter_limit_sq = limit > 0.0 ? limit * limit : 0.0;
 
-  // fixed point for the sweep: 2^22 units >= 8.5 l (kernel < 2e-16 beyond,
-  // where the 1.5*2^23 conversion saturates) and |x - anchor| < 2^28 units
-  double maxabs = 1e-3;
-  for (int k = 0; k < 3; ++k) {
-    p->anchor[k] = 0.5 * (X->lo[k] + X->hi[k]);
-    maxabs = std::max(maxabs, std::max(X->hi[k] - p->anchor[k], p->anchor[k] - X->lo[k]));
-  }
-  const int k1 = static_cast<int>(std::floor(std::log2(4194304.0 / (8.5 * job.params.lengthscale))));
-  const int k2 = static_cast<int>(std::floor(std::log2(268435456.0 / (maxabs * 1.0001))));
-  const int kq = std::max(-30, std::min(std::min(k1, k2), 40));
-  p->qscale = std::ldexp(1.0, kq);
-  for (int k = 0; k < 3; ++k) R.anchor[k] = p->anchor[k];
-  R.qscale = p->qscale;
+  // torque arm origin of the sweep (FP32 arms T z - anchor stay small)
+  for (int k = 0; k < 3; ++k) p->anchor[k] = 0.5 * (X->lo[k] + X->hi[k]);
 
   // sweep-list buffers
-  p->count.ensure(nz + 1);
+  p->count.ensure(nz + 4);
+  p->perm.ensure(nz + 1);
+  p->pos.ensure(nz + 1);
+  p->deg_s.ensure(nz + 1);
+  p->zs.ensure(nz + 1);
+  p->chunks.ensure(kreg_dev::kMaxChunks + 1);
+  R.perm = p->perm.ptr;
+  R.pos = p->pos.ptr;
+  R.deg_s = p->deg_s.ptr;
+  R.zs = p->zs.ptr;
+  R.chunks = p->chunks.ptr;
   const long long want = p->expected_pairs > 0 ? p->expected_pairs : static_cast<long long>(nz) * 96 + 4096;
   if (p->slot_buf.cap < static_cast<size_t>(want)) {
     p->slot_buf.ensure(static_cast<size_t>(want), false, 1.5);
@@ -394,12 +469,10 @@ static void prepare_build(kreg_ctx* ctx, BuildJob& job, kreg_dev::BuildReq& R) {
   }
   p->tile_off.ensure(n_tiles + 2);
   p->unit_off.ensure(n_tiles + 2);
-  p->unit_tile.ensure(p->slot_buf.cap / (32 * kreg_dev::kUnitSteps) + n_tiles + 2);
   p->disp_blk.ensure(nz / 8 + 2);
   R.count = p->count.ptr;
   R.tile_off = p->tile_off.ptr;
   R.unit_off = p->unit_off.ptr;
-  R.unit_tile = p->unit_tile.ptr;
   R.slots = p->slot_buf.ptr;
   R.slot_i = p->slot_i.ptr;
   R.capacity = static_cast<long long>(p->slot_buf.cap);
@@ -413,15 +486,13 @@ struct SweepScratch {
 };
 
 static long long sweep_units(const kreg_pairs* p) {
-  // every sweep unit is exactly 32 * kUnitSteps slots (k_tile_sizes); before
-  // the build round has been read back use the capacity bound
-  if (p->counts_valid) return p->slots / (32LL * kreg_dev::kUnitSteps);
-  return static_cast<long long>(p->slot_buf.cap) / (32 * kreg_dev::kUnitSteps) + p->n_tiles + 1;
+  // every sweep unit is exactly 32 * kUnitSteps slots (k_tile_offsets)
+  return p->slots / (32LL * kreg_dev::kUnitSteps);
 }
 
-static size_t sweep_nvb_cap(const EvalJob& job) {
-  const long long b = sweep_units(job.pairs) / kreg_dev::kUnitsPerBlock + 1;
-  return static_cast<size_t>(std::max(1LL, std::min(b, kreg_dev::kMaxSweepBlocks)));
+// chunk partials of one request: at most kMaxChunks x M x (7 | 1) doubles
+static size_t sweep_partials(const EvalJob& job) {
+  return static_cast<size_t>(kreg_dev::kMaxChunks) * job.M * (job.grad ? 7 : 1);
 }
 
 static void prepare_sweep(kreg_ctx* ctx, EvalJob& job, kreg_dev::SweepReq& R, const SweepScratch& s, int e) {
@@ -431,7 +502,8 @@ static void prepare_sweep(kreg_ctx* ctx, EvalJob& job, kreg_dev::SweepReq& R, co
   R.units = p->counts_valid ? sweep_units(p) : -1;
   R.tile_off = p->tile_off.ptr;
   R.unit_off = p->unit_off.ptr;
-  R.unit_tile = p->unit_tile.ptr;
+  R.zs = p->zs.ptr;
+  R.chunks = p->chunks.ptr;
   R.n_tiles = p->n_tiles;
   R.slots = p->slot_buf.ptr;
   R.capacity = static_cast<long long>(p->slot_buf.cap);
@@ -442,13 +514,19 @@ static void prepare_sweep(kreg_ctx* ctx, EvalJob& job, kreg_dev::SweepReq& R, co
   for (int m = 0; m < job.M; ++m) std::memcpy(R.T[m], job.T[m], sizeof(double) * 12);
   std::memcpy(R.Tb, p->T_build, sizeof(R.Tb));
   for (int k = 0; k < 3; ++k) R.anchor[k] = p->anchor[k];
-  R.qscale = p->qscale;
+  for (int m = 0; m < job.M; ++m) {
+    // {R_m - R_b, t_m - t_b} and {R_m, t_m - anchor} in FP32 (the sweep
+    // forms (T_m - T_b) z and T_m z - anchor per source)
+    for (int k = 0; k < 12; ++k) {
+      R.Td[m][k] = static_cast<float>(job.T[m][k] - p->T_build[k]);
+      R.Ta[m][k] = static_cast<float>(job.T[m][k] - ((k % 4) == 3 ? p->anchor[k / 4] : 0.0));
+    }
+  }
   const double l = job.lengthscale;
-  R.kappa = static_cast<float>(-1.4426950408889634 / (2.0 * l * l) / (p->qscale * p->qscale));
+  R.kappa = static_cast<float>(-1.4426950408889634 / (2.0 * l * l));
   R.sigma2 = p->sigma * p->sigma;
   R.inv_l2 = 1.0 / (l * l);
   R.partials = ctx->part_arena.ptr + s.part_off;
-  R.counter = ctx->counter_arena.ptr + e;
   R.disp_bits = ctx->disp_arena.ptr + static_cast<size_t>(e) * kreg_dev::kMaxCandidates;
 }
 
@@ -474,24 +552,22 @@ void run_round(kreg_ctx* ctx, std::vector<BuildJob>& builds, std::vector<EvalJob
   }
   const auto tb = clk::now();
   ctx->t_build_prep += std::chrono::duration<double>(tb - t0).count();
-  long long max_nvb_est = 1;
   // gradient requests first, F-only requests after (one launch per group)
   std::stable_partition(evals.begin(), evals.end(), [](const EvalJob& e) { return e.grad; });
   std::vector<SweepScratch> scratch(static_cast<size_t>(ne));
   size_t part_total = 0;
   for (int e = 0; e < ne; ++e) {
     scratch[e].part_off = part_total;
-    part_total += sweep_nvb_cap(evals[e]) * evals[e].M * 7;
+    part_total += sweep_partials(evals[e]);
   }
   if (ne) {
     ctx->part_arena.ensure(part_total + 1, false, 1.5);
-    ctx->counter_arena.ensure(ne + 1, /*zero=*/true);
+    ctx->counter_arena.ensure(2 * (ne / kreg_dev::kMaxSweepReqs + 1) + 2, /*zero=*/true);
     ctx->disp_arena.ensure(static_cast<size_t>(ne + 1) * kreg_dev::kMaxCandidates, /*zero=*/true);
   }
   for (int e = 0; e < ne; ++e) {
     prepare_sweep(ctx, evals[e], ctx->h_sweep.ptr[e], scratch[e], e);
     ctx->h_sweep.ptr[e].out = ctx->d_results.ptr + static_cast<size_t>(e) * kreg_dev::kMaxCandidates * kreg_dev::kOut;
-    max_nvb_est = std::max<long long>(max_nvb_est, static_cast<long long>(sweep_nvb_cap(evals[e])));
   }
   const auto ts = clk::now();
   ctx->t_sweep_prep += std::chrono::duration<double>(ts - tb).count();
@@ -503,9 +579,7 @@ void run_round(kreg_ctx* ctx, std::vector<BuildJob>& builds, std::vector<EvalJob
                               cudaMemcpyHostToDevice, ctx->stream));
   if (nb) kreg_dev::build_pairs_batched(ctx->h_build.ptr, ctx->d_build.ptr, nb, ctx->stream);
   if (ne) {
-    // one physical block per work block (blocks beyond a request's work exit at once)
-    const int bpr = static_cast<int>(max_nvb_est);
-    kreg_dev::sweep_batched(ctx->h_sweep.ptr, ctx->d_sweep.ptr, ne, bpr, ctx->stream,
+    kreg_dev::sweep_batched(ctx->h_sweep.ptr, ctx->d_sweep.ptr, ne, ctx->sm_count, ctx->counter_arena.ptr, ctx->stream,
                             ctx->profiling ? ctx->ev_sweep0 : nullptr, ctx->profiling ? ctx->ev_sweep1 : nullptr);
   }
   KREG_CUDA(cudaGetLastError());
@@ -606,12 +680,13 @@ double max_point_displacement_dev(kreg_ctx* ctx, const kreg_cloud* Z, const doub
 void pairs_export(kreg_ctx* ctx, const kreg_pairs* p, int64_t* offsets, int32_t* x_index, double* coeff) {
   // reference layout: CSR by ORIGINAL source index j, ascending ORIGINAL i
   const int nz = p->Z ? p->Z->n : 0;
-  std::vector<int> deg(static_cast<size_t>(nz) + 1, 0);
+  std::vector<int> deg(static_cast<size_t>(nz) + 1, 0), pos(static_cast<size_t>(nz) + 1, 0);
   std::vector<long long> toff(static_cast<size_t>(p->n_tiles) + 1, 0);
   std::vector<int4> sl(static_cast<size_t>(p->slots));
   std::vector<int> si(static_cast<size_t>(p->slots));
   if (nz) {
     KREG_CUDA(cudaMemcpyAsync(deg.data(), p->count.ptr, sizeof(int) * nz, cudaMemcpyDeviceToHost, ctx->stream));
+    KREG_CUDA(cudaMemcpyAsync(pos.data(), p->pos.ptr, sizeof(int) * nz, cudaMemcpyDeviceToHost, ctx->stream));
     KREG_CUDA(cudaMemcpyAsync(toff.data(), p->tile_off.ptr, sizeof(long long) * (p->n_tiles + 1),
                               cudaMemcpyDeviceToHost, ctx->stream));
     if (p->slots) {
@@ -629,7 +704,8 @@ void pairs_export(kreg_ctx* ctx, const kreg_pairs* p, int64_t* offsets, int32_t*
   for (int js = 0; js < nz; ++js) {
     const int j = p->Z->order[js];
     tmp.clear();
-    const long long col = toff[static_cast<size_t>(js >> 5)] + (js & 31);  // sliced-ELL column of js
+    const int ps = pos[static_cast<size_t>(js)];                         // degree-sorted position of js
+    const long long col = toff[static_cast<size_t>(ps >> 5)] + (ps & 31);  // its sliced-ELL column
     for (long long k = 0; k < deg[js]; ++k) {
       const size_t at = static_cast<size_t>(col + 32 * k);
       float lc;

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -41,9 +42,17 @@ struct DevBuf {
   DevBuf& operator=(const DevBuf&) = delete;
   ~DevBuf() { release(); }
   void release() {
-    if (ptr) cudaFree(ptr);
+    if (ptr && owned) cudaFree(ptr);
     ptr = nullptr;
     cap = 0;
+    owned = true;
+  }
+  bool owned = true;  // false: points into memory owned elsewhere (a context arena)
+  void borrow(T* p, size_t n) {
+    release();
+    ptr = p;
+    cap = n;
+    owned = false;
   }
   // grow (discarding contents) to hold at least n elements; optional zero fill
   void ensure(size_t n, bool zero = false, double slack = 1.25) {
@@ -73,7 +82,7 @@ struct PinnedBuf {
   void ensure(size_t n) {
     if (n <= cap && ptr) return;
     if (ptr) cudaFreeHost(ptr);
-    size_t want = n < 16 ? 16 : n * 2;
+    size_t want = n < 16 ? 16 : n + n / 4;
     KREG_CUDA(cudaMallocHost(&ptr, want * sizeof(T)));
     cap = want;
   }
@@ -120,8 +129,13 @@ struct kreg_ctx {
   kreg_host::DevBuf<unsigned long long> d_disp;
   // per-round sweep scratch arenas (one slice per request)
   kreg_host::DevBuf<double> part_arena;
-  kreg_host::DevBuf<unsigned int> counter_arena;        // self-resetting, zero between rounds
+  kreg_host::DevBuf<unsigned int> counter_arena;        // sweep chunk counters, self-resetting
   kreg_host::DevBuf<unsigned long long> disp_arena;    // self-resetting, zero between rounds
+  // end-to-end calls: pinned host staging and device arena of their clouds
+  kreg_host::PinnedBuf<double> stage_d;
+  kreg_host::PinnedBuf<float> stage_f;
+  kreg_host::DevBuf<double> arena_d;
+  kreg_host::DevBuf<float> arena_f;
   // pair-list workspaces kept across registrations (device buffers keep capacity)
   std::vector<kreg_pairs*> pool;
   int max_active = 0;  // lockstep window of kreg_register_batch (0 = all at once)
@@ -183,17 +197,19 @@ struct kreg_pairs {
   long long sup_entries = 0;
   long long expected_sup = 0;              // capacity hint
   // sweep list
-  kreg_host::DevBuf<int> count;            // degree per source (sorted order)
+  kreg_host::DevBuf<int> count;            // degree per source (Morton order)
+  kreg_host::DevBuf<int> perm, pos, deg_s; // degree-sorted sweep order of the sources
   kreg_host::DevBuf<long long> tile_off;
   kreg_host::DevBuf<int4> slot_buf;        // sliced-ELL slots {x fixed point, log2 c}
   kreg_host::DevBuf<int> slot_i;           // target index per slot (export only)
-  kreg_host::DevBuf<int> unit_off, unit_tile;
+  kreg_host::DevBuf<int> unit_off;
+  kreg_host::DevBuf<float4> zs;                 // sources in sweep order (FP32)
+  kreg_host::DevBuf<kreg_dev::ChunkRec> chunks; // sweep chunk records
   kreg_host::DevBuf<unsigned long long> disp_blk;
   int n_tiles = 0;
   long long slots = 0;                     // valid after the build round
   bool counts_valid = false;               // P / slots known on the host
   double anchor[3] = {0, 0, 0};
-  double qscale = 1.0;
   long long expected_pairs = 0;  // capacity hint
   // statistics
   long long full_builds = 0, filter_builds = 0;
@@ -211,6 +227,10 @@ std::string describe_schema(const kreg_cloud* c);
 void check_config(const kreg_registration_config& c);
 
 kreg_cloud* cloud_create(kreg_ctx* ctx, const kreg_cloud_view* v);
+// Many clouds: host staging on worker threads, device copies into a context
+// arena (valid until the next call of this function on the context).
+std::vector<std::unique_ptr<kreg_cloud>> cloud_create_many(kreg_ctx* ctx, const kreg_cloud_view* const* views,
+                                                           int n);
 double diameter_host(const double* xyz, int n);
 
 // One build request; `pairs` is (re)initialised for X, Z at transform T.

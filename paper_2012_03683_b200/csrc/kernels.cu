@@ -75,6 +75,17 @@ __device__ V block_excl_scan(V v, V* total) {
 // ------------------------------------------------------------------ K1
 constexpr int kUnitSlots = 32 * kUnitSteps;  // slots per sweep work unit
 
+// Sweep chunks of a request with U units: chunk_count(U) chunks of
+// chunk_units(U) units (a function of the pair list only).
+__host__ __device__ __forceinline__ long long chunk_units(long long U) {
+  long long cu = (U + kMaxChunks - 1) / kMaxChunks;
+  cu = (cu + kStageUnits - 1) / kStageUnits * kStageUnits;
+  return cu < kMinChunkUnits ? kMinChunkUnits : cu;
+}
+__host__ __device__ __forceinline__ int chunk_count(long long U) {
+  return U <= 0 ? 1 : (int)((U + chunk_units(U) - 1) / chunk_units(U));
+}
+
 // Candidate stage, grid over X (requests with full == 0 exit at once).
 // Cell id + occupancy count.
 __global__ void k_cell_assign(const BuildReq* reqs) {
@@ -226,9 +237,11 @@ constexpr int kMaxFeat = 64;  // max padded feature row handled in registers/sme
 // Ts z_j is 9 contiguous x-rows of the dense grid; lanes stride over the
 // candidates (coalesced FP64 loads), FP64 distance test against R_s
 // (kernels.hpp:37-42, inner_product.cpp:69), c_ij, c > c_min (:73).
-// EMIT=false writes sup_count[j]; EMIT=true writes j's candidates in stencil
-// order, contiguously: tile t = j/32 owns 32 rows of H_t entries (H_t = max
-// candidates in the tile), entry(j, k) = sup_off[t] + (j%32) H_t + k.
+// EMIT=false writes the geometric count (distance test only, an upper bound
+// that sizes the rows) to sup_count[j]; EMIT=true writes j's candidates (c >
+// c_min) in stencil order, contiguously: tile t = j/32 owns 32 rows of H_t
+// entries (H_t = max bound in the tile), entry(j, k) = sup_off[t] + (j%32) H_t
+// + k, and replaces sup_count[j] by the number written.
 template <bool EMIT>
 __global__ void __launch_bounds__(256) k_pair_pass(const BuildReq* reqs) {
   const BuildReq& R = reqs[blockIdx.y];
@@ -239,8 +252,10 @@ __global__ void __launch_bounds__(256) k_pair_pass(const BuildReq* reqs) {
   __shared__ __align__(16) float zf_s[8][kMaxFeat];
   float* zf = zf_s[threadIdx.x >> 5];
   const int fs = R.cp.fstride;
-  for (int d = lane; d < fs; d += 32) zf[d] = R.zfeat[(long long)j * fs + d];
-  __syncwarp();
+  if (EMIT) {
+    for (int d = lane; d < fs; d += 32) zf[d] = R.zfeat[(long long)j * fs + d];
+    __syncwarp();
+  }
 
   double qx, qy, qz;
   apply_T(R.Ts, R.zx[j], R.zy[j], R.zz[j], qx, qy, qz);
@@ -254,7 +269,7 @@ __global__ void __launch_bounds__(256) k_pair_pass(const BuildReq* reqs) {
     out = t0 + (j & 31) * H;
   }
   int cnt = 0;
-  const bool geo = R.cp.n_channels == 0;
+  const bool geo = !EMIT || R.cp.n_channels == 0;
   if (cxl + 1 >= 0 && cxl - 1 < R.gx) {
     const int x_lo = (int)(cxl - 1 < 0 ? 0 : cxl - 1);
     const int x_hi = (int)(cxl + 1 >= R.gx ? R.gx - 1 : cxl + 1);
@@ -289,17 +304,17 @@ __global__ void __launch_bounds__(256) k_pair_pass(const BuildReq* reqs) {
       }
     }
   }
-  if (!EMIT && lane == 0) R.sup_count[j] = cnt;
+  if (lane == 0) R.sup_count[j] = cnt;
 }
 
 // Tile offsets, one block per request (grid.x = requests):
 //  SUP:  candidate list, column height = max candidates in the tile
 //        -> sup_off = 32 x prefix; status[3, 4] = {overflow, entries}.
-//  !SUP: sweep list, column height = max degree rounded up to whole sweep
-//        units of kUnitSteps steps (>= 1 unit so the sweep also visits
-//        isolated sources for their displacement) -> unit_off, tile_off =
-//        kUnitSlots x unit_off, unit_tile[], status {P, overflow, slots,
-//        |T - Ts| displacement, invalid}; resets disp_bits.
+//  !SUP: sweep list over the degree-sorted source order, column height =
+//        the tile's first (largest) degree rounded up to whole sweep units
+//        of kUnitSteps steps (0 for tiles without pairs) -> unit_off,
+//        tile_off = kUnitSlots x unit_off, status {P, overflow,
+//        slots, |T - Ts| displacement, invalid}.
 template <bool SUP>
 __global__ void __launch_bounds__(1024) k_tile_offsets(const BuildReq* reqs) {
   const BuildReq& R = reqs[blockIdx.x];
@@ -311,14 +326,27 @@ __global__ void __launch_bounds__(1024) k_tile_offsets(const BuildReq* reqs) {
     const int t = b + threadIdx.x;
     long long v = 0;
     if (t < nt) {
-      const int j0 = 32 * t, j1 = min(R.n_z, j0 + 32);
+      const int j0 = 32 * t;
       int d = 0;
-      for (int j = j0; j < j1; ++j) {
-        const int c = cnt[j];
-        d = max(d, c);
-        pairs += c;
+      if (j0 + 32 <= R.n_z) {  // 8 independent 16-B loads (count arrays are 16-B aligned)
+        const int4* c4 = reinterpret_cast<const int4*>(cnt + j0);
+        int4 v4[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v4[q] = c4[q];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          d = max(d, max(max(v4[q].x, v4[q].y), max(v4[q].z, v4[q].w)));
+          pairs += (long long)v4[q].x + v4[q].y + v4[q].z + v4[q].w;
+        }
+      } else {
+        for (int j = j0; j < R.n_z; ++j) {
+          const int c = cnt[j];
+          d = max(d, c);
+          pairs += c;
+        }
       }
-      v = SUP ? d : (d > 0 ? (d + kUnitSteps - 1) / kUnitSteps : 1);
+      if (!SUP) d = R.deg_s[j0];  // windows are sorted by degree, descending
+      v = SUP ? d : (d + kUnitSteps - 1) / kUnitSteps;  // sources without pairs take no units
     }
     long long tot;
     const long long ex = carry + block_excl_scan<long long>(v, &tot);
@@ -358,10 +386,75 @@ __global__ void __launch_bounds__(1024) k_tile_offsets(const BuildReq* reqs) {
       R.status[6] = __longlong_as_double((long long)dmax_s) > R.filter_limit_sq ? 1.0 : 0.0;
     }
   }
-  if (!SUP && carry * kUnitSlots <= R.capacity) {
-    __syncthreads();
-    for (int t = threadIdx.x; t < nt; t += blockDim.x)
-      for (int u = R.unit_off[t]; u < R.unit_off[t + 1]; ++u) R.unit_tile[u] = t;
+}
+
+// Chunk records of the sweep list (warp per chunk): the tile holding the
+// chunk's first unit, where that tile ends, and its 32 sources' coordinates
+// (FP32, degree-sorted order), so a sweep warp starts a chunk from one TMA
+// copy instead of dependent loads.
+__global__ void k_chunk_records(const BuildReq* reqs) {
+  const BuildReq& R = reqs[blockIdx.y];
+  const int lane = threadIdx.x & 31;
+  const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (R.tile_off[R.n_tiles] > R.capacity) return;
+  const long long U = R.unit_off[R.n_tiles];
+  if (U == 0 || c >= chunk_count(U)) return;
+  const long long u0 = (long long)c * chunk_units(U);
+  int lo = 0, hi = R.n_tiles - 1;  // last tile t with unit_off[t] <= u0 (it has units)
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (R.unit_off[mid] <= u0) lo = mid;
+    else hi = mid - 1;
+  }
+  ChunkRec& rec = R.chunks[c];
+  if (lane == 0) {
+    rec.t0 = lo;
+    rec.t0_end = R.unit_off[lo + 1];
+  }
+  const int p = 32 * lo + lane;
+  const float4 z = p < R.n_z ? R.zs[p] : make_float4(0.f, 0.f, 0.f, 0.f);
+  rec.x[lane] = z.x;
+  rec.y[lane] = z.y;
+  rec.z[lane] = z.z;
+}
+
+// Sweep order of the sources: windows of kOrderWindow consecutive (Morton)
+// sources sorted by degree, descending (ties by index), one CTA per window
+// (bitonic sort of 64-bit keys in shared memory). Tiles of 32 sorted sources
+// then hold similar degrees, so the sliced-ELL padding is a few percent, and
+// sources without pairs end up in tiles that take no sweep units.
+// perm[p] = source at sorted position p, pos[j] = position of source j,
+// deg_s[p] = degree at position p.
+constexpr int kOrderWindow = 1024;
+__global__ void __launch_bounds__(kOrderWindow) k_order(const BuildReq* reqs) {
+  const BuildReq& R = reqs[blockIdx.y];
+  const int base = blockIdx.x * kOrderWindow;
+  if (base >= R.n_z) return;
+  __shared__ unsigned long long key[kOrderWindow];
+  const int j = base + threadIdx.x;
+  key[threadIdx.x] =
+      j < R.n_z ? ((unsigned long long)(0x7FFFFFFFu - (unsigned)R.count[j]) << 32) | (unsigned)j : ~0ull;
+  __syncthreads();
+  for (int k = 2; k <= kOrderWindow; k <<= 1) {
+    for (int s = k >> 1; s > 0; s >>= 1) {
+      const int i = threadIdx.x, p = i ^ s;
+      if (p > i) {
+        const unsigned long long a = key[i], b = key[p];
+        if ((a > b) == ((i & k) == 0)) {
+          key[i] = b;
+          key[p] = a;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  const unsigned long long kk = key[threadIdx.x];
+  if (kk != ~0ull) {
+    const int js = (int)(kk & 0xffffffffu), p = base + threadIdx.x;
+    R.perm[p] = js;
+    R.pos[js] = p;
+    R.deg_s[p] = (int)(0x7FFFFFFFu - (unsigned)(kk >> 32));
+    R.zs[p] = make_float4((float)R.zx[js], (float)R.zy[js], (float)R.zz[js], 0.0f);
   }
 }
 
@@ -411,7 +504,11 @@ __global__ void __launch_bounds__(256) k_filter(const BuildReq* reqs) {
     const long long t0 = R.sup_off[t], H = (R.sup_off[t + 1] - t0) >> 5;
     row = R.sup + t0 + (j & 31) * H;
   }
-  const long long out = EMIT ? R.tile_off[t] + (j & 31) : 0;
+  long long out = 0;
+  if (EMIT) {  // column of j in the degree-sorted order
+    const int p = R.pos[j];
+    out = R.tile_off[p >> 5] + (p & 31);
+  }
   const double c2 = R.cutoff_sq;
   int cnt = 0;
   for (int sb = 0; sb < ds; sb += 32) {
@@ -430,9 +527,10 @@ __global__ void __launch_bounds__(256) k_filter(const BuildReq* reqs) {
     const unsigned m = __ballot_sync(0xffffffffu, keep);
     if (EMIT && keep) {
       const long long at = out + 32LL * (cnt + __popc(m & ((1u << lane) - 1u)));
-      R.slots[at] = make_int4(__double2int_rn((x - R.anchor[0]) * R.qscale),
-                              __double2int_rn((y - R.anchor[1]) * R.qscale),
-                              __double2int_rn((z - R.anchor[2]) * R.qscale), e.y);
+      // x_i - T_b z_j in FP32 (|.| <= cutoff): the sweep forms d = x_i - T z_j
+      // as this minus the source's displacement (T - T_b) z_j
+      R.slots[at] = make_int4(__float_as_int((float)(x - qx)), __float_as_int((float)(y - qy)),
+                              __float_as_int((float)(z - qz)), e.y);
       R.slot_i[at] = e.x;
     }
     cnt += __popc(m);
@@ -441,7 +539,8 @@ __global__ void __launch_bounds__(256) k_filter(const BuildReq* reqs) {
     if (lane == 0) R.count[j] = cnt;
   } else {
     // pad the column to the tile's unit-rounded height: w = ex2(-inf) = 0
-    const int height = (R.unit_off[t + 1] - R.unit_off[t]) * kUnitSteps;
+    const int ts = R.pos[j] >> 5;
+    const int height = (R.unit_off[ts + 1] - R.unit_off[ts]) * kUnitSteps;
     for (int k = cnt + lane; k < height; k += 32) {
       R.slots[out + 32LL * k] = make_int4(0, 0, 0, __float_as_int(-INFINITY));
       R.slot_i[out + 32LL * k] = -1;
@@ -483,32 +582,36 @@ __device__ __forceinline__ double warp_sum_d(double v) {
   return v;
 }
 
-// Fused F + gradient + displacement sweep over the sliced-ELL pair list.
-//  * Work unit = one tile of 32 consecutive sources x kUnitSteps degree steps;
-//    lane l owns source j = 32 t + l: per-j moments stay in registers, pair
-//    slots (tile_off + 32 k + l) load coalesced, and the x gathers of
-//    neighbouring sources (Morton order) hit the same lines.
-//  * At every tile change a lane computes q = T_m z_j in FP64 for all M
-//    candidates -> fixed point (kept as magic - q), and the displacement
-//    |T_m z_j - T_b z_j| (inner_product.cpp:238-246); every tile has >= 1 unit.
-//  * Per slot and candidate: d = x - q exactly (IADD + FADD with the 1.5*2^23
-//    magic), r^2, w = ex2(r^2 kappa + log2 c) on MUFU, W += w, S += w d;
-//    candidates run in pairs on FFMA2/FADD2/FMUL2. Per tile: torque +=
-//    q_j x S_j (gw = sum_j q_j x S_j since q x x = q x (x - q)).
-//  * Units are cut into nblk = ceil(U / kUnitsPerBlock) work blocks, a function
-//    of the pair list only; warp w of a work block takes a contiguous unit
-//    range. Work-block totals are reduced in FP64 in a fixed order and the
-//    last block of the request reduces the work-block partials in a fixed
-//    order: bitwise reproducible, independent of grid and batch composition.
-__device__ __forceinline__ long long sweep_work_blocks(long long units) {
-  const long long b = (units + kUnitsPerBlock - 1) / kUnitsPerBlock;
-  return b < 1 ? 1 : (b > kMaxSweepBlocks ? kMaxSweepBlocks : b);
+// Fused F + gradient sweep over the sliced-ELL pair list.
+//  * Work unit = one tile of 32 degree-sorted sources x kUnitSteps degree
+//    steps = kUnitSlots contiguous 16-B slots {x_i - T_b z_j (FP32 x3),
+//    log2 c_ij}; lane l owns the source at sorted position 32 t + l, so the
+//    per-source moments stay in registers.
+//  * A request's units are cut into chunk_count(U) chunks. The chunks of all
+//    requests of a launch form one queue; every warp of a persistent grid
+//    grabs chunks dynamically and streams their units through a private TMA
+//    ring (kSweepStages stages of kStageUnits units), prefetching across
+//    chunk boundaries. A chunk's first stage also carries its ChunkRec (first
+//    tile + its sources), later tiles' sources are prefetched one tile ahead:
+//    the stream has no dependent global loads.
+//  * Per tile and candidate m (FP32): delta = (R_m - R_b) z_j + (t_m - t_b)
+//    and the torque arm a_j = T_m z_j - anchor. Per slot: d = (x_i - T_b z_j)
+//    - delta = x_i - T_m z_j, r^2, w = ex2(r^2 kappa + log2 c) on MUFU, W += w,
+//    S += w d; candidates in pairs on FFMA2/FADD2/FMUL2. Per tile: torque +=
+//    a_j x S_j (sum_j q_j x S_j = sum_j (q_j - a) x S_j + a x sum S).
+//  * Each chunk's sums are one partial (FP32 warp sums widened to FP64);
+//    k_sweep_reduce adds a request's partials in a fixed order: bitwise
+//    reproducible, independent of scheduling and batch composition.
+//  * max_j |T_m z_j - T_b z_j| (inner_product.cpp:238-246) comes from
+//    k_displacement_batched in FP64 over the original coordinates.
+__device__ __forceinline__ long long request_units(const SweepReq& R) {
+  // an overflowed build is skipped (its result is discarded by the host); the
+  // unit count is passed by the host when the pair list was built earlier
+  if (R.units >= 0) return R.units;
+  return R.tile_off[R.n_tiles] <= R.capacity ? (long long)R.unit_off[R.n_tiles] : 0;
 }
 
-// TMA (bulk async copy) + mbarrier helpers: each warp streams its sweep units
-// (32 * kUnitSteps contiguous 8-B slots = 2 KB each) through a private ring of
-// kSweepStages shared-memory stages, so DRAM/L2 latency of the pair stream is
-// hidden behind the x gathers and math of earlier units.
+// TMA (bulk async copy) + mbarrier helpers.
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
@@ -536,30 +639,35 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phas
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-constexpr unsigned kStageBytes = kUnitSlots * sizeof(int4);
-constexpr size_t kSweepSmem = (size_t)(kSweepThreads / 32) * kSweepStages * kStageBytes +
-                              (size_t)(kSweepThreads / 32) * kSweepStages * sizeof(unsigned long long);
+constexpr unsigned kUnitBytes = kUnitSlots * sizeof(int4);
+constexpr int kStageSlots = kStageUnits * kUnitSlots;
+constexpr int kSweepWarps = kSweepThreads / 32;
+// chunk records in flight per warp: the producer runs <= kSweepStages stages
+// ahead and a record is read when its chunk starts (before its first stage is
+// released), so at most kSweepStages first stages hold records
+constexpr int kRecSlots = kSweepStages;
+constexpr size_t kSweepSmem = (size_t)kSweepWarps * kSweepStages * kStageSlots * sizeof(int4) +
+                              (size_t)kSweepWarps * kRecSlots * sizeof(ChunkRec) +
+                              (size_t)kSweepWarps * kSweepStages * sizeof(unsigned long long);
 
-// One unit of one sliced-ELL column (lane = source j) for M candidates. The
-// unit's 16-B slots {x fixed point, log2 c} are in shared memory (TMA);
-// per candidate pair d = x - q (exact, fixed point), w = ex2(r^2 kappa +
-// log2 c), W += w and (GRAD) S += w d on FFMA2/FADD2/FMUL2 + 2 MUFU.EX2.
+// `steps` degree steps of one sliced-ELL column (lane = source) for M
+// candidates: d = (x - T_b z) - delta, w = ex2(r^2 kappa + log2 c), W += w
+// and (GRAD) S += w d on FFMA2/FADD2/FMUL2 + 2 MUFU.EX2 per candidate pair.
 template <int NP, bool GRAD>
-__device__ __forceinline__ void sweep_unit(const int4* __restrict__ stage, int lane, const int (&qx)[2 * NP],
-                                           const int (&qy)[2 * NP], const int (&qz)[2 * NP], f2_t kap2,
-                                           f2_t (&W)[NP], f2_t (&Sx)[NP], f2_t (&Sy)[NP], f2_t (&Sz)[NP]) {
-  const f2_t nmag = pk2(-12582912.0f, -12582912.0f);
-#pragma unroll
-  for (int k = 0; k < kUnitSteps; ++k) {
-    const int4 sl = stage[32 * k + lane];  // conflict-free LDS.128
+__device__ __forceinline__ void sweep_steps(const int4* __restrict__ col, int steps, const f2_t (&ndx)[NP],
+                                            const f2_t (&ndy)[NP], const f2_t (&ndz)[NP], f2_t kap2, f2_t (&W)[NP],
+                                            f2_t (&Sx)[NP], f2_t (&Sy)[NP], f2_t (&Sz)[NP]) {
+#pragma unroll 2
+  for (int k = 0; k < steps; ++k) {
+    const int4 sl = col[32 * k];  // conflict-free LDS.128
+    const float x = __int_as_float(sl.x), y = __int_as_float(sl.y), z = __int_as_float(sl.z);
     const float lc = __int_as_float(sl.w);
-    const f2_t lc2 = pk2(lc, lc);
+    const f2_t x2 = pk2(x, x), y2 = pk2(y, y), z2 = pk2(z, z), lc2 = pk2(lc, lc);
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
-      const int a = 2 * p, b = 2 * p + 1;
-      const f2_t dx = add2(pk2(__int_as_float(sl.x + qx[a]), __int_as_float(sl.x + qx[b])), nmag);
-      const f2_t dy = add2(pk2(__int_as_float(sl.y + qy[a]), __int_as_float(sl.y + qy[b])), nmag);
-      const f2_t dz = add2(pk2(__int_as_float(sl.z + qz[a]), __int_as_float(sl.z + qz[b])), nmag);
+      const f2_t dx = add2(x2, ndx[p]);
+      const f2_t dy = add2(y2, ndy[p]);
+      const f2_t dz = add2(z2, ndz[p]);
       const f2_t r2 = fma2(dz, dz, fma2(dy, dy, mul2(dx, dx)));
       float e0, e1;
       upk2(fma2(r2, kap2, lc2), e0, e1);
@@ -574,83 +682,179 @@ __device__ __forceinline__ void sweep_unit(const int4* __restrict__ stage, int l
   }
 }
 
+__device__ __forceinline__ f2_t warp_sum_f2(f2_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = add2(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Per-warp chunk queue and TMA producer state (driven by lane 0).
+struct WarpQueue {
+  int ids[kQueueDepth];
+  int head, tail;
+  int done;
+  int pr, pc;        // request / chunk being prefetched
+  long long pu, pend;
+  unsigned issued;   // stages issued so far
+  unsigned recs;     // chunk records issued so far
+  int first;         // next stage is the first of chunk pc
+};
+
 template <int NP, bool GRAD>
-__global__ void __launch_bounds__(kSweepThreads, kSweepMinBlocks) k_sweep(const SweepReq* reqs) {
+__global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(const SweepReq* reqs, int n_req, unsigned* next_chunk) {
   constexpr int MAXM = 2 * NP;
-  constexpr int NV = GRAD ? 7 : 1;  // reduced values per candidate
-  constexpr int NW = kSweepThreads / 32;
-  // the request descriptor (~1 KB) is staged in shared memory once per block
-  __shared__ __align__(16) SweepReq Rs;
-  {
-    const int4* g = reinterpret_cast<const int4*>(reqs + blockIdx.y);
-    int4* s = reinterpret_cast<int4*>(&Rs);
-    for (int k = threadIdx.x; k < (int)(sizeof(SweepReq) / 16); k += blockDim.x) s[k] = g[k];
-  }
-  __syncthreads();
-  const SweepReq& R = Rs;
-  const int M = R.M;
-  // an overflowed build is skipped (its result is discarded by the host);
-  // the unit count is passed by the host when the pair list was built earlier
-  long long U = R.units;
-  if (U < 0) U = R.tile_off[R.n_tiles] <= R.capacity ? (long long)R.unit_off[R.n_tiles] : 0;
-  const long long nblk = sweep_work_blocks(U);
-  const long long upb = (U + nblk - 1) / nblk;
-  const f2_t kap2 = pk2(R.kappa, R.kappa);
-  __shared__ double red[NW][MAXM * 7];
-  __shared__ unsigned long long dred[NW][MAXM];
-  extern __shared__ __align__(128) unsigned char dyn_smem[];
-  int4* ring_all = reinterpret_cast<int4*>(dyn_smem);
-  unsigned long long* bar_all =
-      reinterpret_cast<unsigned long long*>(dyn_smem + (size_t)NW * kSweepStages * kStageBytes);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  if (threadIdx.x < NW * kSweepStages) mbar_init(&bar_all[threadIdx.x], 1);
+  __shared__ int cbase[kMaxSweepReqs + 1];
+  __shared__ int units_s[kMaxSweepReqs];
+  __shared__ WarpQueue wq[kSweepWarps];
+  extern __shared__ __align__(128) unsigned char dyn_smem[];
+  int4* ring = reinterpret_cast<int4*>(dyn_smem) + (size_t)wid * kSweepStages * kStageSlots;
+  ChunkRec* recs = reinterpret_cast<ChunkRec*>(dyn_smem + (size_t)kSweepWarps * kSweepStages * kStageSlots * sizeof(int4)) +
+                   wid * kRecSlots;
+  unsigned long long* bars =
+      reinterpret_cast<unsigned long long*>(dyn_smem + (size_t)kSweepWarps * kSweepStages * kStageSlots * sizeof(int4) +
+                                            (size_t)kSweepWarps * kRecSlots * sizeof(ChunkRec)) +
+      wid * kSweepStages;
+
+  // chunk prefix over the launch's requests (every CTA computes it)
+  {
+    int C = 0;
+    if (threadIdx.x < n_req) {
+      const long long U = request_units(reqs[threadIdx.x]);
+      C = chunk_count(U);
+      units_s[threadIdx.x] = (int)U;
+    }
+    int tot;
+    const int ex = block_excl_scan<int>(C, &tot);
+    if (threadIdx.x < n_req) cbase[threadIdx.x] = ex;
+    if (threadIdx.x == 0) cbase[n_req] = tot;
+  }
+  if (lane < kSweepStages) mbar_init(&bars[lane], 1);
+  if (lane == 0) {
+    WarpQueue& q = wq[wid];
+    q.head = q.tail = 0;
+    q.done = 0;
+    q.pr = q.pc = 0;
+    q.pu = q.pend = 0;
+    q.issued = q.recs = 0;
+    q.first = 0;
+  }
   mbar_fence_init();
   __syncthreads();
+  const int total = cbase[n_req];
+  WarpQueue& Q = wq[wid];
 
-  if (blockIdx.x < nblk) {
-    f2_t acc[NP][7];
-    unsigned long long dmax[MAXM];
+  // locate chunk g: request r with cbase[r] <= g < cbase[r + 1]
+  auto locate = [&](int g) {
+    int lo = 0, hi = n_req - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (cbase[mid] <= g) lo = mid;
+      else hi = mid - 1;
+    }
+    return lo;
+  };
+  // lane 0: issue the next stage (grabbing chunks as needed); false if none
+  auto produce = [&]() -> bool {
+    while (Q.pu >= Q.pend) {
+      if (Q.done || Q.tail - Q.head >= kQueueDepth) return false;
+      const int g = (int)atomicAdd(next_chunk, 1u);
+      if (g >= total) {
+        Q.done = 1;
+        return false;
+      }
+      const int r = locate(g);
+      const long long U = units_s[r], cu = chunk_units(U);
+      Q.ids[Q.tail % kQueueDepth] = g;
+      ++Q.tail;
+      Q.pr = r;
+      Q.pc = g - cbase[r];
+      Q.pu = (long long)Q.pc * cu;
+      Q.pend = min(U, Q.pu + cu);
+      Q.first = 1;
+    }
+    const int nu = (int)min((long long)kStageUnits, Q.pend - Q.pu);
+    const int s = Q.issued % kSweepStages;
+    const SweepReq& P = reqs[Q.pr];
+    fence_proxy_async();
+    mbar_expect_tx(&bars[s], nu * kUnitBytes + (Q.first ? (unsigned)sizeof(ChunkRec) : 0u));
+    tma_load_1d(ring + s * kStageSlots, P.slots + Q.pu * kUnitSlots, nu * kUnitBytes, &bars[s]);
+    if (Q.first) {
+      tma_load_1d(recs + Q.recs % kRecSlots, P.chunks + Q.pc, sizeof(ChunkRec), &bars[s]);
+      ++Q.recs;
+      Q.first = 0;
+    }
+    Q.pu += nu;
+    ++Q.issued;
+    return true;
+  };
+  if (lane == 0)
+    for (int s = 0; s < kSweepStages; ++s)
+      if (!produce()) break;
+  __syncwarp();
+
+  unsigned consumed = 0, rec_used = 0;
+  f2_t acc[NP][7];
+  f2_t ndx[NP], ndy[NP], ndz[NP];  // -delta per candidate pair
+  float ax[MAXM], ay[MAXM], az[MAXM];  // torque arm T_m z_j - anchor
+  f2_t W[NP], Sx[NP], Sy[NP], Sz[NP];
+  for (;;) {
+    // next chunk of this warp (produced in order by lane 0)
+    int g = -1;
+    if (lane == 0) {
+      if (Q.head == Q.tail) produce();  // grabs the next chunk (zero-unit chunks issue no stage)
+      if (Q.head != Q.tail) g = Q.ids[Q.head % kQueueDepth];
+    }
+    g = __shfl_sync(0xffffffffu, g, 0);
+    if (g < 0) break;
+    const int r = locate(g);
+    const SweepReq& R = reqs[r];
+    const int M = R.M;
+    const long long U = units_s[r], cu = chunk_units(U);
+    const int c = g - cbase[r];
+    const long long u0 = (long long)c * cu, u1 = min(U, u0 + cu);
+    const f2_t kap2 = pk2(R.kappa, R.kappa);
 #pragma unroll
     for (int p = 0; p < NP; ++p)
 #pragma unroll
-      for (int c = 0; c < 7; ++c) acc[p][c] = 0ull;
-#pragma unroll
-    for (int m = 0; m < MAXM; ++m) dmax[m] = 0ull;
-
-    const long long u0 = blockIdx.x * upb;
-    const long long u1 = min(U, u0 + upb);
-    const long long upw = (upb + NW - 1) / NW;
-    const long long wu0 = min(u1, u0 + wid * upw);
-    const int nunits = (int)(min(u1, wu0 + upw) - wu0);
-    int4* ring = ring_all + (size_t)wid * kSweepStages * kUnitSlots;
-    unsigned long long* bars = bar_all + wid * kSweepStages;
-    const int4* src = R.slots + wu0 * kUnitSlots;
-    if (lane == 0) {
-      for (int s = 0; s < kSweepStages && s < nunits; ++s) {
-        mbar_expect_tx(&bars[s], kStageBytes);
-        tma_load_1d(ring + s * kUnitSlots, src + (long long)s * kUnitSlots, kStageBytes, &bars[s]);
-      }
-    }
-
-    int t = -1;
-    bool active = false;
-    int qx[MAXM], qy[MAXM], qz[MAXM];
-    f2_t W[NP], Sx[NP], Sy[NP], Sz[NP];
-#pragma unroll
-    for (int m = 0; m < MAXM; ++m) qx[m] = qy[m] = qz[m] = (int)kMagic;
+      for (int v = 0; v < 7; ++v) acc[p][v] = 0ull;
 #pragma unroll
     for (int p = 0; p < NP; ++p) W[p] = Sx[p] = Sy[p] = Sz[p] = 0ull;
 
+    // per-tile setup from the source's FP32 coordinates
+    auto start_tile = [&](float zx, float zy, float zz) {
+#pragma unroll
+      for (int m = 0; m < MAXM; m += 2) {
+        const float* A = R.Td[m < M ? m : 0];
+        const float* B = R.Td[m + 1 < M ? m + 1 : 0];
+        ndx[m / 2] = pk2(-fmaf(A[0], zx, fmaf(A[1], zy, fmaf(A[2], zz, A[3]))),
+                         -fmaf(B[0], zx, fmaf(B[1], zy, fmaf(B[2], zz, B[3]))));
+        ndy[m / 2] = pk2(-fmaf(A[4], zx, fmaf(A[5], zy, fmaf(A[6], zz, A[7]))),
+                         -fmaf(B[4], zx, fmaf(B[5], zy, fmaf(B[6], zz, B[7]))));
+        ndz[m / 2] = pk2(-fmaf(A[8], zx, fmaf(A[9], zy, fmaf(A[10], zz, A[11]))),
+                         -fmaf(B[8], zx, fmaf(B[9], zy, fmaf(B[10], zz, B[11]))));
+      }
+      if (GRAD) {
+#pragma unroll
+        for (int m = 0; m < MAXM; ++m) {
+          const float* A = R.Ta[m < M ? m : 0];
+          ax[m] = fmaf(A[0], zx, fmaf(A[1], zy, fmaf(A[2], zz, A[3])));
+          ay[m] = fmaf(A[4], zx, fmaf(A[5], zy, fmaf(A[6], zz, A[7])));
+          az[m] = fmaf(A[8], zx, fmaf(A[9], zy, fmaf(A[10], zz, A[11])));
+        }
+      }
+    };
+    bool active = false;
     auto flush_tile = [&]() {
       if (active) {
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
-          const f2_t fqx = pk2((float)(int)(kMagic - (unsigned)qx[2 * p]), (float)(int)(kMagic - (unsigned)qx[2 * p + 1]));
-          const f2_t fqy = pk2((float)(int)(kMagic - (unsigned)qy[2 * p]), (float)(int)(kMagic - (unsigned)qy[2 * p + 1]));
-          const f2_t fqz = pk2((float)(int)(kMagic - (unsigned)qz[2 * p]), (float)(int)(kMagic - (unsigned)qz[2 * p + 1]));
-          const f2_t neg = pk2(-1.0f, -1.0f);
           acc[p][0] = add2(acc[p][0], W[p]);
           if (GRAD) {
+            const f2_t fqx = pk2(ax[2 * p], ax[2 * p + 1]);
+            const f2_t fqy = pk2(ay[2 * p], ay[2 * p + 1]);
+            const f2_t fqz = pk2(az[2 * p], az[2 * p + 1]);
+            const f2_t neg = pk2(-1.0f, -1.0f);
             acc[p][1] = add2(acc[p][1], Sx[p]);
             acc[p][2] = add2(acc[p][2], Sy[p]);
             acc[p][3] = add2(acc[p][3], Sz[p]);
@@ -664,121 +868,162 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMinBlocks) k_sweep(const 
       for (int p = 0; p < NP; ++p) W[p] = Sx[p] = Sy[p] = Sz[p] = 0ull;
     };
 
-    int tiles32 = 0;  // unit -> tile for 32 units at a time, one load per lane
-    for (int i = 0; i < nunits; ++i) {
-      if ((i & 31) == 0) tiles32 = (i + lane < nunits) ? R.unit_tile[wu0 + i + lane] : 0;
-      const int tu = __shfl_sync(0xffffffffu, tiles32, i & 31);
-      if (tu != t) {
-        flush_tile();
-        t = tu;
-        const int j = t * 32 + lane;
-        active = j < R.n_z;
-        if (active) {
-          const double zx = R.zx[j], zy = R.zy[j], zz = R.zz[j];
-          double bx, by, bz;
-          apply_T(R.Tb, zx, zy, zz, bx, by, bz);
-          const double lim = 536870912.0;  // 2^29 units; X lies within 2^28 of the anchor
-#pragma unroll
-          for (int m = 0; m < MAXM; ++m) {
-            const int mm = m < M ? m : 0;  // padding candidates repeat candidate 0
-            double x, y, z;
-            apply_T(R.T[mm], zx, zy, zz, x, y, z);
-            const double dx = x - bx, dy = y - by, dz = z - bz;
-            const unsigned long long d2 = (unsigned long long)__double_as_longlong(dx * dx + dy * dy + dz * dz);
-            dmax[m] = d2 > dmax[m] ? d2 : dmax[m];
-            qx[m] = (int)(kMagic - (unsigned)__double2int_rn(fmin(fmax((x - R.anchor[0]) * R.qscale, -lim), lim)));
-            qy[m] = (int)(kMagic - (unsigned)__double2int_rn(fmin(fmax((y - R.anchor[1]) * R.qscale, -lim), lim)));
-            qz[m] = (int)(kMagic - (unsigned)__double2int_rn(fmin(fmax((z - R.anchor[2]) * R.qscale, -lim), lim)));
+    if (u1 > u0) {
+      // first stage carries the chunk record
+      const int s0 = consumed % kSweepStages;
+      mbar_wait(&bars[s0], (consumed / kSweepStages) & 1);
+      const ChunkRec& rec = recs[rec_used % kRecSlots];
+      ++rec_used;
+      int t = rec.t0;
+      long long t_end = rec.t0_end;
+      active = 32 * t + lane < R.n_z;
+      start_tile(rec.x[lane], rec.y[lane], rec.z[lane]);
+      // prefetch of the next tile (speculatively t + 1)
+      auto prefetch = [&](int tn, float4& pz, long long& pend) {
+        pz = make_float4(0.f, 0.f, 0.f, 0.f);
+        pend = U;
+        if (tn < R.n_tiles) {
+          if (32 * tn + lane < R.n_z) pz = R.zs[32 * tn + lane];
+          pend = R.unit_off[tn + 1];
+        }
+      };
+      float4 pz;
+      long long p_end;
+      prefetch(t + 1, pz, p_end);
+
+      for (long long u = u0; u < u1; u += kStageUnits) {
+        const int nu = (int)min((long long)kStageUnits, u1 - u);
+        const int s = consumed % kSweepStages;
+        if (u != u0) mbar_wait(&bars[s], (consumed / kSweepStages) & 1);
+        const int4* stage = ring + s * kStageSlots + lane;
+        if (u + nu <= t_end) {  // whole stage inside the current tile
+          if (active) sweep_steps<NP, GRAD>(stage, nu * kUnitSteps, ndx, ndy, ndz, kap2, W, Sx, Sy, Sz);
+        } else {
+          long long v = u;
+          while (v < u + nu) {
+            while (v >= t_end) {  // next tile with units
+              flush_tile();
+              ++t;
+              if (p_end > v) {
+                t_end = p_end;
+                active = 32 * t + lane < R.n_z;
+                start_tile(pz.x, pz.y, pz.z);
+              } else {  // tile t had no units (window end): load directly
+                long long e = R.unit_off[t + 1];
+                while (e <= v) e = R.unit_off[++t + 1];
+                t_end = e;
+                const float4 z = 32 * t + lane < R.n_z ? R.zs[32 * t + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+                active = 32 * t + lane < R.n_z;
+                start_tile(z.x, z.y, z.z);
+              }
+              prefetch(t + 1, pz, p_end);
+            }
+            const long long w_end = min(u + nu, t_end);
+            if (active)
+              sweep_steps<NP, GRAD>(stage + (v - u) * kUnitSlots, (int)(w_end - v) * kUnitSteps, ndx, ndy, ndz, kap2,
+                                    W, Sx, Sy, Sz);
+            v = w_end;
           }
         }
+        __syncwarp();
+        ++consumed;
+        if (lane == 0) produce();  // refill the stage just consumed
+        __syncwarp();
       }
-      const int s = i % kSweepStages;
-      mbar_wait(&bars[s], (unsigned)((i / kSweepStages) & 1));
-      if (active) sweep_unit<NP, GRAD>(ring + s * kUnitSlots, lane, qx, qy, qz, kap2, W, Sx, Sy, Sz);
-      __syncwarp();
-      if (lane == 0 && i + kSweepStages < nunits) {  // refill this stage with unit i + stages
-        fence_proxy_async();
-        mbar_expect_tx(&bars[s], kStageBytes);
-        tma_load_1d(ring + s * kUnitSlots, src + (long long)(i + kSweepStages) * kUnitSlots, kStageBytes, &bars[s]);
-      }
+      flush_tile();
     }
-    flush_tile();
 
-    // deterministic block reduction in FP64; displacement max
+    // chunk partial: FP32 warp sums (fixed butterfly order) widened to FP64
+    double* part = R.partials + (size_t)c * (M * (GRAD ? 7 : 1));
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
 #pragma unroll
-      for (int c = 0; c < 7; ++c) {
-        float a0 = 0.0f, a1 = 0.0f;
-        if (c < NV) upk2(acc[p][c], a0, a1);
-        const double s0 = c < NV ? warp_sum_d((double)a0) : 0.0;
-        const double s1 = c < NV ? warp_sum_d((double)a1) : 0.0;
+      for (int v = 0; v < (GRAD ? 7 : 1); ++v) {
+        float a0, a1;
+        upk2(warp_sum_f2(acc[p][v]), a0, a1);
         if (lane == 0) {
-          red[wid][(2 * p) * 7 + c] = s0;
-          red[wid][(2 * p + 1) * 7 + c] = s1;
+          if (2 * p < M) part[(2 * p) * (GRAD ? 7 : 1) + v] = (double)a0;
+          if (2 * p + 1 < M) part[(2 * p + 1) * (GRAD ? 7 : 1) + v] = (double)a1;
         }
       }
     }
-#pragma unroll
-    for (int m = 0; m < MAXM; ++m) {
-      unsigned long long d = dmax[m];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const unsigned long long other = __shfl_down_sync(0xffffffffu, d, o);
-        d = other > d ? other : d;
-      }
-      if (lane == 0) dred[wid][m] = d;
-    }
-    __syncthreads();
-    if (threadIdx.x < M * 7) {
-      double s = 0.0;
-      for (int w = 0; w < kSweepThreads / 32; ++w) s += red[w][threadIdx.x];
-      R.partials[blockIdx.x * (M * 7) + threadIdx.x] = s;
-      __threadfence();
-    } else if (threadIdx.x >= 64 && threadIdx.x < 64 + M) {
-      const int m = threadIdx.x - 64;
-      unsigned long long d = 0;
-      for (int w = 0; w < kSweepThreads / 32; ++w) d = dred[w][m] > d ? dred[w][m] : d;
-      if (d) atomicMax(&R.disp_bits[m], d);
-      __threadfence();
-    }
+    __syncwarp();
+    if (lane == 0) ++Q.head;
+    __syncwarp();
   }
-  // last physical block of this request reduces the work-block partials
-  __shared__ bool is_last;
-  __syncthreads();
-  if (threadIdx.x == 0) is_last = atomicAdd(R.counter, 1u) == gridDim.x - 1;
-  __syncthreads();
-  if (!is_last) return;
-  // thread t sums a contiguous range of work blocks, then fixed-order tree
-  const long long per = (nblk + kSweepThreads - 1) / kSweepThreads;
-  const long long b0 = threadIdx.x * per, b1 = min(nblk, b0 + per);
+}
+
+// Displacement max_j |T_m z_j - T_b z_j| (inner_product.cpp:238-246) of every
+// sweep request in FP64 over the original coordinates; warp max, one atomic
+// per warp and candidate (max is order-free). grid = (n_z / 256, requests).
+__global__ void __launch_bounds__(256) k_displacement_batched(const SweepReq* reqs) {
+  const SweepReq& R = reqs[blockIdx.y];
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (blockIdx.x * blockDim.x >= R.n_z) return;
+  const int M = R.M;
+  double zx = 0, zy = 0, zz = 0, bx = 0, by = 0, bz = 0;
+  const bool ok = j < R.n_z;
+  if (ok) {
+    zx = R.zx[j];
+    zy = R.zy[j];
+    zz = R.zz[j];
+    apply_T(R.Tb, zx, zy, zz, bx, by, bz);
+  }
+  for (int m = 0; m < M; ++m) {
+    unsigned long long d2 = 0;
+    if (ok) {
+      double x, y, z;
+      apply_T(R.T[m], zx, zy, zz, x, y, z);
+      const double dx = x - bx, dy = y - by, dz = z - bz;
+      d2 = (unsigned long long)__double_as_longlong(dx * dx + dy * dy + dz * dz);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long other = __shfl_xor_sync(0xffffffffu, d2, o);
+      d2 = other > d2 ? other : d2;
+    }
+    if ((threadIdx.x & 31) == 0 && d2) atomicMax(&R.disp_bits[m], d2);
+  }
+}
+
+// Final sums of every request (one CTA each): partials of its chunks in a
+// fixed order (thread-contiguous ranges, then a fixed tree), the gradient
+// assembled in FP64 (inner_product.cpp:121-157), displacement from the max
+// bits; resets the displacement bits and the launches' chunk counters.
+__global__ void __launch_bounds__(kSweepThreads) k_sweep_reduce(const SweepReq* reqs, unsigned* next_chunk,
+                                                                 int n_ctl) {
+  const SweepReq& R = reqs[blockIdx.x];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int M = R.M, NV = R.grad ? 7 : 1;
+  const int C = chunk_count(request_units(R));
+  __shared__ double red[kSweepWarps][kMaxCandidates * 7];
+  const int per = (C + kSweepThreads - 1) / kSweepThreads;
+  const int c0 = threadIdx.x * per, c1 = min(C, c0 + per);
   for (int m = 0; m < M; ++m) {
     double v[7] = {0, 0, 0, 0, 0, 0, 0};
-    for (long long b = b0; b < b1; ++b)
+    for (int c = c0; c < c1; ++c)
+      for (int k = 0; k < NV; ++k) v[k] += __ldcg(R.partials + (size_t)c * (M * NV) + m * NV + k);
 #pragma unroll
-      for (int c = 0; c < 7; ++c) v[c] += __ldcg(R.partials + b * (M * 7) + m * 7 + c);
-#pragma unroll
-    for (int c = 0; c < 7; ++c) {
-      const double s = warp_sum_d(v[c]);
-      if (lane == 0) red[wid][m * 7 + c] = s;
+    for (int k = 0; k < 7; ++k) {
+      const double s = warp_sum_d(v[k]);
+      if (lane == 0) red[wid][m * 7 + k] = s;
     }
   }
   __syncthreads();
   if (threadIdx.x < M) {
     const int m = threadIdx.x;
     double t[7];
-    for (int c = 0; c < 7; ++c) {
+    for (int k = 0; k < 7; ++k) {
       double s = 0.0;
-      for (int w = 0; w < kSweepThreads / 32; ++w) s += red[w][m * 7 + c];
-      t[c] = s;
+      for (int w = 0; w < kSweepWarps; ++w) s += red[w][m * 7 + k];
+      t[k] = s;
     }
-    const double u = 1.0 / R.qscale;
-    const double gvx = t[1] * u, gvy = t[2] * u, gvz = t[3] * u;  // sum w (x - q), meters
+    const double gvx = t[1], gvy = t[2], gvz = t[3];  // sum w (x - q), meters
     const double* a = R.anchor;
     // sum w q x (x - q) = sum_j (q_j - a) x S_j + a x sum_j S_j
-    const double gwx = t[4] * u * u + (a[1] * gvz - a[2] * gvy);
-    const double gwy = t[5] * u * u + (a[2] * gvx - a[0] * gvz);
-    const double gwz = t[6] * u * u + (a[0] * gvy - a[1] * gvx);
+    const double gwx = t[4] + (a[1] * gvz - a[2] * gvy);
+    const double gwy = t[5] + (a[2] * gvx - a[0] * gvz);
+    const double gwz = t[6] + (a[0] * gvy - a[1] * gvx);
     const double g = R.sigma2 * R.inv_l2;
     double* o = R.out + m * kOut;
     o[0] = R.sigma2 * t[0];
@@ -792,7 +1037,7 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMinBlocks) k_sweep(const 
     o[7] = sqrt(__longlong_as_double((long long)db));
     R.disp_bits[m] = 0ull;
   }
-  if (threadIdx.x == 0) *R.counter = 0u;
+  if (blockIdx.x == 0 && threadIdx.x < 2 * n_ctl) next_chunk[threadIdx.x] = 0u;
 }
 
 __global__ void k_displacement(const double* zx, const double* zy, const double* zz, int n,
@@ -847,12 +1092,14 @@ void build_pairs_batched(const BuildReq* h, const BuildReq* d, int n, cudaStream
   }
   const dim3 gt(max(1, (max_nz + 7) / 8), n);  // warp per source
   k_filter<false><<<gt, 256, 0, st>>>(d);
+  k_order<<<dim3(max(1, (max_nz + kOrderWindow - 1) / kOrderWindow), n), kOrderWindow, 0, st>>>(d);
   k_tile_offsets<false><<<n, 1024, 0, st>>>(d);
   k_filter<true><<<gt, 256, 0, st>>>(d);
-  count_launch(launches + 3);
+  k_chunk_records<<<dim3(kMaxChunks / 8, n), 256, 0, st>>>(d);
+  count_launch(launches + 5);
 }
 
-void sweep_batched(const SweepReq* h, const SweepReq* d, int n, int blocks_per_req, cudaStream_t st,
+void sweep_batched(const SweepReq* h, const SweepReq* d, int n, int sm_count, unsigned* d_ctl, cudaStream_t st,
                    cudaEvent_t ev0, cudaEvent_t ev1) {
   if (n == 0) return;
   static bool attr_set = false;
@@ -866,27 +1113,37 @@ void sweep_batched(const SweepReq* h, const SweepReq* d, int n, int blocks_per_r
     attr_set = true;
   }
   if (ev0) cudaEventRecord(ev0, st);
-  // requests arrive grouped: gradient requests first, then F-only ones
-  int n_grad = 0;
+  // requests arrive grouped: gradient requests first, then F-only ones; one
+  // persistent launch per group (<= kMaxSweepReqs requests each), then one
+  // reduction over all requests
+  int n_grad = 0, max_nz = 1;
   while (n_grad < n && h[n_grad].grad) ++n_grad;
+  for (int r = 0; r < n; ++r) max_nz = max(max_nz, h[r].n_z);
+  k_displacement_batched<<<dim3((max_nz + 255) / 256, n), 256, 0, st>>>(d);
+  const int grid = 2 * sm_count;
+  int launches = 0;
   for (int grp = 0; grp < 2; ++grp) {
-    const int r0 = grp == 0 ? 0 : n_grad, r1 = grp == 0 ? n_grad : n;
-    if (r1 <= r0) continue;
-    int max_m = 1;
-    for (int r = r0; r < r1; ++r) max_m = max(max_m, h[r].M);
-    const dim3 g(blocks_per_req, r1 - r0);
-    const SweepReq* dr = d + r0;
-    if (grp == 0) {
-      if (max_m <= 2) k_sweep<1, true><<<g, kSweepThreads, kSweepSmem, st>>>(dr);
-      else if (max_m <= 4) k_sweep<2, true><<<g, kSweepThreads, kSweepSmem, st>>>(dr);
-      else k_sweep<4, true><<<g, kSweepThreads, kSweepSmem, st>>>(dr);
-    } else {
-      if (max_m <= 2) k_sweep<1, false><<<g, kSweepThreads, kSweepSmem, st>>>(dr);
-      else if (max_m <= 4) k_sweep<2, false><<<g, kSweepThreads, kSweepSmem, st>>>(dr);
-      else k_sweep<4, false><<<g, kSweepThreads, kSweepSmem, st>>>(dr);
+    const int g0 = grp == 0 ? 0 : n_grad, g1 = grp == 0 ? n_grad : n;
+    for (int r0 = g0; r0 < g1; r0 += kMaxSweepReqs) {
+      const int r1 = min(g1, r0 + kMaxSweepReqs);
+      int max_m = 1;
+      for (int r = r0; r < r1; ++r) max_m = max(max_m, h[r].M);
+      const SweepReq* dr = d + r0;
+      unsigned* ctl = d_ctl + 2 * (r0 / kMaxSweepReqs) + grp;
+      if (grp == 0) {
+        if (max_m <= 2) k_sweep<1, true><<<grid, kSweepThreads, kSweepSmem, st>>>(dr, r1 - r0, ctl);
+        else if (max_m <= 4) k_sweep<2, true><<<grid, kSweepThreads, kSweepSmem, st>>>(dr, r1 - r0, ctl);
+        else k_sweep<4, true><<<grid, kSweepThreads, kSweepSmem, st>>>(dr, r1 - r0, ctl);
+      } else {
+        if (max_m <= 2) k_sweep<1, false><<<grid, kSweepThreads, kSweepSmem, st>>>(dr, r1 - r0, ctl);
+        else if (max_m <= 4) k_sweep<2, false><<<grid, kSweepThreads, kSweepSmem, st>>>(dr, r1 - r0, ctl);
+        else k_sweep<4, false><<<grid, kSweepThreads, kSweepSmem, st>>>(dr, r1 - r0, ctl);
+      }
+      ++launches;
     }
-    count_launch(1);
   }
+  k_sweep_reduce<<<n, kSweepThreads, 0, st>>>(d, d_ctl, (n + kMaxSweepReqs - 1) / kMaxSweepReqs);
+  count_launch(launches + 2);
   if (ev1) cudaEventRecord(ev1, st);
 }
 

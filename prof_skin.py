@@ -34,5 +34,6 @@ for skin in skins:
                       "mean_it": sum(its) / len(its), "rounds": h["rounds"], "t_prepare": round(h["t_prepare_s"], 4),
                       "t_wait": round(h["t_wait_s"], 4), "t_solver": round(h["t_solver_s"], 4),
                       "t_build_prep": round(h["t_build_prep_s"], 4), "t_sweep_prep": round(h["t_sweep_prep_s"], 4),
-                      "sweep_ms": round(s["sweep_ms"], 1), "builds": b, "allocs": h["device_allocs"],
+                      "sweep_ms": round(s["sweep_ms"], 1), "pairs_streamed": s["pairs_streamed"],
+                      "slots_streamed": s["slots_streamed"], "pair_evals": s["pair_evals"], "builds": b, "allocs": h["device_allocs"],
                       "launches": ctx.kernel_launches()}), flush=True)

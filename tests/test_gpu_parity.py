@@ -333,6 +333,25 @@ def test_deterministic_and_batch_independent(ctx):
     assert np.array_equal(res[0].transform.as12(), a.transform.as12())
 
 
+def test_host_buffer_batch_matches_device_batch(ctx):
+    """register_batch_host (clouds staged on host threads, uploaded into the
+    context arena) gives bitwise the results of register_batch."""
+    Xs, Zs, inits = [], [], []
+    for s in (31, 32, 33):
+        X, Z, T = synth.kitti_pair(s, 6000)
+        Xs.append(X)
+        Zs.append(Z)
+        inits.append(synth.perturbed(T, s))
+    p, cfg = synth.kitti_params(), synth.kitti_subsequent_config()
+    a, sa = api.register_batch(Xs, Zs, inits, p, cfg)
+    for _ in range(2):  # the arena is reused by the second call
+        b, sb = api.register_batch_host(Xs, Zs, inits, p, cfg)
+        assert list(sa) == list(sb) == [0, 0, 0]
+        for ra, rb in zip(a, b):
+            assert np.array_equal(ra.transform.as12(), rb.transform.as12())
+            assert np.array_equal(ra.objective_trace, rb.objective_trace)
+
+
 def test_kitti_registration_end_to_end_vs_reference(ctx, ref):
     X, Z, Ts = synth.kitti_pair(7, 40000)
     p, cfg = synth.kitti_params(), synth.kitti_subsequent_config()
