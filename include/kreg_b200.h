@@ -161,7 +161,7 @@ kreg_status kreg_ctx_set_profiling(kreg_ctx* ctx, int32_t enabled);
 kreg_status kreg_ctx_set_max_active(kreg_ctx* ctx, int32_t n);
 /* Host-side round accounting: {rounds, s preparing + launching, s waiting for
  * the device, s preparing builds, s preparing sweeps, s in the solver state
- * machines, device allocations so far (process), bytes allocated}. */
+ * machines, device allocations so far (process), s spent in them (process)}. */
 kreg_status kreg_ctx_host_stats(const kreg_ctx* ctx, double out[8]);
 /* All counters: {sweep kernel ms (profiling on), sweep launches, pair-evals
  * (pairs x candidates), pairs streamed (sum of P per sweep request),

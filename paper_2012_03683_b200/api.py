@@ -155,7 +155,7 @@ class Context:
         _check(lib().kreg_ctx_host_stats(self.h, _abi.as_ptr(out)))
         return {"rounds": int(out[0]), "t_prepare_s": float(out[1]), "t_wait_s": float(out[2]),
                 "t_build_prep_s": float(out[3]), "t_sweep_prep_s": float(out[4]), "t_solver_s": float(out[5]),
-                "device_allocs": int(out[6]), "device_alloc_bytes": int(out[7])}
+                "device_allocs": int(out[6]), "device_alloc_s": float(out[7])}
 
     def sweep_stats(self):
         o = np.zeros(8)

@@ -206,8 +206,6 @@ kreg_status kreg_ctx_create(int32_t device, kreg_ctx** out) {
     KREG_CUDA(cudaSetDevice(device));
     KREG_CUDA(cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device));
     KREG_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
-    KREG_CUDA(cudaEventCreate(&ctx->ev_sweep0));
-    KREG_CUDA(cudaEventCreate(&ctx->ev_sweep1));
     ctx->launches_base = kreg_dev::kernel_launch_count();
     if (const char* sk = std::getenv("KREG_SKIN")) ctx->skin = std::atof(sk);
     *out = ctx.release();
@@ -235,13 +233,8 @@ kreg_status kreg_ctx_destroy(kreg_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
-    ctx->d_build.release();
-    ctx->d_sweep.release();
-    ctx->d_results.release();
     ctx->d_T2.release();
     ctx->d_disp.release();
-    cudaEventDestroy(ctx->ev_sweep0);
-    cudaEventDestroy(ctx->ev_sweep1);
     cudaStreamDestroy(ctx->stream);
     delete ctx;
   });
@@ -270,7 +263,7 @@ kreg_status kreg_ctx_host_stats(const kreg_ctx* ctx, double out[8]) {
     out[4] = ctx->t_sweep_prep;
     out[5] = ctx->t_total;
     out[6] = static_cast<double>(g_device_allocs);
-    out[7] = static_cast<double>(g_device_alloc_bytes);
+    out[7] = g_device_alloc_seconds;
   });
 }
 

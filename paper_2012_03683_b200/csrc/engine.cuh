@@ -39,6 +39,9 @@ constexpr int kMaxChunks = 1184;                 // chunks per request (8 x 148)
 constexpr int kMinChunkUnits = 8;                // >= 2 stages per chunk
 constexpr int kQueueDepth = 8;                   // chunks a warp may hold in its prefetch queue
 constexpr int kMaxSweepReqs = kSweepThreads;     // requests per sweep launch
+constexpr int kChunkGroup = 32;                  // chunk partials summed per group (first reduction level)
+constexpr int kMaxChunkGroups = (kMaxChunks + kChunkGroup - 1) / kChunkGroup;
+constexpr int kDispItem = 512;                   // sources per displacement work item
 constexpr int kMaxChannels = 8;
 constexpr int kMaxCandidates = 8;   // candidate transforms per sweep request
 constexpr int kOut = 8;             // {F, omega[3], v[3], max displacement}
@@ -143,15 +146,16 @@ struct alignas(16) SweepReq {
   float kappa;           // -log2(e) / (2 l^2): ex2 argument per m^2
   double sigma2;
   double inv_l2;
-  double* partials;      // kMaxChunks x M x (7 | 1)
+  double* partials;      // (kMaxChunks + kMaxChunkGroups) x M x (7 | 1): chunk, then group partials
   unsigned long long* disp_bits;  // M, max squared displacement (self-resetting)
   double* out;           // M x kOut
 };
 
 // All launches go to `stream`; d_reqs are device copies of h_reqs.
 void build_pairs_batched(const BuildReq* h_reqs, const BuildReq* d_reqs, int n, cudaStream_t stream);
-// d_ctl: 2 x ceil(n / kMaxSweepReqs) chunk counters, zero between launches
-// (reset by the reduction kernel).
+// d_ctl: sweep_ctl_bytes(n) bytes of launch control blocks, zero between
+// launches (the kernels reset them).
+size_t sweep_ctl_bytes(int n);
 void sweep_batched(const SweepReq* h_reqs, const SweepReq* d_reqs, int n, int sm_count, unsigned* d_ctl,
                    cudaStream_t stream, cudaEvent_t sweep_begin, cudaEvent_t sweep_end);
 void displacement(const double* zx, const double* zy, const double* zz, int n, const double* d_T2,

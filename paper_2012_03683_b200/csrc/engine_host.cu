@@ -13,6 +13,10 @@
 kreg_ctx::~kreg_ctx() {
   for (kreg_pairs* p : pool) delete p;
   pool.clear();
+  for (auto*& S : rs) {
+    delete S;
+    S = nullptr;
+  }
 }
 
 namespace kreg_host {
@@ -415,8 +419,9 @@ static void prepare_build(kreg_ctx* ctx, BuildJob& job, kreg_dev::BuildReq& R) {
     R.n_cells = g[0] * g[1] * g[2];
     p->n_cells = R.n_cells;
     p->gx = R.gx; p->gy = R.gy; p->gz = R.gz;
-    p->cell_count.ensure(static_cast<size_t>(R.n_cells) + 1, /*zero=*/true);
-    p->cell_start.ensure(static_cast<size_t>(R.n_cells) + 1);
+    ctx->hw_cells = std::max(ctx->hw_cells, R.n_cells + 1);
+    p->cell_count.ensure(static_cast<size_t>(ctx->hw_cells), /*zero=*/true);
+    p->cell_start.ensure(static_cast<size_t>(ctx->hw_cells));
     p->cell_of.ensure(nx + 1);
     p->tmp_items.ensure(nx + 1);
     p->cell_items.ensure(nx + 1);
@@ -425,7 +430,10 @@ static void prepare_build(kreg_ctx* ctx, BuildJob& job, kreg_dev::BuildReq& R) {
     p->cz.ensure(nx + 1);
     p->scan_tiles.ensure(static_cast<size_t>(R.n_cells / kreg_dev::kScanTile + 4));
     const long long want = p->expected_sup > 0 ? p->expected_sup : static_cast<long long>(nz) * 256 + 4096;
-    if (p->sup.cap < static_cast<size_t>(want)) p->sup.ensure(static_cast<size_t>(want), false, 1.25);
+    if (p->sup.cap < static_cast<size_t>(want)) {
+      p->sup.ensure(static_cast<size_t>(std::max<long long>(want + want / 4, ctx->hw_sup)), false, 1.0);
+      ctx->hw_sup = std::max<long long>(ctx->hw_sup, static_cast<long long>(p->sup.cap));
+    }
     R.cell_count = p->cell_count.ptr;
     R.cell_start = p->cell_start.ptr;
     R.cell_of = p->cell_of.ptr;
@@ -464,8 +472,9 @@ static void prepare_build(kreg_ctx* ctx, BuildJob& job, kreg_dev::BuildReq& R) {
   R.chunks = p->chunks.ptr;
   const long long want = p->expected_pairs > 0 ? p->expected_pairs : static_cast<long long>(nz) * 96 + 4096;
   if (p->slot_buf.cap < static_cast<size_t>(want)) {
-    p->slot_buf.ensure(static_cast<size_t>(want), false, 1.5);
+    p->slot_buf.ensure(static_cast<size_t>(std::max<long long>(want + want / 2, ctx->hw_slots)), false, 1.0);
     p->slot_i.ensure(p->slot_buf.cap, false, 1.0);
+    ctx->hw_slots = std::max<long long>(ctx->hw_slots, static_cast<long long>(p->slot_buf.cap));
   }
   p->tile_off.ensure(n_tiles + 2);
   p->unit_off.ensure(n_tiles + 2);
@@ -492,10 +501,10 @@ static long long sweep_units(const kreg_pairs* p) {
 
 // chunk partials of one request: at most kMaxChunks x M x (7 | 1) doubles
 static size_t sweep_partials(const EvalJob& job) {
-  return static_cast<size_t>(kreg_dev::kMaxChunks) * job.M * (job.grad ? 7 : 1);
+  return static_cast<size_t>(kreg_dev::kMaxChunks + kreg_dev::kMaxChunkGroups) * job.M * (job.grad ? 7 : 1);
 }
 
-static void prepare_sweep(kreg_ctx* ctx, EvalJob& job, kreg_dev::SweepReq& R, const SweepScratch& s, int e) {
+static void prepare_sweep(EvalJob& job, kreg_dev::SweepReq& R, double* partials, unsigned long long* disp_bits) {
   kreg_pairs* p = job.pairs;
   std::memset(&R, 0, sizeof(R));
   const int nz = p->Z->n;
@@ -526,29 +535,52 @@ static void prepare_sweep(kreg_ctx* ctx, EvalJob& job, kreg_dev::SweepReq& R, co
   R.kappa = static_cast<float>(-1.4426950408889634 / (2.0 * l * l));
   R.sigma2 = p->sigma * p->sigma;
   R.inv_l2 = 1.0 / (l * l);
-  R.partials = ctx->part_arena.ptr + s.part_off;
-  R.disp_bits = ctx->disp_arena.ptr + static_cast<size_t>(e) * kreg_dev::kMaxCandidates;
+  R.partials = partials;
+  R.disp_bits = disp_bits;
 }
 
-void run_round(kreg_ctx* ctx, std::vector<BuildJob>& builds, std::vector<EvalJob>& evals) {
+RoundSlot* round_slot(kreg_ctx* ctx, int i) {
+  if (!ctx->rs[i]) {
+    auto* S = new RoundSlot;
+    KREG_CUDA(cudaEventCreateWithFlags(&S->done, cudaEventDisableTiming));
+    KREG_CUDA(cudaEventCreate(&S->ev0));
+    KREG_CUDA(cudaEventCreate(&S->ev1));
+    ctx->rs[i] = S;
+  }
+  return ctx->rs[i];
+}
+
+RoundSlot::~RoundSlot() {
+  if (done) cudaEventDestroy(done);
+  if (ev0) cudaEventDestroy(ev0);
+  if (ev1) cudaEventDestroy(ev1);
+}
+
+void begin_round(kreg_ctx* ctx, RoundSlot& S, std::vector<BuildJob>&& builds_in, std::vector<EvalJob>&& evals_in) {
+  S.builds = std::move(builds_in);
+  S.evals = std::move(evals_in);
+  std::vector<BuildJob>& builds = S.builds;
+  std::vector<EvalJob>& evals = S.evals;
   const int nb = static_cast<int>(builds.size());
   const int ne = static_cast<int>(evals.size());
+  S.in_flight = false;
   if (nb == 0 && ne == 0) return;
   using clk = std::chrono::steady_clock;
   const auto t0 = clk::now();
   KREG_CUDA(cudaSetDevice(ctx->device));
-  ctx->h_build.ensure(nb + 1);
-  ctx->d_build.ensure(nb + 1);
-  ctx->h_sweep.ensure(ne + 1);
-  ctx->d_sweep.ensure(ne + 1);
+  S.h_build.ensure(nb + 1);
+  S.d_build.ensure(nb + 1);
+  S.h_sweep.ensure(ne + 1);
+  S.d_sweep.ensure(ne + 1);
   const size_t n_res = static_cast<size_t>(ne) * kreg_dev::kMaxCandidates * kreg_dev::kOut + kreg_dev::kBuildStatus * (nb + 1);
-  ctx->d_results.ensure(n_res);
-  ctx->h_results.ensure(n_res);
+  S.n_res = n_res;
+  S.d_results.ensure(n_res);
+  S.h_results.ensure(n_res);
 
   for (int b = 0; b < nb; ++b) {
-    prepare_build(ctx, builds[b], ctx->h_build.ptr[b]);
-    ctx->h_build.ptr[b].status = ctx->d_results.ptr + static_cast<size_t>(ne) * kreg_dev::kMaxCandidates * kreg_dev::kOut +
-                                    kreg_dev::kBuildStatus * b;
+    prepare_build(ctx, builds[b], S.h_build.ptr[b]);
+    S.h_build.ptr[b].status = S.d_results.ptr + static_cast<size_t>(ne) * kreg_dev::kMaxCandidates * kreg_dev::kOut +
+                              kreg_dev::kBuildStatus * b;
   }
   const auto tb = clk::now();
   ctx->t_build_prep += std::chrono::duration<double>(tb - t0).count();
@@ -561,45 +593,56 @@ void run_round(kreg_ctx* ctx, std::vector<BuildJob>& builds, std::vector<EvalJob
     part_total += sweep_partials(evals[e]);
   }
   if (ne) {
-    ctx->part_arena.ensure(part_total + 1, false, 1.5);
-    ctx->counter_arena.ensure(2 * (ne / kreg_dev::kMaxSweepReqs + 1) + 2, /*zero=*/true);
-    ctx->disp_arena.ensure(static_cast<size_t>(ne + 1) * kreg_dev::kMaxCandidates, /*zero=*/true);
+    S.part_arena.ensure(part_total + 1, false, 1.5);
+    S.counter_arena.ensure(kreg_dev::sweep_ctl_bytes(ne) / sizeof(unsigned) + 1, /*zero=*/true);
+    S.disp_arena.ensure(static_cast<size_t>(ne + 1) * kreg_dev::kMaxCandidates, /*zero=*/true);
   }
   for (int e = 0; e < ne; ++e) {
-    prepare_sweep(ctx, evals[e], ctx->h_sweep.ptr[e], scratch[e], e);
-    ctx->h_sweep.ptr[e].out = ctx->d_results.ptr + static_cast<size_t>(e) * kreg_dev::kMaxCandidates * kreg_dev::kOut;
+    prepare_sweep(evals[e], S.h_sweep.ptr[e], S.part_arena.ptr + scratch[e].part_off,
+                  S.disp_arena.ptr + static_cast<size_t>(e) * kreg_dev::kMaxCandidates);
+    S.h_sweep.ptr[e].out = S.d_results.ptr + static_cast<size_t>(e) * kreg_dev::kMaxCandidates * kreg_dev::kOut;
   }
   const auto ts = clk::now();
   ctx->t_sweep_prep += std::chrono::duration<double>(ts - tb).count();
   if (nb)
-    KREG_CUDA(cudaMemcpyAsync(ctx->d_build.ptr, ctx->h_build.ptr, sizeof(kreg_dev::BuildReq) * nb,
-                              cudaMemcpyHostToDevice, ctx->stream));
+    KREG_CUDA(cudaMemcpyAsync(S.d_build.ptr, S.h_build.ptr, sizeof(kreg_dev::BuildReq) * nb, cudaMemcpyHostToDevice,
+                              ctx->stream));
   if (ne)
-    KREG_CUDA(cudaMemcpyAsync(ctx->d_sweep.ptr, ctx->h_sweep.ptr, sizeof(kreg_dev::SweepReq) * ne,
-                              cudaMemcpyHostToDevice, ctx->stream));
-  if (nb) kreg_dev::build_pairs_batched(ctx->h_build.ptr, ctx->d_build.ptr, nb, ctx->stream);
+    KREG_CUDA(cudaMemcpyAsync(S.d_sweep.ptr, S.h_sweep.ptr, sizeof(kreg_dev::SweepReq) * ne, cudaMemcpyHostToDevice,
+                              ctx->stream));
+  if (nb) kreg_dev::build_pairs_batched(S.h_build.ptr, S.d_build.ptr, nb, ctx->stream);
   if (ne) {
-    kreg_dev::sweep_batched(ctx->h_sweep.ptr, ctx->d_sweep.ptr, ne, ctx->sm_count, ctx->counter_arena.ptr, ctx->stream,
-                            ctx->profiling ? ctx->ev_sweep0 : nullptr, ctx->profiling ? ctx->ev_sweep1 : nullptr);
+    kreg_dev::sweep_batched(S.h_sweep.ptr, S.d_sweep.ptr, ne, ctx->sm_count, S.counter_arena.ptr, ctx->stream,
+                            ctx->profiling ? S.ev0 : nullptr, ctx->profiling ? S.ev1 : nullptr);
   }
   KREG_CUDA(cudaGetLastError());
-  KREG_CUDA(cudaMemcpyAsync(ctx->h_results.ptr, ctx->d_results.ptr, sizeof(double) * n_res,
-                            cudaMemcpyDeviceToHost, ctx->stream));
-  const auto t1 = clk::now();
-  KREG_CUDA(cudaStreamSynchronize(ctx->stream));
-  const auto t2 = clk::now();
-  ctx->rounds += 1;
-  ctx->t_prepare += std::chrono::duration<double>(t1 - t0).count();
-  ctx->t_wait += std::chrono::duration<double>(t2 - t1).count();
+  KREG_CUDA(cudaMemcpyAsync(S.h_results.ptr, S.d_results.ptr, sizeof(double) * n_res, cudaMemcpyDeviceToHost,
+                            ctx->stream));
+  KREG_CUDA(cudaEventRecord(S.done, ctx->stream));
+  S.in_flight = true;
+  ctx->t_prepare += std::chrono::duration<double>(clk::now() - t0).count();
+}
 
-  const double* res = ctx->h_results.ptr;
+void end_round(kreg_ctx* ctx, RoundSlot& S) {
+  if (!S.in_flight) return;
+  using clk = std::chrono::steady_clock;
+  const auto t1 = clk::now();
+  KREG_CUDA(cudaEventSynchronize(S.done));
+  S.in_flight = false;
+  ctx->t_wait += std::chrono::duration<double>(clk::now() - t1).count();
+  ctx->rounds += 1;
+  std::vector<BuildJob>& builds = S.builds;
+  std::vector<EvalJob>& evals = S.evals;
+  const int nb = static_cast<int>(builds.size());
+  const int ne = static_cast<int>(evals.size());
+  const double* res = S.h_results.ptr;
   std::vector<int> redo;
   for (int b = 0; b < nb; ++b) {
     const double* st =
         res + static_cast<size_t>(ne) * kreg_dev::kMaxCandidates * kreg_dev::kOut + kreg_dev::kBuildStatus * b;
     BuildJob& job = builds[b];
     kreg_pairs* p = job.pairs;
-    const bool full = ctx->h_build.ptr[b].full != 0;
+    const bool full = S.h_build.ptr[b].full != 0;
     bool ok = true;
     if (full) {
       p->sup_entries = static_cast<long long>(st[4]);
@@ -638,7 +681,9 @@ void run_round(kreg_ctx* ctx, std::vector<BuildJob>& builds, std::vector<EvalJob
     // grow and re-run the failed builds and every evaluation in this round
     std::vector<BuildJob> b2;
     for (int b : redo) b2.push_back(builds[b]);
-    run_round(ctx, b2, evals);
+    std::vector<EvalJob> e2 = std::move(evals);
+    begin_round(ctx, S, std::move(b2), std::move(e2));
+    end_round(ctx, S);
     return;
   }
   for (int e = 0; e < ne; ++e) {
@@ -652,17 +697,22 @@ void run_round(kreg_ctx* ctx, std::vector<BuildJob>& builds, std::vector<EvalJob
     ctx->sweep_launches += 1;
     if (ctx->profiling) {
       float ms = 0.0f;
-      KREG_CUDA(cudaEventElapsedTime(&ms, ctx->ev_sweep0, ctx->ev_sweep1));
+      KREG_CUDA(cudaEventElapsedTime(&ms, S.ev0, S.ev1));
       ctx->sweep_ms += ms;
     }
   }
+}
+
+void run_round(kreg_ctx* ctx, std::vector<BuildJob>& builds, std::vector<EvalJob>& evals) {
+  RoundSlot& S = *round_slot(ctx, 2);
+  begin_round(ctx, S, std::move(builds), std::move(evals));
+  end_round(ctx, S);
 }
 
 double max_point_displacement_dev(kreg_ctx* ctx, const kreg_cloud* Z, const double* built, const double* now) {
   if (Z->n == 0) return 0.0;
   ctx->d_T2.ensure(24);
   ctx->d_disp.ensure(1);
-  ctx->h_results.ensure(4);
   double T2[24];
   std::memcpy(T2, built, sizeof(double) * 12);
   std::memcpy(T2 + 12, now, sizeof(double) * 12);

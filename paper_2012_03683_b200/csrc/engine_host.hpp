@@ -5,6 +5,7 @@
 
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <cstdint>
 #include <memory>
 #include <stdexcept>
@@ -32,6 +33,7 @@ struct Error : std::runtime_error {
 // device allocation accounting (count, bytes) — cudaMalloc/cudaFree synchronise
 inline long long g_device_allocs = 0;
 inline long long g_device_alloc_bytes = 0;
+inline double g_device_alloc_seconds = 0.0;  // host time spent in cudaFree/cudaMalloc/cudaMemset of DevBuf
 
 template <typename T>
 struct DevBuf {
@@ -57,6 +59,7 @@ struct DevBuf {
   // grow (discarding contents) to hold at least n elements; optional zero fill
   void ensure(size_t n, bool zero = false, double slack = 1.25) {
     if (n <= cap && ptr) return;
+    const auto t0 = std::chrono::steady_clock::now();
     release();
     size_t want = n < 16 ? 16 : static_cast<size_t>(static_cast<double>(n) * slack);
     ++g_device_allocs;
@@ -69,6 +72,7 @@ struct DevBuf {
     }
     cap = want;
     if (zero) KREG_CUDA(cudaMemset(ptr, 0, want * sizeof(T)));
+    g_device_alloc_seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   }
 };
 
@@ -104,13 +108,14 @@ struct Config {  // RegistrationConfig (registration.hpp:13-40)
   kreg_registration_config c;
 };
 
+struct RoundSlot;
+
 }  // namespace kreg_host
 
 struct kreg_ctx {
   int device = 0;
   int sm_count = 148;
   cudaStream_t stream = nullptr;
-  cudaEvent_t ev_sweep0 = nullptr, ev_sweep1 = nullptr;
   bool profiling = false;
   double sweep_ms = 0.0;
   long long sweep_launches = 0;
@@ -118,19 +123,12 @@ struct kreg_ctx {
   long long pairs_streamed = 0;
   long long slots_streamed = 0;
   long long launches_base = 0;
-  // round staging
-  kreg_host::DevBuf<kreg_dev::BuildReq> d_build;
-  kreg_host::DevBuf<kreg_dev::SweepReq> d_sweep;
-  kreg_host::PinnedBuf<kreg_dev::BuildReq> h_build;
-  kreg_host::PinnedBuf<kreg_dev::SweepReq> h_sweep;
-  kreg_host::DevBuf<double> d_results;
-  kreg_host::PinnedBuf<double> h_results;
+  // round staging: slots 0 and 1 alternate in the batched solver (one round
+  // in flight on the device while the host plans the other), slot 2 serves
+  // the synchronous calls
+  kreg_host::RoundSlot* rs[3] = {nullptr, nullptr, nullptr};
   kreg_host::DevBuf<double> d_T2;
   kreg_host::DevBuf<unsigned long long> d_disp;
-  // per-round sweep scratch arenas (one slice per request)
-  kreg_host::DevBuf<double> part_arena;
-  kreg_host::DevBuf<unsigned int> counter_arena;        // sweep chunk counters, self-resetting
-  kreg_host::DevBuf<unsigned long long> disp_arena;    // self-resetting, zero between rounds
   // end-to-end calls: pinned host staging and device arena of their clouds
   kreg_host::PinnedBuf<double> stage_d;
   kreg_host::PinnedBuf<float> stage_f;
@@ -141,6 +139,9 @@ struct kreg_ctx {
   int max_active = 0;  // lockstep window of kreg_register_batch (0 = all at once)
   // candidate-list radius R_s = cutoff (1 + skin); 0 disables reuse
   double skin = 0.25;
+  // capacity high-water marks over all workspaces: a pooled workspace that
+  // must grow goes straight to the largest size any registration needed
+  long long hw_slots = 0, hw_sup = 0, hw_cells = 0;
   long long full_builds = 0, filter_builds = 0;
   // host-side round accounting (seconds)
   long long rounds = 0;
@@ -258,9 +259,33 @@ struct EvalJob {
   bool grad = true;    // false: F + displacement only (gradient left zero)
 };
 
-// Executes builds (then, in stream order, evaluations) as batched launches,
-// one D2H, one synchronize. Builds whose pair list overflowed its capacity
-// are grown and re-run transparently. Updates pairs->P.
+// Device resources of one in-flight round.
+struct RoundSlot {
+  DevBuf<kreg_dev::BuildReq> d_build;
+  PinnedBuf<kreg_dev::BuildReq> h_build;
+  DevBuf<kreg_dev::SweepReq> d_sweep;
+  PinnedBuf<kreg_dev::SweepReq> h_sweep;
+  DevBuf<double> d_results;
+  PinnedBuf<double> h_results;
+  DevBuf<double> part_arena;                // sweep chunk partials (one slice per request)
+  DevBuf<unsigned int> counter_arena;       // sweep chunk counters, self-resetting
+  DevBuf<unsigned long long> disp_arena;    // displacement maxima, self-resetting
+  cudaEvent_t done = nullptr, ev0 = nullptr, ev1 = nullptr;
+  std::vector<BuildJob> builds;
+  std::vector<EvalJob> evals;
+  size_t n_res = 0;
+  bool in_flight = false;
+  ~RoundSlot();
+};
+RoundSlot* round_slot(kreg_ctx* ctx, int i);
+
+// Executes builds (then, in stream order, evaluations) as batched launches
+// and one D2H, without waiting (begin_round); end_round waits for the slot's
+// round and stores the results. Builds whose pair list overflowed its
+// capacity are grown and re-run transparently. Updates pairs->P.
+void begin_round(kreg_ctx* ctx, RoundSlot& S, std::vector<BuildJob>&& builds, std::vector<EvalJob>&& evals);
+void end_round(kreg_ctx* ctx, RoundSlot& S);
+// begin_round + end_round on the synchronous slot.
 void run_round(kreg_ctx* ctx, std::vector<BuildJob>& builds, std::vector<EvalJob>& evals);
 
 double max_point_displacement_dev(kreg_ctx* ctx, const kreg_cloud* Z, const double* built, const double* now);

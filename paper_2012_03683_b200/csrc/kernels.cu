@@ -688,6 +688,66 @@ __device__ __forceinline__ f2_t warp_sum_f2(f2_t v) {
   return v;
 }
 
+// Launch control block (device, zero between launches: the last CTA to exit
+// resets the global counters, request finishers reset theirs).
+struct SweepCtl {
+  unsigned next_item;              // work-item queue head
+  unsigned exited;                 // CTAs done
+  unsigned req_done[kMaxSweepReqs];                    // finished groups + displacement items
+  unsigned grp_done[kMaxSweepReqs][kMaxChunkGroups];  // finished chunks per group
+};
+
+// A request's work item (chunk group or displacement slice) is complete; the
+// warp completing its last item adds the group partials in a fixed order and
+// writes F, the gradient (inner_product.cpp:121-157, assembled in FP64) and
+// the displacement; resets the request's counters and displacement bits.
+template <bool GRAD>
+__device__ __noinline__ void item_done(const SweepReq& R, SweepCtl* ctl, int r, int n_items, int MV, int lane) {
+  unsigned old = 0;
+  if (lane == 0) old = atomicAdd(&ctl->req_done[r], 1u);
+  old = __shfl_sync(0xffffffffu, old, 0);
+  if ((int)old != n_items - 1) return;
+  __threadfence();
+  const int C = chunk_count(request_units(R));
+  const int NG = (C + kChunkGroup - 1) / kChunkGroup;
+  const double* gpart = R.partials + (size_t)kMaxChunks * MV;
+  double v0 = 0.0, v1 = 0.0;  // values lane and lane + 32
+  for (int g = 0; g < NG; ++g) {
+    if (lane < MV) v0 += __ldcg(gpart + (size_t)g * MV + lane);
+    if (lane + 32 < MV) v1 += __ldcg(gpart + (size_t)g * MV + lane + 32);
+  }
+  const int M = R.M, NV = GRAD ? 7 : 1;
+  double t[7];
+#pragma unroll
+  for (int k = 0; k < 7; ++k) {
+    const int src = (lane < M ? lane : 0) * NV + (k < NV ? k : 0);
+    const double a = __shfl_sync(0xffffffffu, v0, src & 31);
+    const double b = __shfl_sync(0xffffffffu, v1, src & 31);
+    t[k] = k < NV ? (src < 32 ? a : b) : 0.0;
+  }
+  if (lane < M) {
+    const double gvx = t[1], gvy = t[2], gvz = t[3];  // sum w (x - q), meters
+    const double* a = R.anchor;
+    // sum w q x (x - q) = sum_j (q_j - a) x S_j + a x sum_j S_j
+    const double gwx = t[4] + (a[1] * gvz - a[2] * gvy);
+    const double gwy = t[5] + (a[2] * gvx - a[0] * gvz);
+    const double gwz = t[6] + (a[0] * gvy - a[1] * gvx);
+    const double g = R.sigma2 * R.inv_l2;
+    double* o = R.out + lane * kOut;
+    o[0] = R.sigma2 * t[0];
+    o[1] = g * gwx;
+    o[2] = g * gwy;
+    o[3] = g * gwz;
+    o[4] = g * gvx;
+    o[5] = g * gvy;
+    o[6] = g * gvz;
+    const unsigned long long db = __ldcg(&R.disp_bits[lane]);
+    o[7] = sqrt(__longlong_as_double((long long)db));
+    R.disp_bits[lane] = 0ull;
+  }
+  if (lane == 0) ctl->req_done[r] = 0u;
+}
+
 // Per-warp chunk queue and TMA producer state (driven by lane 0).
 struct WarpQueue {
   int ids[kQueueDepth];
@@ -701,11 +761,13 @@ struct WarpQueue {
 };
 
 template <int NP, bool GRAD>
-__global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(const SweepReq* reqs, int n_req, unsigned* next_chunk) {
+__global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(const SweepReq* reqs, int n_req, SweepCtl* ctl) {
   constexpr int MAXM = 2 * NP;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  unsigned* next_chunk = &ctl->next_item;
   __shared__ int cbase[kMaxSweepReqs + 1];
   __shared__ int units_s[kMaxSweepReqs];
+  __shared__ int disp_s[kMaxSweepReqs];  // displacement items of each request
   __shared__ WarpQueue wq[kSweepWarps];
   extern __shared__ __align__(128) unsigned char dyn_smem[];
   int4* ring = reinterpret_cast<int4*>(dyn_smem) + (size_t)wid * kSweepStages * kStageSlots;
@@ -716,13 +778,17 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(const SweepReq* reqs
                                             (size_t)kSweepWarps * kRecSlots * sizeof(ChunkRec)) +
       wid * kSweepStages;
 
-  // chunk prefix over the launch's requests (every CTA computes it)
+  // work items of request r: disp_s[r] displacement slices, then its chunks;
+  // item prefix over the launch's requests (every CTA computes it)
   {
     int C = 0;
     if (threadIdx.x < n_req) {
-      const long long U = request_units(reqs[threadIdx.x]);
-      C = chunk_count(U);
+      const SweepReq& Rq = reqs[threadIdx.x];
+      const long long U = request_units(Rq);
+      const int D = (Rq.n_z + kDispItem - 1) / kDispItem;
+      C = chunk_count(U) + D;
       units_s[threadIdx.x] = (int)U;
+      disp_s[threadIdx.x] = D;
     }
     int tot;
     const int ex = block_excl_scan<int>(C, &tot);
@@ -764,11 +830,13 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(const SweepReq* reqs
         return false;
       }
       const int r = locate(g);
-      const long long U = units_s[r], cu = chunk_units(U);
       Q.ids[Q.tail % kQueueDepth] = g;
       ++Q.tail;
+      const int i = g - cbase[r] - disp_s[r];
+      if (i < 0) continue;  // displacement item: no stages
+      const long long U = units_s[r], cu = chunk_units(U);
       Q.pr = r;
-      Q.pc = g - cbase[r];
+      Q.pc = i;
       Q.pu = (long long)Q.pc * cu;
       Q.pend = min(U, Q.pu + cu);
       Q.first = 1;
@@ -810,8 +878,50 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(const SweepReq* reqs
     const int r = locate(g);
     const SweepReq& R = reqs[r];
     const int M = R.M;
+    const int MV = M * (GRAD ? 7 : 1);
     const long long U = units_s[r], cu = chunk_units(U);
-    const int c = g - cbase[r];
+    const int D = disp_s[r];
+    const int C = cbase[r + 1] - cbase[r] - D;
+    const int NG = (C + kChunkGroup - 1) / kChunkGroup;
+    const int c = g - cbase[r] - D;
+    if (c < 0) {
+      // displacement slice (FP64 over the original coordinates, order-free max)
+      const int j0 = (c + D) * kDispItem, j1 = min(R.n_z, j0 + kDispItem);
+      unsigned long long dmax[MAXM];
+#pragma unroll
+      for (int m = 0; m < MAXM; ++m) dmax[m] = 0ull;
+#pragma unroll 4
+      for (int j = j0 + lane; j < j1; j += 32) {
+        const double zx = R.zx[j], zy = R.zy[j], zz = R.zz[j];
+        double bx, by, bz;
+        apply_T(R.Tb, zx, zy, zz, bx, by, bz);
+#pragma unroll
+        for (int m = 0; m < MAXM; ++m) {
+          if (m < M) {
+            double x, y, z;
+            apply_T(R.T[m], zx, zy, zz, x, y, z);
+            const double dx = x - bx, dy = y - by, dz = z - bz;
+            const unsigned long long d2 = (unsigned long long)__double_as_longlong(dx * dx + dy * dy + dz * dz);
+            dmax[m] = d2 > dmax[m] ? d2 : dmax[m];
+          }
+        }
+      }
+#pragma unroll
+      for (int m = 0; m < MAXM; ++m) {
+        unsigned long long d = dmax[m];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const unsigned long long other = __shfl_xor_sync(0xffffffffu, d, o);
+          d = other > d ? other : d;
+        }
+        if (lane == 0 && m < M && d) atomicMax(&R.disp_bits[m], d);
+      }
+      item_done<GRAD>(R, ctl, r, NG + D, MV, lane);
+      __syncwarp();
+      if (lane == 0) ++Q.head;
+      __syncwarp();
+      continue;
+    }
     const long long u0 = (long long)c * cu, u1 = min(U, u0 + cu);
     const f2_t kap2 = pk2(R.kappa, R.kappa);
 #pragma unroll
@@ -933,111 +1043,54 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(const SweepReq* reqs
       flush_tile();
     }
 
-    // chunk partial: FP32 warp sums (fixed butterfly order) widened to FP64
-    double* part = R.partials + (size_t)c * (M * (GRAD ? 7 : 1));
+    // chunk partial: FP32 warp sums (fixed butterfly order) widened to FP64;
+    // lane v stores value v
+    double* part = R.partials + (size_t)c * MV;
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
 #pragma unroll
       for (int v = 0; v < (GRAD ? 7 : 1); ++v) {
         float a0, a1;
         upk2(warp_sum_f2(acc[p][v]), a0, a1);
-        if (lane == 0) {
-          if (2 * p < M) part[(2 * p) * (GRAD ? 7 : 1) + v] = (double)a0;
-          if (2 * p + 1 < M) part[(2 * p + 1) * (GRAD ? 7 : 1) + v] = (double)a1;
-        }
+        const int i0 = (2 * p) * (GRAD ? 7 : 1) + v, i1 = (2 * p + 1) * (GRAD ? 7 : 1) + v;
+        if (2 * p < M && lane == (i0 & 31)) part[i0] = (double)a0;
+        if (2 * p + 1 < M && lane == (i1 & 31)) part[i1] = (double)a1;
       }
+    }
+    // chunk group done? its last chunk sums the group's partials in order
+    __threadfence();
+    __syncwarp();
+    const int grp = c / kChunkGroup;
+    unsigned old = 0;
+    if (lane == 0) old = atomicAdd(&ctl->grp_done[r][grp], 1u);
+    old = __shfl_sync(0xffffffffu, old, 0);
+    const int gsize = min(kChunkGroup, C - grp * kChunkGroup);
+    if ((int)old == gsize - 1) {
+      __threadfence();
+      double* gpart = R.partials + (size_t)kMaxChunks * MV + (size_t)grp * MV;
+      for (int v = lane; v < MV; v += 32) {
+        double t = 0.0;
+        for (int k = grp * kChunkGroup; k < grp * kChunkGroup + gsize; ++k) t += __ldcg(R.partials + (size_t)k * MV + v);
+        gpart[v] = t;
+      }
+      if (lane == 0) ctl->grp_done[r][grp] = 0u;
+      __threadfence();
+      __syncwarp();
+      item_done<GRAD>(R, ctl, r, NG + D, MV, lane);
     }
     __syncwarp();
     if (lane == 0) ++Q.head;
     __syncwarp();
   }
-}
-
-// Displacement max_j |T_m z_j - T_b z_j| (inner_product.cpp:238-246) of every
-// sweep request in FP64 over the original coordinates; warp max, one atomic
-// per warp and candidate (max is order-free). grid = (n_z / 256, requests).
-__global__ void __launch_bounds__(256) k_displacement_batched(const SweepReq* reqs) {
-  const SweepReq& R = reqs[blockIdx.y];
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (blockIdx.x * blockDim.x >= R.n_z) return;
-  const int M = R.M;
-  double zx = 0, zy = 0, zz = 0, bx = 0, by = 0, bz = 0;
-  const bool ok = j < R.n_z;
-  if (ok) {
-    zx = R.zx[j];
-    zy = R.zy[j];
-    zz = R.zz[j];
-    apply_T(R.Tb, zx, zy, zz, bx, by, bz);
-  }
-  for (int m = 0; m < M; ++m) {
-    unsigned long long d2 = 0;
-    if (ok) {
-      double x, y, z;
-      apply_T(R.T[m], zx, zy, zz, x, y, z);
-      const double dx = x - bx, dy = y - by, dz = z - bz;
-      d2 = (unsigned long long)__double_as_longlong(dx * dx + dy * dy + dz * dz);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const unsigned long long other = __shfl_xor_sync(0xffffffffu, d2, o);
-      d2 = other > d2 ? other : d2;
-    }
-    if ((threadIdx.x & 31) == 0 && d2) atomicMax(&R.disp_bits[m], d2);
-  }
-}
-
-// Final sums of every request (one CTA each): partials of its chunks in a
-// fixed order (thread-contiguous ranges, then a fixed tree), the gradient
-// assembled in FP64 (inner_product.cpp:121-157), displacement from the max
-// bits; resets the displacement bits and the launches' chunk counters.
-__global__ void __launch_bounds__(kSweepThreads) k_sweep_reduce(const SweepReq* reqs, unsigned* next_chunk,
-                                                                 int n_ctl) {
-  const SweepReq& R = reqs[blockIdx.x];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int M = R.M, NV = R.grad ? 7 : 1;
-  const int C = chunk_count(request_units(R));
-  __shared__ double red[kSweepWarps][kMaxCandidates * 7];
-  const int per = (C + kSweepThreads - 1) / kSweepThreads;
-  const int c0 = threadIdx.x * per, c1 = min(C, c0 + per);
-  for (int m = 0; m < M; ++m) {
-    double v[7] = {0, 0, 0, 0, 0, 0, 0};
-    for (int c = c0; c < c1; ++c)
-      for (int k = 0; k < NV; ++k) v[k] += __ldcg(R.partials + (size_t)c * (M * NV) + m * NV + k);
-#pragma unroll
-    for (int k = 0; k < 7; ++k) {
-      const double s = warp_sum_d(v[k]);
-      if (lane == 0) red[wid][m * 7 + k] = s;
-    }
-  }
+  // the last CTA to exit resets the launch's item counter
   __syncthreads();
-  if (threadIdx.x < M) {
-    const int m = threadIdx.x;
-    double t[7];
-    for (int k = 0; k < 7; ++k) {
-      double s = 0.0;
-      for (int w = 0; w < kSweepWarps; ++w) s += red[w][m * 7 + k];
-      t[k] = s;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&ctl->exited, 1u) == gridDim.x - 1) {
+      ctl->next_item = 0u;
+      ctl->exited = 0u;
     }
-    const double gvx = t[1], gvy = t[2], gvz = t[3];  // sum w (x - q), meters
-    const double* a = R.anchor;
-    // sum w q x (x - q) = sum_j (q_j - a) x S_j + a x sum_j S_j
-    const double gwx = t[4] + (a[1] * gvz - a[2] * gvy);
-    const double gwy = t[5] + (a[2] * gvx - a[0] * gvz);
-    const double gwz = t[6] + (a[0] * gvy - a[1] * gvx);
-    const double g = R.sigma2 * R.inv_l2;
-    double* o = R.out + m * kOut;
-    o[0] = R.sigma2 * t[0];
-    o[1] = g * gwx;
-    o[2] = g * gwy;
-    o[3] = g * gwz;
-    o[4] = g * gvx;
-    o[5] = g * gvy;
-    o[6] = g * gvz;
-    const unsigned long long db = R.disp_bits[m];
-    o[7] = sqrt(__longlong_as_double((long long)db));
-    R.disp_bits[m] = 0ull;
   }
-  if (blockIdx.x == 0 && threadIdx.x < 2 * n_ctl) next_chunk[threadIdx.x] = 0u;
 }
 
 __global__ void k_displacement(const double* zx, const double* zy, const double* zz, int n,
@@ -1099,6 +1152,8 @@ void build_pairs_batched(const BuildReq* h, const BuildReq* d, int n, cudaStream
   count_launch(launches + 5);
 }
 
+size_t sweep_ctl_bytes(int n) { return sizeof(SweepCtl) * (2 * ((n + kMaxSweepReqs - 1) / kMaxSweepReqs) + 2); }
+
 void sweep_batched(const SweepReq* h, const SweepReq* d, int n, int sm_count, unsigned* d_ctl, cudaStream_t st,
                    cudaEvent_t ev0, cudaEvent_t ev1) {
   if (n == 0) return;
@@ -1116,10 +1171,8 @@ void sweep_batched(const SweepReq* h, const SweepReq* d, int n, int sm_count, un
   // requests arrive grouped: gradient requests first, then F-only ones; one
   // persistent launch per group (<= kMaxSweepReqs requests each), then one
   // reduction over all requests
-  int n_grad = 0, max_nz = 1;
+  int n_grad = 0;
   while (n_grad < n && h[n_grad].grad) ++n_grad;
-  for (int r = 0; r < n; ++r) max_nz = max(max_nz, h[r].n_z);
-  k_displacement_batched<<<dim3((max_nz + 255) / 256, n), 256, 0, st>>>(d);
   const int grid = 2 * sm_count;
   int launches = 0;
   for (int grp = 0; grp < 2; ++grp) {
@@ -1129,7 +1182,7 @@ void sweep_batched(const SweepReq* h, const SweepReq* d, int n, int sm_count, un
       int max_m = 1;
       for (int r = r0; r < r1; ++r) max_m = max(max_m, h[r].M);
       const SweepReq* dr = d + r0;
-      unsigned* ctl = d_ctl + 2 * (r0 / kMaxSweepReqs) + grp;
+      SweepCtl* ctl = reinterpret_cast<SweepCtl*>(d_ctl) + launches;
       if (grp == 0) {
         if (max_m <= 2) k_sweep<1, true><<<grid, kSweepThreads, kSweepSmem, st>>>(dr, r1 - r0, ctl);
         else if (max_m <= 4) k_sweep<2, true><<<grid, kSweepThreads, kSweepSmem, st>>>(dr, r1 - r0, ctl);
@@ -1142,8 +1195,7 @@ void sweep_batched(const SweepReq* h, const SweepReq* d, int n, int sm_count, un
       ++launches;
     }
   }
-  k_sweep_reduce<<<n, kSweepThreads, 0, st>>>(d, d_ctl, (n + kMaxSweepReqs - 1) / kMaxSweepReqs);
-  count_launch(launches + 2);
+  count_launch(launches);
   if (ev1) cudaEventRecord(ev1, st);
 }
 

@@ -474,49 +474,72 @@ void register_many(kreg_ctx* ctx, std::vector<RegJob>& jobs) {
     regs.push_back(std::move(r));
   }
 
-  std::vector<BuildJob> builds;
-  std::vector<EvalJob> evals;
-  std::vector<Reg*> owners;
   using clk = std::chrono::steady_clock;
   // At most `window` registrations are in flight; a finished one is replaced
   // by the next job at once (dynamic refill), so one slow registration does
-  // not hold the batch. Results do not depend on the window: every sweep
-  // request is evaluated independently of what else shares its launch.
+  // not hold the batch. The active registrations form two groups whose
+  // rounds alternate on the device: while one group's round runs, the host
+  // consumes and plans the other's (the stream orders the rounds). Results
+  // do not depend on the window or the grouping: every sweep request is
+  // evaluated independently of what else shares its launch.
   const size_t window = ctx && ctx->max_active > 0 ? static_cast<size_t>(ctx->max_active) : regs.size();
+  const int n_groups = ctx && window >= 2 && env_int("KREG_GROUPS", 1) >= 2 ? 2 : 1;
   size_t started = 0;
-  std::vector<Reg*> active;
-  for (;;) {
+  struct Group {
+    std::vector<Reg*> active;
+    std::vector<Reg*> owners;
+    RoundSlot* slot = nullptr;
+    bool pending = false;  // a round of this group is in flight
+  };
+  Group groups[2];
+  for (int g = 0; g < n_groups; ++g) groups[g].slot = round_slot(ctx, g);
+  const size_t per_group = (window + n_groups - 1) / n_groups;
+
+  // consume the finished round of group g, refill, plan and launch its next
+  auto step = [&](Group& G) -> bool {
     const auto t0 = clk::now();
-    active.erase(std::remove_if(active.begin(), active.end(), [](Reg* r) { return r->phase == Phase::kDone; }),
-                 active.end());
-    while (active.size() < window && started < regs.size()) {
-      Reg* r = regs[started++].get();
-      r->pairs.ctx = ctx;
-      r->pairs.p = acquire_workspace(ctx);
-      if (r->job->expected_pairs > 0) r->pairs->expected_pairs = r->job->expected_pairs;
-      active.push_back(r);
+    if (G.pending) {
+      end_round(ctx, *G.slot);
+      G.pending = false;
+      const auto t1 = clk::now();
+      Reg* last = nullptr;
+      for (Reg* r : G.owners) {  // each registration consumes once per round
+        if (r == last) continue;
+        last = r;
+        consume(*r);
+      }
+      if (ctx) ctx->t_total += std::chrono::duration<double>(clk::now() - t1).count();
     }
-    builds.clear();
-    evals.clear();
-    owners.clear();
-    for (Reg* r : active) plan(*r, builds, evals, owners, k_first, fail_grad);
-    if (builds.empty() && evals.empty()) {
-      if (started >= regs.size()) break;
-      continue;  // all active registrations finished this round: refill
-    }
-    const auto t1 = clk::now();
-    run_round(ctx, builds, evals);
     const auto t2 = clk::now();
-    // each registration consumes once per round
-    Reg* last = nullptr;
-    for (Reg* r : owners) {
-      if (r == last) continue;
-      last = r;
-      consume(*r);
+    for (;;) {
+      G.active.erase(std::remove_if(G.active.begin(), G.active.end(), [](Reg* r) { return r->phase == Phase::kDone; }),
+                     G.active.end());
+      while (G.active.size() < per_group && started < regs.size()) {
+        Reg* r = regs[started++].get();
+        r->pairs.ctx = ctx;
+        r->pairs.p = acquire_workspace(ctx);
+        if (r->job->expected_pairs > 0) r->pairs->expected_pairs = r->job->expected_pairs;
+        G.active.push_back(r);
+      }
+      std::vector<BuildJob> builds;
+      std::vector<EvalJob> evals;
+      G.owners.clear();
+      for (Reg* r : G.active) plan(*r, builds, evals, G.owners, k_first, fail_grad);
+      if (!builds.empty() || !evals.empty()) {
+        if (ctx) ctx->t_total += std::chrono::duration<double>(clk::now() - t2).count();
+        begin_round(ctx, *G.slot, std::move(builds), std::move(evals));
+        G.pending = true;
+        (void)t0;
+        return true;
+      }
+      if (started >= regs.size()) return false;  // group drained
+      // every active registration finished without device work: refill
     }
-    if (ctx)
-      ctx->t_total += std::chrono::duration<double>(t1 - t0).count() +
-                      std::chrono::duration<double>(clk::now() - t2).count();
+  };
+  bool live[2] = {true, n_groups > 1};
+  while (live[0] || live[1]) {
+    for (int g = 0; g < n_groups; ++g)
+      if (live[g]) live[g] = step(groups[g]);
   }
 }
 

@@ -21,6 +21,7 @@ for skin in skins:
     ctx.set_candidate_skin(skin)
     api.register_batch(dX, dZ, inits, p, cfg, ctx=ctx)
     ctx.reset_stats()
+    h0 = ctx.host_stats()
     ctx.set_profiling(True)
     ctx.synchronize()
     t0 = time.perf_counter()
@@ -35,5 +36,6 @@ for skin in skins:
                       "t_wait": round(h["t_wait_s"], 4), "t_solver": round(h["t_solver_s"], 4),
                       "t_build_prep": round(h["t_build_prep_s"], 4), "t_sweep_prep": round(h["t_sweep_prep_s"], 4),
                       "sweep_ms": round(s["sweep_ms"], 1), "pairs_streamed": s["pairs_streamed"],
-                      "slots_streamed": s["slots_streamed"], "pair_evals": s["pair_evals"], "builds": b, "allocs": h["device_allocs"],
+                      "slots_streamed": s["slots_streamed"], "pair_evals": s["pair_evals"], "builds": b, "allocs": h["device_allocs"] - h0["device_allocs"],
+                      "alloc_s": round(h["device_alloc_s"] - h0["device_alloc_s"], 4),
                       "launches": ctx.kernel_launches()}), flush=True)

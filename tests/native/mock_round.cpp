@@ -66,6 +66,21 @@ void run_round(kreg_ctx*, std::vector<BuildJob>& builds, std::vector<EvalJob>& e
     }
   }
 }
+
+// the oracle evaluates synchronously: begin_round does the work, end_round
+// has nothing to wait for
+RoundSlot::~RoundSlot() {}
+RoundSlot* round_slot(kreg_ctx*, int i) {
+  static RoundSlot slots[3];
+  return &slots[i];
+}
+void begin_round(kreg_ctx* ctx, RoundSlot& S, std::vector<BuildJob>&& builds, std::vector<EvalJob>&& evals) {
+  S.builds = std::move(builds);
+  S.evals = std::move(evals);
+  run_round(ctx, S.builds, S.evals);
+  S.in_flight = true;
+}
+void end_round(kreg_ctx*, RoundSlot& S) { S.in_flight = false; }
 }  // namespace kreg_host
 
 // registers once through the product solver with the oracle standing in for the device
