@@ -82,6 +82,7 @@ struct alignas(16) ChunkRec {
 // inequality); the kernel checks that bound and flags the build otherwise.
 struct BuildReq {
   const double* xx; const double* xy; const double* xz; const float* xfeat; int n_x;
+  const double4* xw;     // X positions as {x, y, z, 0} (filter gathers)
   const double* zx; const double* zy; const double* zz; const float* zfeat; int n_z;
   double T[12];          // build transform, row-major 3x4
   int full;              // run the candidate stage first
@@ -160,6 +161,8 @@ void sweep_batched(const SweepReq* h_reqs, const SweepReq* d_reqs, int n, int sm
                    cudaStream_t stream, cudaEvent_t sweep_begin, cudaEvent_t sweep_end);
 void displacement(const double* zx, const double* zy, const double* zz, int n, const double* d_T2,
                   unsigned long long* d_out, cudaStream_t stream);
+
+void interleave_positions(const double* x, const double* y, const double* z, int n, double4* out, cudaStream_t stream);
 
 long long kernel_launch_count();
 

@@ -262,6 +262,7 @@ void cloud_upload(kreg_ctx* ctx, kreg_cloud* c, const double* sx, const double* 
     c->z.ensure(n, false, 1.0);
     c->feat.ensure(cloud_stage_floats(c), false, 1.0);
   }
+  c->xw.ensure(static_cast<size_t>(n) + 1, false, 1.0);
   if (n) {
     KREG_CUDA(cudaMemcpyAsync(c->x.ptr, sx, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
     KREG_CUDA(cudaMemcpyAsync(c->y.ptr, sy, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
@@ -269,6 +270,7 @@ void cloud_upload(kreg_ctx* ctx, kreg_cloud* c, const double* sx, const double* 
     if (c->fstride)
       KREG_CUDA(cudaMemcpyAsync(c->feat.ptr, sf, sizeof(float) * static_cast<size_t>(n) * c->fstride,
                                 cudaMemcpyHostToDevice, ctx->stream));
+    kreg_dev::interleave_positions(c->x.ptr, c->y.ptr, c->z.ptr, n, c->xw.ptr, ctx->stream);
   }
 }
 
@@ -378,6 +380,7 @@ static void prepare_build(kreg_ctx* ctx, BuildJob& job, kreg_dev::BuildReq& R) {
   std::memcpy(p->T_build, job.T, sizeof(p->T_build));
 
   R.xx = X->x.ptr; R.xy = X->y.ptr; R.xz = X->z.ptr; R.xfeat = X->feat.ptr; R.n_x = X->n;
+  R.xw = X->xw.ptr;
   R.zx = Z->x.ptr; R.zy = Z->y.ptr; R.zz = Z->z.ptr; R.zfeat = Z->feat.ptr; R.n_z = Z->n;
   std::memcpy(R.T, job.T, sizeof(R.T));
   R.cutoff_sq = cutoff * cutoff;  // inner_product.cpp:59
@@ -584,8 +587,8 @@ void begin_round(kreg_ctx* ctx, RoundSlot& S, std::vector<BuildJob>&& builds_in,
   }
   const auto tb = clk::now();
   ctx->t_build_prep += std::chrono::duration<double>(tb - t0).count();
-  // gradient requests first, F-only requests after (one launch per group)
-  std::stable_partition(evals.begin(), evals.end(), [](const EvalJob& e) { return e.grad; });
+  // F-only requests first (their chunks are the heaviest; see sweep_batched)
+  std::stable_partition(evals.begin(), evals.end(), [](const EvalJob& e) { return !e.grad; });
   std::vector<SweepScratch> scratch(static_cast<size_t>(ne));
   size_t part_total = 0;
   for (int e = 0; e < ne; ++e) {

@@ -160,6 +160,7 @@ struct kreg_cloud {
   double diam = 0.0;
   double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
   kreg_host::DevBuf<double> x, y, z;  // sorted order
+  kreg_host::DevBuf<double4> xw;      // sorted order, {x, y, z, 0}
   kreg_host::DevBuf<float> feat;      // sorted order, stride fstride
   std::vector<int> order;              // sorted rank -> original index
   std::vector<int> rank;               // original index -> sorted rank

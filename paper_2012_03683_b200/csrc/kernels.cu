@@ -518,9 +518,10 @@ __global__ void __launch_bounds__(256) k_filter(const BuildReq* reqs) {
     double x = 0, y = 0, z = 0;
     if (k < ds) {
       e = row[k];
-      x = R.xx[e.x];
-      y = R.xy[e.x];
-      z = R.xz[e.x];
+      const double4 xp = R.xw[e.x];  // one 32-B sector per candidate
+      x = xp.x;
+      y = xp.y;
+      z = xp.z;
       const double dx = x - qx, dy = y - qy, dz = z - qz;
       keep = dx * dx + dy * dy + dz * dz <= c2;
     }
@@ -701,22 +702,25 @@ struct SweepCtl {
 // warp completing its last item adds the group partials in a fixed order and
 // writes F, the gradient (inner_product.cpp:121-157, assembled in FP64) and
 // the displacement; resets the request's counters and displacement bits.
-template <bool GRAD>
-__device__ __noinline__ void item_done(const SweepReq& R, SweepCtl* ctl, int r, int n_items, int MV, int lane) {
+__device__ __noinline__ void item_done(const SweepReq& R, SweepCtl* ctl, int r, int n_items, int lane) {
   unsigned old = 0;
   if (lane == 0) old = atomicAdd(&ctl->req_done[r], 1u);
   old = __shfl_sync(0xffffffffu, old, 0);
   if ((int)old != n_items - 1) return;
   __threadfence();
+  const int M = R.M, NV = R.grad ? 7 : 1, MV = M * NV;
   const int C = chunk_count(request_units(R));
   const int NG = (C + kChunkGroup - 1) / kChunkGroup;
   const double* gpart = R.partials + (size_t)kMaxChunks * MV;
-  double v0 = 0.0, v1 = 0.0;  // values lane and lane + 32
-  for (int g = 0; g < NG; ++g) {
-    if (lane < MV) v0 += __ldcg(gpart + (size_t)g * MV + lane);
-    if (lane + 32 < MV) v1 += __ldcg(gpart + (size_t)g * MV + lane + 32);
+  double v0 = 0.0, v1 = 0.0;  // values lane and lane + 32 (loads batched, adds in order)
+  if (lane < MV) {
+#pragma unroll 8
+    for (int g = 0; g < NG; ++g) v0 += __ldcg(gpart + (size_t)g * MV + lane);
   }
-  const int M = R.M, NV = GRAD ? 7 : 1;
+  if (lane + 32 < MV) {
+#pragma unroll 8
+    for (int g = 0; g < NG; ++g) v1 += __ldcg(gpart + (size_t)g * MV + lane + 32);
+  }
   double t[7];
 #pragma unroll
   for (int k = 0; k < 7; ++k) {
@@ -754,29 +758,330 @@ struct WarpQueue {
   int head, tail;
   int done;
   int pr, pc;        // request / chunk being prefetched
-  long long pu, pend;
+  int pu, pend;      // units
   unsigned issued;   // stages issued so far
   unsigned recs;     // chunk records issued so far
   int first;         // next stage is the first of chunk pc
 };
 
+// Everything a sweep warp needs across work items.
+struct SweepWarp {
+  const SweepReq* reqs;
+  SweepCtl* ctl;
+  const int* cbase;  // item prefix over the launch's requests (shared)
+  const int* units;  // sweep units of each request (shared)
+  int n_req;
+  int total;         // items of the launch
+  int4* ring;
+  ChunkRec* recs;
+  unsigned long long* bars;
+  WarpQueue* Q;
+  float* tc;         // transform coefficients of the current chunk (shared)
+  int lane;
+  unsigned consumed, rec_used;
+};
+
+__device__ __forceinline__ int disp_items(const SweepReq& R) { return (R.n_z + kDispItem - 1) / kDispItem; }
+
+__device__ __forceinline__ int locate_item(const SweepWarp& w, int g) {
+  int lo = 0, hi = w.n_req - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (w.cbase[mid] <= g) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+// lane 0: issue the next stage (grabbing items as needed); false if none
+__device__ __forceinline__ bool produce(SweepWarp& w) {
+  WarpQueue& Q = *w.Q;
+  while (Q.pu >= Q.pend) {
+    if (Q.done || Q.tail - Q.head >= kQueueDepth) return false;
+    const int g = (int)atomicAdd(&w.ctl->next_item, 1u);
+    if (g >= w.total) {
+      Q.done = 1;
+      return false;
+    }
+    const int r = locate_item(w, g);
+    Q.ids[Q.tail % kQueueDepth] = g;
+    ++Q.tail;
+    const int i = g - w.cbase[r] - disp_items(w.reqs[r]);
+    if (i < 0) continue;  // displacement item: no stages
+    const long long U = w.units[r], cu = chunk_units(U);
+    Q.pr = r;
+    Q.pc = i;
+    Q.pu = (int)(Q.pc * cu);
+    Q.pend = (int)min(U, Q.pu + cu);
+    Q.first = 1;
+  }
+  const int nu = min(kStageUnits, Q.pend - Q.pu);
+  const int s = Q.issued % kSweepStages;
+  const SweepReq& P = w.reqs[Q.pr];
+  fence_proxy_async();
+  mbar_expect_tx(&w.bars[s], nu * kUnitBytes + (Q.first ? (unsigned)sizeof(ChunkRec) : 0u));
+  tma_load_1d(w.ring + s * kStageSlots, P.slots + (long long)Q.pu * kUnitSlots, nu * kUnitBytes, &w.bars[s]);
+  if (Q.first) {
+    tma_load_1d(w.recs + Q.recs % kRecSlots, P.chunks + Q.pc, sizeof(ChunkRec), &w.bars[s]);
+    ++Q.recs;
+    Q.first = 0;
+  }
+  Q.pu += nu;
+  ++Q.issued;
+  return true;
+}
+
+// Displacement slice of request r: max_j |T_m z_j - T_b z_j| in FP64 over the
+// original coordinates (order-free max).
+__device__ __noinline__ void displacement_item(SweepWarp& w, const SweepReq& R, int r, int item, int n_items) {
+  const int lane = w.lane, M = R.M;
+  const int j0 = item * kDispItem, j1 = min(R.n_z, j0 + kDispItem);
+  unsigned long long dmax[kMaxCandidates];
+#pragma unroll
+  for (int m = 0; m < kMaxCandidates; ++m) dmax[m] = 0ull;
+  for (int j = j0 + lane; j < j1; j += 32) {
+    const double zx = R.zx[j], zy = R.zy[j], zz = R.zz[j];
+    double bx, by, bz;
+    apply_T(R.Tb, zx, zy, zz, bx, by, bz);
+#pragma unroll
+    for (int m = 0; m < kMaxCandidates; ++m) {
+      if (m < M) {
+        double x, y, z;
+        apply_T(R.T[m], zx, zy, zz, x, y, z);
+        const double dx = x - bx, dy = y - by, dz = z - bz;
+        const unsigned long long d2 = (unsigned long long)__double_as_longlong(dx * dx + dy * dy + dz * dz);
+        dmax[m] = d2 > dmax[m] ? d2 : dmax[m];
+      }
+    }
+  }
+#pragma unroll
+  for (int m = 0; m < kMaxCandidates; ++m) {
+    if (m < M) {
+      unsigned long long d = dmax[m];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long other = __shfl_xor_sync(0xffffffffu, d, o);
+        d = other > d ? other : d;
+      }
+      if (lane == 0 && d) atomicMax(&R.disp_bits[m], d);
+    }
+  }
+  item_done(R, w.ctl, r, n_items, lane);
+}
+
+// One chunk (units [u0, u1) of request r) for M <= 2 NP candidates: stream the
+// stages, accumulate per tile, write the chunk partial, then the group /
+// request completion steps.
 template <int NP, bool GRAD>
-__global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(const SweepReq* reqs, int n_req, SweepCtl* ctl) {
+__device__ __forceinline__ void chunk_body(SweepWarp& w, const SweepReq& R, int r, int c, int C, int n_items) {
   constexpr int MAXM = 2 * NP;
+  const int lane = w.lane;
+  const int M = R.M;
+  const int MV = M * (GRAD ? 7 : 1);
+  const long long U = w.units[r], cu = chunk_units(U);
+  const long long u0 = (long long)c * cu, u1 = min(U, u0 + cu);
+  const f2_t kap2 = pk2(R.kappa, R.kappa);
+  // this chunk's transform coefficients in shared memory (read at every tile
+  // start); 96 floats hold Td for 8 candidates or Td + Ta for 4
+  constexpr bool kStage = !GRAD || NP <= 2;
+  float* tc = w.tc;
+  if (kStage) {
+    __syncwarp();
+    for (int i = lane; i < M * 12; i += 32) {
+      tc[i] = (&R.Td[0][0])[i];
+      if (GRAD) tc[48 + i] = (&R.Ta[0][0])[i];
+    }
+    __syncwarp();
+  }
+
+  f2_t acc[NP][7];
+  f2_t ndx[NP], ndy[NP], ndz[NP];  // -delta per candidate pair
+  float ax[MAXM], ay[MAXM], az[MAXM];  // torque arm T_m z_j - anchor
+  f2_t W[NP], Sx[NP], Sy[NP], Sz[NP];
+#pragma unroll
+  for (int p = 0; p < NP; ++p)
+#pragma unroll
+    for (int v = 0; v < 7; ++v) acc[p][v] = 0ull;
+#pragma unroll
+  for (int p = 0; p < NP; ++p) W[p] = Sx[p] = Sy[p] = Sz[p] = 0ull;
+
+  auto start_tile = [&](float zx, float zy, float zz) {
+#pragma unroll
+    for (int m = 0; m < MAXM; m += 2) {
+      const float* A = kStage ? tc + 12 * (m < M ? m : 0) : R.Td[m < M ? m : 0];
+      const float* B = kStage ? tc + 12 * (m + 1 < M ? m + 1 : 0) : R.Td[m + 1 < M ? m + 1 : 0];
+      ndx[m / 2] = pk2(-fmaf(A[0], zx, fmaf(A[1], zy, fmaf(A[2], zz, A[3]))),
+                       -fmaf(B[0], zx, fmaf(B[1], zy, fmaf(B[2], zz, B[3]))));
+      ndy[m / 2] = pk2(-fmaf(A[4], zx, fmaf(A[5], zy, fmaf(A[6], zz, A[7]))),
+                       -fmaf(B[4], zx, fmaf(B[5], zy, fmaf(B[6], zz, B[7]))));
+      ndz[m / 2] = pk2(-fmaf(A[8], zx, fmaf(A[9], zy, fmaf(A[10], zz, A[11]))),
+                       -fmaf(B[8], zx, fmaf(B[9], zy, fmaf(B[10], zz, B[11]))));
+    }
+    if (GRAD) {
+#pragma unroll
+      for (int m = 0; m < MAXM; ++m) {
+        const float* A = kStage ? tc + 48 + 12 * (m < M ? m : 0) : R.Ta[m < M ? m : 0];
+        ax[m] = fmaf(A[0], zx, fmaf(A[1], zy, fmaf(A[2], zz, A[3])));
+        ay[m] = fmaf(A[4], zx, fmaf(A[5], zy, fmaf(A[6], zz, A[7])));
+        az[m] = fmaf(A[8], zx, fmaf(A[9], zy, fmaf(A[10], zz, A[11])));
+      }
+    }
+  };
+  bool active = false;
+  auto flush_tile = [&]() {
+    if (active) {
+#pragma unroll
+      for (int p = 0; p < NP; ++p) {
+        acc[p][0] = add2(acc[p][0], W[p]);
+        if (GRAD) {
+          const f2_t fqx = pk2(ax[2 * p], ax[2 * p + 1]);
+          const f2_t fqy = pk2(ay[2 * p], ay[2 * p + 1]);
+          const f2_t fqz = pk2(az[2 * p], az[2 * p + 1]);
+          const f2_t neg = pk2(-1.0f, -1.0f);
+          acc[p][1] = add2(acc[p][1], Sx[p]);
+          acc[p][2] = add2(acc[p][2], Sy[p]);
+          acc[p][3] = add2(acc[p][3], Sz[p]);
+          acc[p][4] = add2(acc[p][4], fma2(mul2(neg, fqz), Sy[p], mul2(fqy, Sz[p])));
+          acc[p][5] = add2(acc[p][5], fma2(mul2(neg, fqx), Sz[p], mul2(fqz, Sx[p])));
+          acc[p][6] = add2(acc[p][6], fma2(mul2(neg, fqy), Sx[p], mul2(fqx, Sy[p])));
+        }
+      }
+    }
+#pragma unroll
+    for (int p = 0; p < NP; ++p) W[p] = Sx[p] = Sy[p] = Sz[p] = 0ull;
+  };
+
+  if (u1 > u0) {
+    // the first stage carries the chunk record
+    const int s0 = w.consumed % kSweepStages;
+    mbar_wait(&w.bars[s0], (w.consumed / kSweepStages) & 1);
+    const ChunkRec& rec = w.recs[w.rec_used % kRecSlots];
+    ++w.rec_used;
+    int t = rec.t0;
+    long long t_end = rec.t0_end;
+    active = 32 * t + lane < R.n_z;
+    start_tile(rec.x[lane], rec.y[lane], rec.z[lane]);
+    // prefetch of the next tile (speculatively t + 1)
+    auto prefetch = [&](int tn, float4& pz, long long& pend) {
+      pz = make_float4(0.f, 0.f, 0.f, 0.f);
+      pend = U;
+      if (tn < R.n_tiles) {
+        if (32 * tn + lane < R.n_z) pz = R.zs[32 * tn + lane];
+        pend = R.unit_off[tn + 1];
+      }
+    };
+    float4 pz;
+    long long p_end;
+    prefetch(t + 1, pz, p_end);
+
+    for (long long u = u0; u < u1; u += kStageUnits) {
+      const int nu = (int)min((long long)kStageUnits, u1 - u);
+      const int s = w.consumed % kSweepStages;
+      if (u != u0) mbar_wait(&w.bars[s], (w.consumed / kSweepStages) & 1);
+      const int4* stage = w.ring + s * kStageSlots + lane;
+      if (u + nu <= t_end) {  // whole stage inside the current tile
+        if (active) sweep_steps<NP, GRAD>(stage, nu * kUnitSteps, ndx, ndy, ndz, kap2, W, Sx, Sy, Sz);
+      } else {
+        long long v = u;
+        while (v < u + nu) {
+          while (v >= t_end) {  // next tile with units
+            flush_tile();
+            ++t;
+            if (p_end > v) {
+              t_end = p_end;
+              active = 32 * t + lane < R.n_z;
+              start_tile(pz.x, pz.y, pz.z);
+            } else {  // tile t had no units (window end): load directly
+              long long e = R.unit_off[t + 1];
+              while (e <= v) e = R.unit_off[++t + 1];
+              t_end = e;
+              const float4 z = 32 * t + lane < R.n_z ? R.zs[32 * t + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+              active = 32 * t + lane < R.n_z;
+              start_tile(z.x, z.y, z.z);
+            }
+            prefetch(t + 1, pz, p_end);
+          }
+          const long long w_end = min(u + nu, t_end);
+          if (active)
+            sweep_steps<NP, GRAD>(stage + (v - u) * kUnitSlots, (int)(w_end - v) * kUnitSteps, ndx, ndy, ndz, kap2, W,
+                                  Sx, Sy, Sz);
+          v = w_end;
+        }
+      }
+      __syncwarp();
+      ++w.consumed;
+      if (lane == 0) produce(w);  // refill the stage just consumed
+      __syncwarp();
+    }
+    flush_tile();
+  }
+
+  // chunk partial: FP32 warp sums (fixed butterfly order) widened to FP64;
+  // lane v stores value v
+  double* part = R.partials + (size_t)c * MV;
+#pragma unroll
+  for (int p = 0; p < NP; ++p) {
+#pragma unroll
+    for (int v = 0; v < (GRAD ? 7 : 1); ++v) {
+      float a0, a1;
+      upk2(warp_sum_f2(acc[p][v]), a0, a1);
+      const int i0 = (2 * p) * (GRAD ? 7 : 1) + v, i1 = (2 * p + 1) * (GRAD ? 7 : 1) + v;
+      if (2 * p < M && lane == (i0 & 31)) part[i0] = (double)a0;
+      if (2 * p + 1 < M && lane == (i1 & 31)) part[i1] = (double)a1;
+    }
+  }
+  // chunk group done? its last chunk sums the group's partials in order
+  __threadfence();
+  __syncwarp();
+  const int grp = c / kChunkGroup;
+  unsigned old = 0;
+  if (lane == 0) old = atomicAdd(&w.ctl->grp_done[r][grp], 1u);
+  old = __shfl_sync(0xffffffffu, old, 0);
+  const int gsize = min(kChunkGroup, C - grp * kChunkGroup);
+  if ((int)old == gsize - 1) {
+    __threadfence();
+    double* gpart = R.partials + (size_t)kMaxChunks * MV + (size_t)grp * MV;
+    for (int v = lane; v < MV; v += 32) {
+      double t = 0.0;
+      const double* src = R.partials + (size_t)grp * kChunkGroup * MV + v;
+#pragma unroll 8
+      for (int k = 0; k < gsize; ++k) t += __ldcg(src + (size_t)k * MV);  // loads batched, adds in order
+      gpart[v] = t;
+    }
+    if (lane == 0) w.ctl->grp_done[r][grp] = 0u;
+    __threadfence();
+    __syncwarp();
+    item_done(R, w.ctl, r, n_items, lane);
+  }
+}
+
+// Persistent sweep over the work items (displacement slices + chunks) of up
+// to kMaxSweepReqs requests; gradient requests with M <= 2 NPG candidates,
+// F-only requests (line-search failure path) with M <= 8.
+template <int NPG>
+__global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(const SweepReq* reqs, int n_req, SweepCtl* ctl) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  unsigned* next_chunk = &ctl->next_item;
   __shared__ int cbase[kMaxSweepReqs + 1];
   __shared__ int units_s[kMaxSweepReqs];
-  __shared__ int disp_s[kMaxSweepReqs];  // displacement items of each request
+  __shared__ float tco[kSweepWarps][96];  // per warp: Td (and Ta) of its current chunk
   __shared__ WarpQueue wq[kSweepWarps];
   extern __shared__ __align__(128) unsigned char dyn_smem[];
-  int4* ring = reinterpret_cast<int4*>(dyn_smem) + (size_t)wid * kSweepStages * kStageSlots;
-  ChunkRec* recs = reinterpret_cast<ChunkRec*>(dyn_smem + (size_t)kSweepWarps * kSweepStages * kStageSlots * sizeof(int4)) +
-                   wid * kRecSlots;
-  unsigned long long* bars =
-      reinterpret_cast<unsigned long long*>(dyn_smem + (size_t)kSweepWarps * kSweepStages * kStageSlots * sizeof(int4) +
-                                            (size_t)kSweepWarps * kRecSlots * sizeof(ChunkRec)) +
-      wid * kSweepStages;
+  SweepWarp w;
+  w.reqs = reqs;
+  w.ctl = ctl;
+  w.cbase = cbase;
+  w.units = units_s;
+  w.n_req = n_req;
+  w.ring = reinterpret_cast<int4*>(dyn_smem) + (size_t)wid * kSweepStages * kStageSlots;
+  w.recs = reinterpret_cast<ChunkRec*>(dyn_smem + (size_t)kSweepWarps * kSweepStages * kStageSlots * sizeof(int4)) +
+           wid * kRecSlots;
+  w.bars = reinterpret_cast<unsigned long long*>(dyn_smem + (size_t)kSweepWarps * kSweepStages * kStageSlots * sizeof(int4) +
+                                                 (size_t)kSweepWarps * kRecSlots * sizeof(ChunkRec)) +
+           wid * kSweepStages;
+  w.Q = &wq[wid];
+  w.tc = tco[wid];
+  w.lane = lane;
+  w.consumed = w.rec_used = 0;
 
   // work items of request r: disp_s[r] displacement slices, then its chunks;
   // item prefix over the launch's requests (every CTA computes it)
@@ -785,17 +1090,15 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(const SweepReq* reqs
     if (threadIdx.x < n_req) {
       const SweepReq& Rq = reqs[threadIdx.x];
       const long long U = request_units(Rq);
-      const int D = (Rq.n_z + kDispItem - 1) / kDispItem;
-      C = chunk_count(U) + D;
+      C = chunk_count(U) + disp_items(Rq);
       units_s[threadIdx.x] = (int)U;
-      disp_s[threadIdx.x] = D;
     }
     int tot;
     const int ex = block_excl_scan<int>(C, &tot);
     if (threadIdx.x < n_req) cbase[threadIdx.x] = ex;
     if (threadIdx.x == 0) cbase[n_req] = tot;
   }
-  if (lane < kSweepStages) mbar_init(&bars[lane], 1);
+  if (lane < kSweepStages) mbar_init(&w.bars[lane], 1);
   if (lane == 0) {
     WarpQueue& q = wq[wid];
     q.head = q.tail = 0;
@@ -807,279 +1110,32 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(const SweepReq* reqs
   }
   mbar_fence_init();
   __syncthreads();
-  const int total = cbase[n_req];
-  WarpQueue& Q = wq[wid];
-
-  // locate chunk g: request r with cbase[r] <= g < cbase[r + 1]
-  auto locate = [&](int g) {
-    int lo = 0, hi = n_req - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (cbase[mid] <= g) lo = mid;
-      else hi = mid - 1;
-    }
-    return lo;
-  };
-  // lane 0: issue the next stage (grabbing chunks as needed); false if none
-  auto produce = [&]() -> bool {
-    while (Q.pu >= Q.pend) {
-      if (Q.done || Q.tail - Q.head >= kQueueDepth) return false;
-      const int g = (int)atomicAdd(next_chunk, 1u);
-      if (g >= total) {
-        Q.done = 1;
-        return false;
-      }
-      const int r = locate(g);
-      Q.ids[Q.tail % kQueueDepth] = g;
-      ++Q.tail;
-      const int i = g - cbase[r] - disp_s[r];
-      if (i < 0) continue;  // displacement item: no stages
-      const long long U = units_s[r], cu = chunk_units(U);
-      Q.pr = r;
-      Q.pc = i;
-      Q.pu = (long long)Q.pc * cu;
-      Q.pend = min(U, Q.pu + cu);
-      Q.first = 1;
-    }
-    const int nu = (int)min((long long)kStageUnits, Q.pend - Q.pu);
-    const int s = Q.issued % kSweepStages;
-    const SweepReq& P = reqs[Q.pr];
-    fence_proxy_async();
-    mbar_expect_tx(&bars[s], nu * kUnitBytes + (Q.first ? (unsigned)sizeof(ChunkRec) : 0u));
-    tma_load_1d(ring + s * kStageSlots, P.slots + Q.pu * kUnitSlots, nu * kUnitBytes, &bars[s]);
-    if (Q.first) {
-      tma_load_1d(recs + Q.recs % kRecSlots, P.chunks + Q.pc, sizeof(ChunkRec), &bars[s]);
-      ++Q.recs;
-      Q.first = 0;
-    }
-    Q.pu += nu;
-    ++Q.issued;
-    return true;
-  };
+  w.total = cbase[n_req];
   if (lane == 0)
     for (int s = 0; s < kSweepStages; ++s)
-      if (!produce()) break;
+      if (!produce(w)) break;
   __syncwarp();
 
-  unsigned consumed = 0, rec_used = 0;
-  f2_t acc[NP][7];
-  f2_t ndx[NP], ndy[NP], ndz[NP];  // -delta per candidate pair
-  float ax[MAXM], ay[MAXM], az[MAXM];  // torque arm T_m z_j - anchor
-  f2_t W[NP], Sx[NP], Sy[NP], Sz[NP];
   for (;;) {
-    // next chunk of this warp (produced in order by lane 0)
+    // next item of this warp (queued in order by lane 0)
     int g = -1;
     if (lane == 0) {
-      if (Q.head == Q.tail) produce();  // grabs the next chunk (zero-unit chunks issue no stage)
-      if (Q.head != Q.tail) g = Q.ids[Q.head % kQueueDepth];
+      if (w.Q->head == w.Q->tail) produce(w);  // grabs the next item (items without stages issue none)
+      if (w.Q->head != w.Q->tail) g = w.Q->ids[w.Q->head % kQueueDepth];
     }
     g = __shfl_sync(0xffffffffu, g, 0);
     if (g < 0) break;
-    const int r = locate(g);
+    const int r = locate_item(w, g);
     const SweepReq& R = reqs[r];
-    const int M = R.M;
-    const int MV = M * (GRAD ? 7 : 1);
-    const long long U = units_s[r], cu = chunk_units(U);
-    const int D = disp_s[r];
+    const int D = disp_items(R);
     const int C = cbase[r + 1] - cbase[r] - D;
-    const int NG = (C + kChunkGroup - 1) / kChunkGroup;
+    const int n_items = (C + kChunkGroup - 1) / kChunkGroup + D;
     const int c = g - cbase[r] - D;
-    if (c < 0) {
-      // displacement slice (FP64 over the original coordinates, order-free max)
-      const int j0 = (c + D) * kDispItem, j1 = min(R.n_z, j0 + kDispItem);
-      unsigned long long dmax[MAXM];
-#pragma unroll
-      for (int m = 0; m < MAXM; ++m) dmax[m] = 0ull;
-#pragma unroll 4
-      for (int j = j0 + lane; j < j1; j += 32) {
-        const double zx = R.zx[j], zy = R.zy[j], zz = R.zz[j];
-        double bx, by, bz;
-        apply_T(R.Tb, zx, zy, zz, bx, by, bz);
-#pragma unroll
-        for (int m = 0; m < MAXM; ++m) {
-          if (m < M) {
-            double x, y, z;
-            apply_T(R.T[m], zx, zy, zz, x, y, z);
-            const double dx = x - bx, dy = y - by, dz = z - bz;
-            const unsigned long long d2 = (unsigned long long)__double_as_longlong(dx * dx + dy * dy + dz * dz);
-            dmax[m] = d2 > dmax[m] ? d2 : dmax[m];
-          }
-        }
-      }
-#pragma unroll
-      for (int m = 0; m < MAXM; ++m) {
-        unsigned long long d = dmax[m];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const unsigned long long other = __shfl_xor_sync(0xffffffffu, d, o);
-          d = other > d ? other : d;
-        }
-        if (lane == 0 && m < M && d) atomicMax(&R.disp_bits[m], d);
-      }
-      item_done<GRAD>(R, ctl, r, NG + D, MV, lane);
-      __syncwarp();
-      if (lane == 0) ++Q.head;
-      __syncwarp();
-      continue;
-    }
-    const long long u0 = (long long)c * cu, u1 = min(U, u0 + cu);
-    const f2_t kap2 = pk2(R.kappa, R.kappa);
-#pragma unroll
-    for (int p = 0; p < NP; ++p)
-#pragma unroll
-      for (int v = 0; v < 7; ++v) acc[p][v] = 0ull;
-#pragma unroll
-    for (int p = 0; p < NP; ++p) W[p] = Sx[p] = Sy[p] = Sz[p] = 0ull;
-
-    // per-tile setup from the source's FP32 coordinates
-    auto start_tile = [&](float zx, float zy, float zz) {
-#pragma unroll
-      for (int m = 0; m < MAXM; m += 2) {
-        const float* A = R.Td[m < M ? m : 0];
-        const float* B = R.Td[m + 1 < M ? m + 1 : 0];
-        ndx[m / 2] = pk2(-fmaf(A[0], zx, fmaf(A[1], zy, fmaf(A[2], zz, A[3]))),
-                         -fmaf(B[0], zx, fmaf(B[1], zy, fmaf(B[2], zz, B[3]))));
-        ndy[m / 2] = pk2(-fmaf(A[4], zx, fmaf(A[5], zy, fmaf(A[6], zz, A[7]))),
-                         -fmaf(B[4], zx, fmaf(B[5], zy, fmaf(B[6], zz, B[7]))));
-        ndz[m / 2] = pk2(-fmaf(A[8], zx, fmaf(A[9], zy, fmaf(A[10], zz, A[11]))),
-                         -fmaf(B[8], zx, fmaf(B[9], zy, fmaf(B[10], zz, B[11]))));
-      }
-      if (GRAD) {
-#pragma unroll
-        for (int m = 0; m < MAXM; ++m) {
-          const float* A = R.Ta[m < M ? m : 0];
-          ax[m] = fmaf(A[0], zx, fmaf(A[1], zy, fmaf(A[2], zz, A[3])));
-          ay[m] = fmaf(A[4], zx, fmaf(A[5], zy, fmaf(A[6], zz, A[7])));
-          az[m] = fmaf(A[8], zx, fmaf(A[9], zy, fmaf(A[10], zz, A[11])));
-        }
-      }
-    };
-    bool active = false;
-    auto flush_tile = [&]() {
-      if (active) {
-#pragma unroll
-        for (int p = 0; p < NP; ++p) {
-          acc[p][0] = add2(acc[p][0], W[p]);
-          if (GRAD) {
-            const f2_t fqx = pk2(ax[2 * p], ax[2 * p + 1]);
-            const f2_t fqy = pk2(ay[2 * p], ay[2 * p + 1]);
-            const f2_t fqz = pk2(az[2 * p], az[2 * p + 1]);
-            const f2_t neg = pk2(-1.0f, -1.0f);
-            acc[p][1] = add2(acc[p][1], Sx[p]);
-            acc[p][2] = add2(acc[p][2], Sy[p]);
-            acc[p][3] = add2(acc[p][3], Sz[p]);
-            acc[p][4] = add2(acc[p][4], fma2(mul2(neg, fqz), Sy[p], mul2(fqy, Sz[p])));
-            acc[p][5] = add2(acc[p][5], fma2(mul2(neg, fqx), Sz[p], mul2(fqz, Sx[p])));
-            acc[p][6] = add2(acc[p][6], fma2(mul2(neg, fqy), Sx[p], mul2(fqx, Sy[p])));
-          }
-        }
-      }
-#pragma unroll
-      for (int p = 0; p < NP; ++p) W[p] = Sx[p] = Sy[p] = Sz[p] = 0ull;
-    };
-
-    if (u1 > u0) {
-      // first stage carries the chunk record
-      const int s0 = consumed % kSweepStages;
-      mbar_wait(&bars[s0], (consumed / kSweepStages) & 1);
-      const ChunkRec& rec = recs[rec_used % kRecSlots];
-      ++rec_used;
-      int t = rec.t0;
-      long long t_end = rec.t0_end;
-      active = 32 * t + lane < R.n_z;
-      start_tile(rec.x[lane], rec.y[lane], rec.z[lane]);
-      // prefetch of the next tile (speculatively t + 1)
-      auto prefetch = [&](int tn, float4& pz, long long& pend) {
-        pz = make_float4(0.f, 0.f, 0.f, 0.f);
-        pend = U;
-        if (tn < R.n_tiles) {
-          if (32 * tn + lane < R.n_z) pz = R.zs[32 * tn + lane];
-          pend = R.unit_off[tn + 1];
-        }
-      };
-      float4 pz;
-      long long p_end;
-      prefetch(t + 1, pz, p_end);
-
-      for (long long u = u0; u < u1; u += kStageUnits) {
-        const int nu = (int)min((long long)kStageUnits, u1 - u);
-        const int s = consumed % kSweepStages;
-        if (u != u0) mbar_wait(&bars[s], (consumed / kSweepStages) & 1);
-        const int4* stage = ring + s * kStageSlots + lane;
-        if (u + nu <= t_end) {  // whole stage inside the current tile
-          if (active) sweep_steps<NP, GRAD>(stage, nu * kUnitSteps, ndx, ndy, ndz, kap2, W, Sx, Sy, Sz);
-        } else {
-          long long v = u;
-          while (v < u + nu) {
-            while (v >= t_end) {  // next tile with units
-              flush_tile();
-              ++t;
-              if (p_end > v) {
-                t_end = p_end;
-                active = 32 * t + lane < R.n_z;
-                start_tile(pz.x, pz.y, pz.z);
-              } else {  // tile t had no units (window end): load directly
-                long long e = R.unit_off[t + 1];
-                while (e <= v) e = R.unit_off[++t + 1];
-                t_end = e;
-                const float4 z = 32 * t + lane < R.n_z ? R.zs[32 * t + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
-                active = 32 * t + lane < R.n_z;
-                start_tile(z.x, z.y, z.z);
-              }
-              prefetch(t + 1, pz, p_end);
-            }
-            const long long w_end = min(u + nu, t_end);
-            if (active)
-              sweep_steps<NP, GRAD>(stage + (v - u) * kUnitSlots, (int)(w_end - v) * kUnitSteps, ndx, ndy, ndz, kap2,
-                                    W, Sx, Sy, Sz);
-            v = w_end;
-          }
-        }
-        __syncwarp();
-        ++consumed;
-        if (lane == 0) produce();  // refill the stage just consumed
-        __syncwarp();
-      }
-      flush_tile();
-    }
-
-    // chunk partial: FP32 warp sums (fixed butterfly order) widened to FP64;
-    // lane v stores value v
-    double* part = R.partials + (size_t)c * MV;
-#pragma unroll
-    for (int p = 0; p < NP; ++p) {
-#pragma unroll
-      for (int v = 0; v < (GRAD ? 7 : 1); ++v) {
-        float a0, a1;
-        upk2(warp_sum_f2(acc[p][v]), a0, a1);
-        const int i0 = (2 * p) * (GRAD ? 7 : 1) + v, i1 = (2 * p + 1) * (GRAD ? 7 : 1) + v;
-        if (2 * p < M && lane == (i0 & 31)) part[i0] = (double)a0;
-        if (2 * p + 1 < M && lane == (i1 & 31)) part[i1] = (double)a1;
-      }
-    }
-    // chunk group done? its last chunk sums the group's partials in order
-    __threadfence();
+    if (c < 0) displacement_item(w, R, r, c + D, n_items);
+    else if (R.grad) chunk_body<NPG, true>(w, R, r, c, C, n_items);
+    else chunk_body<4, false>(w, R, r, c, C, n_items);
     __syncwarp();
-    const int grp = c / kChunkGroup;
-    unsigned old = 0;
-    if (lane == 0) old = atomicAdd(&ctl->grp_done[r][grp], 1u);
-    old = __shfl_sync(0xffffffffu, old, 0);
-    const int gsize = min(kChunkGroup, C - grp * kChunkGroup);
-    if ((int)old == gsize - 1) {
-      __threadfence();
-      double* gpart = R.partials + (size_t)kMaxChunks * MV + (size_t)grp * MV;
-      for (int v = lane; v < MV; v += 32) {
-        double t = 0.0;
-        for (int k = grp * kChunkGroup; k < grp * kChunkGroup + gsize; ++k) t += __ldcg(R.partials + (size_t)k * MV + v);
-        gpart[v] = t;
-      }
-      if (lane == 0) ctl->grp_done[r][grp] = 0u;
-      __threadfence();
-      __syncwarp();
-      item_done<GRAD>(R, ctl, r, NG + D, MV, lane);
-    }
-    __syncwarp();
-    if (lane == 0) ++Q.head;
+    if (lane == 0) ++w.Q->head;
     __syncwarp();
   }
   // the last CTA to exit resets the launch's item counter
@@ -1091,6 +1147,11 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(const SweepReq* reqs
       ctl->exited = 0u;
     }
   }
+}
+
+__global__ void k_interleave(const double* x, const double* y, const double* z, int n, double4* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = make_double4(x[i], y[i], z[i], 0.0);
 }
 
 __global__ void k_displacement(const double* zx, const double* zy, const double* zz, int n,
@@ -1152,48 +1213,37 @@ void build_pairs_batched(const BuildReq* h, const BuildReq* d, int n, cudaStream
   count_launch(launches + 5);
 }
 
-size_t sweep_ctl_bytes(int n) { return sizeof(SweepCtl) * (2 * ((n + kMaxSweepReqs - 1) / kMaxSweepReqs) + 2); }
+size_t sweep_ctl_bytes(int n) { return sizeof(SweepCtl) * ((n + kMaxSweepReqs - 1) / kMaxSweepReqs + 1); }
 
 void sweep_batched(const SweepReq* h, const SweepReq* d, int n, int sm_count, unsigned* d_ctl, cudaStream_t st,
                    cudaEvent_t ev0, cudaEvent_t ev1) {
   if (n == 0) return;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(k_sweep<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepSmem);
-    cudaFuncSetAttribute(k_sweep<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepSmem);
-    cudaFuncSetAttribute(k_sweep<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepSmem);
-    cudaFuncSetAttribute(k_sweep<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepSmem);
-    cudaFuncSetAttribute(k_sweep<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepSmem);
-    cudaFuncSetAttribute(k_sweep<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepSmem);
+    cudaFuncSetAttribute(k_sweep<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepSmem);
+    cudaFuncSetAttribute(k_sweep<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepSmem);
+    cudaFuncSetAttribute(k_sweep<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepSmem);
     attr_set = true;
   }
   if (ev0) cudaEventRecord(ev0, st);
   // requests arrive grouped: gradient requests first, then F-only ones; one
   // persistent launch per group (<= kMaxSweepReqs requests each), then one
   // reduction over all requests
-  int n_grad = 0;
-  while (n_grad < n && h[n_grad].grad) ++n_grad;
+  // one persistent launch per kMaxSweepReqs requests (F-only requests first:
+  // their chunks are the heaviest, so they are grabbed first)
   const int grid = 2 * sm_count;
   int launches = 0;
-  for (int grp = 0; grp < 2; ++grp) {
-    const int g0 = grp == 0 ? 0 : n_grad, g1 = grp == 0 ? n_grad : n;
-    for (int r0 = g0; r0 < g1; r0 += kMaxSweepReqs) {
-      const int r1 = min(g1, r0 + kMaxSweepReqs);
-      int max_m = 1;
-      for (int r = r0; r < r1; ++r) max_m = max(max_m, h[r].M);
-      const SweepReq* dr = d + r0;
-      SweepCtl* ctl = reinterpret_cast<SweepCtl*>(d_ctl) + launches;
-      if (grp == 0) {
-        if (max_m <= 2) k_sweep<1, true><<<grid, kSweepThreads, kSweepSmem, st>>>(dr, r1 - r0, ctl);
-        else if (max_m <= 4) k_sweep<2, true><<<grid, kSweepThreads, kSweepSmem, st>>>(dr, r1 - r0, ctl);
-        else k_sweep<4, true><<<grid, kSweepThreads, kSweepSmem, st>>>(dr, r1 - r0, ctl);
-      } else {
-        if (max_m <= 2) k_sweep<1, false><<<grid, kSweepThreads, kSweepSmem, st>>>(dr, r1 - r0, ctl);
-        else if (max_m <= 4) k_sweep<2, false><<<grid, kSweepThreads, kSweepSmem, st>>>(dr, r1 - r0, ctl);
-        else k_sweep<4, false><<<grid, kSweepThreads, kSweepSmem, st>>>(dr, r1 - r0, ctl);
-      }
-      ++launches;
-    }
+  for (int r0 = 0; r0 < n; r0 += kMaxSweepReqs) {
+    const int r1 = min(n, r0 + kMaxSweepReqs);
+    int max_mg = 1;
+    for (int r = r0; r < r1; ++r)
+      if (h[r].grad) max_mg = max(max_mg, h[r].M);
+    const SweepReq* dr = d + r0;
+    SweepCtl* ctl = reinterpret_cast<SweepCtl*>(d_ctl) + launches;
+    if (max_mg <= 2) k_sweep<1><<<grid, kSweepThreads, kSweepSmem, st>>>(dr, r1 - r0, ctl);
+    else if (max_mg <= 4) k_sweep<2><<<grid, kSweepThreads, kSweepSmem, st>>>(dr, r1 - r0, ctl);
+    else k_sweep<4><<<grid, kSweepThreads, kSweepSmem, st>>>(dr, r1 - r0, ctl);
+    ++launches;
   }
   count_launch(launches);
   if (ev1) cudaEventRecord(ev1, st);
@@ -1202,6 +1252,11 @@ void sweep_batched(const SweepReq* h, const SweepReq* d, int n, int sm_count, un
 void displacement(const double* zx, const double* zy, const double* zz, int n, const double* d_T2,
                   unsigned long long* d_out, cudaStream_t st) {
   k_displacement<<<(n + 255) / 256, 256, 0, st>>>(zx, zy, zz, n, d_T2, d_out);
+  count_launch();
+}
+
+void interleave_positions(const double* x, const double* y, const double* z, int n, double4* out, cudaStream_t st) {
+  k_interleave<<<(n + 255) / 256, 256, 0, st>>>(x, y, z, n, out);
   count_launch();
 }
 

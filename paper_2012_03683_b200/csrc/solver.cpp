@@ -22,6 +22,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <vector>
@@ -163,11 +164,26 @@ void finish(Reg& r) {
   r.pairs.reset();
 }
 
+// Optional line-search statistics (KREG_STATS=1): accepted backtrack index
+// histogram (index 21 = search failed), printed to stderr at exit.
+struct SearchStats {
+  long long hist[22] = {};
+  bool on = std::getenv("KREG_STATS") != nullptr;
+  ~SearchStats() {
+    if (!on) return;
+    std::fprintf(stderr, "kreg line-search accepted-k histogram:");
+    for (int k = 0; k < 22; ++k) std::fprintf(stderr, " %lld", hist[k]);
+    std::fprintf(stderr, "\n");
+  }
+};
+SearchStats g_search_stats;
+
 // End of one reference iteration (registration.cpp:145-182).
 void end_iteration(Reg& r, bool searched, bool accepted, int backtracks, double eps, const double* cand_T,
                    const double* cand_out, bool cand_has_grad = true) {
   const kreg_registration_config& c = r.cfg;
   double accepted_step = 0.0, twist_norm = 0.0, f_now = r.ev[0];
+  if (searched && g_search_stats.on) ++g_search_stats.hist[accepted ? std::min(backtracks, 20) : 21];
   if (searched) {
     if (accepted) {
       accepted_step = eps;
