@@ -511,30 +511,39 @@ __global__ void __launch_bounds__(256) k_filter(const BuildReq* reqs) {
   }
   const double c2 = R.cutoff_sq;
   int cnt = 0;
-  for (int sb = 0; sb < ds; sb += 32) {
-    const int k = sb + lane;
-    bool keep = false;
-    int2 e = make_int2(0, 0);
-    double x = 0, y = 0, z = 0;
-    if (k < ds) {
-      e = row[k];
-      const double4 xp = R.xw[e.x];  // one 32-B sector per candidate
-      x = xp.x;
-      y = xp.y;
-      z = xp.z;
-      const double dx = x - qx, dy = y - qy, dz = z - qz;
-      keep = dx * dx + dy * dy + dz * dz <= c2;
+  // two batches of 32 candidates in flight (entry loads, then the dependent
+  // position gathers, as one 32-B sector each); kept in candidate order
+  for (int sb = 0; sb < ds; sb += 64) {
+    const int k0 = sb + lane, k1 = sb + 32 + lane;
+    int2 e0 = make_int2(0, 0), e1 = make_int2(0, 0);
+    if (k0 < ds) e0 = row[k0];
+    if (k1 < ds) e1 = row[k1];
+    double4 p0 = make_double4(0, 0, 0, 0), p1 = make_double4(0, 0, 0, 0);
+    if (k0 < ds) p0 = R.xw[e0.x];
+    if (k1 < ds) p1 = R.xw[e1.x];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int k = h ? k1 : k0;
+      const int2 e = h ? e1 : e0;
+      const double4 xp = h ? p1 : p0;
+      bool keep = false;
+      double dx = 0, dy = 0, dz = 0;
+      if (k < ds) {
+        dx = xp.x - qx;
+        dy = xp.y - qy;
+        dz = xp.z - qz;
+        keep = dx * dx + dy * dy + dz * dz <= c2;
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, keep);
+      if (EMIT && keep) {
+        const long long at = out + 32LL * (cnt + __popc(m & ((1u << lane) - 1u)));
+        // x_i - T_b z_j in FP32 (|.| <= cutoff): the sweep forms d = x_i - T z_j
+        // as this minus the source's displacement (T - T_b) z_j
+        R.slots[at] = make_int4(__float_as_int((float)dx), __float_as_int((float)dy), __float_as_int((float)dz), e.y);
+        R.slot_i[at] = e.x;
+      }
+      cnt += __popc(m);
     }
-    const unsigned m = __ballot_sync(0xffffffffu, keep);
-    if (EMIT && keep) {
-      const long long at = out + 32LL * (cnt + __popc(m & ((1u << lane) - 1u)));
-      // x_i - T_b z_j in FP32 (|.| <= cutoff): the sweep forms d = x_i - T z_j
-      // as this minus the source's displacement (T - T_b) z_j
-      R.slots[at] = make_int4(__float_as_int((float)(x - qx)), __float_as_int((float)(y - qy)),
-                              __float_as_int((float)(z - qz)), e.y);
-      R.slot_i[at] = e.x;
-    }
-    cnt += __popc(m);
   }
   if (!EMIT) {
     if (lane == 0) R.count[j] = cnt;
@@ -712,22 +721,20 @@ __device__ __noinline__ void item_done(const SweepReq& R, SweepCtl* ctl, int r, 
   const int C = chunk_count(request_units(R));
   const int NG = (C + kChunkGroup - 1) / kChunkGroup;
   const double* gpart = R.partials + (size_t)kMaxChunks * MV;
-  double v0 = 0.0, v1 = 0.0;  // values lane and lane + 32 (loads batched, adds in order)
-  if (lane < MV) {
-#pragma unroll 8
-    for (int g = 0; g < NG; ++g) v0 += __ldcg(gpart + (size_t)g * MV + lane);
-  }
-  if (lane + 32 < MV) {
-#pragma unroll 8
-    for (int g = 0; g < NG; ++g) v1 += __ldcg(gpart + (size_t)g * MV + lane + 32);
-  }
+  // group partials: lane l holds groups l and l + 32 (NG <= 64), fixed-order
+  // shuffle tree per value
   double t[7];
+  for (int m = 0; m < M; ++m) {
 #pragma unroll
-  for (int k = 0; k < 7; ++k) {
-    const int src = (lane < M ? lane : 0) * NV + (k < NV ? k : 0);
-    const double a = __shfl_sync(0xffffffffu, v0, src & 31);
-    const double b = __shfl_sync(0xffffffffu, v1, src & 31);
-    t[k] = k < NV ? (src < 32 ? a : b) : 0.0;
+    for (int k = 0; k < 7; ++k) {
+      double v = 0.0;
+      if (k < NV) {
+        if (lane < NG) v = __ldcg(gpart + (size_t)lane * MV + m * NV + k);
+        if (lane + 32 < NG) v += __ldcg(gpart + (size_t)(lane + 32) * MV + m * NV + k);
+      }
+      const double tot = __shfl_sync(0xffffffffu, warp_sum_d(v), 0);
+      if (lane == m) t[k] = k < NV ? tot : 0.0;
+    }
   }
   if (lane < M) {
     const double gvx = t[1], gvy = t[2], gvz = t[3];  // sum w (x - q), meters
@@ -1041,12 +1048,11 @@ __device__ __forceinline__ void chunk_body(SweepWarp& w, const SweepReq& R, int 
   if ((int)old == gsize - 1) {
     __threadfence();
     double* gpart = R.partials + (size_t)kMaxChunks * MV + (size_t)grp * MV;
-    for (int v = lane; v < MV; v += 32) {
-      double t = 0.0;
-      const double* src = R.partials + (size_t)grp * kChunkGroup * MV + v;
-#pragma unroll 8
-      for (int k = 0; k < gsize; ++k) t += __ldcg(src + (size_t)k * MV);  // loads batched, adds in order
-      gpart[v] = t;
+    // lane l loads chunk (group base + l); fixed-order shuffle tree per value
+    const double* src = R.partials + ((size_t)grp * kChunkGroup + lane) * MV;
+    for (int v = 0; v < MV; ++v) {
+      const double x = warp_sum_d(lane < gsize ? __ldcg(src + v) : 0.0);
+      if (lane == 0) gpart[v] = x;
     }
     if (lane == 0) w.ctl->grp_done[r][grp] = 0u;
     __threadfence();
