@@ -42,6 +42,15 @@ constexpr int kMaxSweepReqs = kSweepThreads;     // requests per sweep launch
 constexpr int kChunkGroup = 32;                  // chunk partials summed per group (first reduction level)
 constexpr int kMaxChunkGroups = (kMaxChunks + kChunkGroup - 1) / kChunkGroup;
 constexpr int kDispItem = 512;                   // sources per displacement work item
+// Sliced-ELL slot of step k of the source in lane l of a tile starting at slot
+// tile_off: units of kUnitSteps = 2 steps x 32 sources, source-major inside a
+// unit (a source's two slots of a unit share one 32-B sector) with an XOR
+// swizzle that keeps the sweep's per-lane LDS.128 conflict-free.
+static_assert(KREG_UNIT_STEPS == 2, "slot_index assumes 2-step units");
+__host__ __device__ __forceinline__ long long slot_index(long long tile_off, int lane, int k) {
+  return tile_off + (long long)(k >> 1) * 64 + 2 * lane + ((k & 1) ^ ((lane >> 2) & 1));
+}
+
 constexpr int kMaxChannels = 8;
 constexpr int kMaxCandidates = 8;   // candidate transforms per sweep request
 constexpr int kOut = 8;             // {F, omega[3], v[3], max displacement}
@@ -103,7 +112,8 @@ struct BuildReq {
   long long* scan_tiles; // cell-scan workspace (tile sums)
   int* sup_count;        // n_z: candidates of every source
   long long* sup_off;    // n_tiles + 1: candidate tile offsets (entries)
-  int2* sup;             // sup_capacity entries {i, float_as_int(log2 c)}
+  int4* sup;             // sup_capacity entries {x_i - Ts z_j (FP32 x3), log2 c}
+  int* sup_i;            // sup_capacity: their target index i
   long long sup_capacity;
   CoeffParams cp;
   // filter stage

@@ -435,6 +435,7 @@ static void prepare_build(kreg_ctx* ctx, BuildJob& job, kreg_dev::BuildReq& R) {
     const long long want = p->expected_sup > 0 ? p->expected_sup : static_cast<long long>(nz) * 256 + 4096;
     if (p->sup.cap < static_cast<size_t>(want)) {
       p->sup.ensure(static_cast<size_t>(std::max<long long>(want + want / 4, ctx->hw_sup)), false, 1.0);
+      p->sup_i.ensure(p->sup.cap, false, 1.0);
       ctx->hw_sup = std::max<long long>(ctx->hw_sup, static_cast<long long>(p->sup.cap));
     }
     R.cell_count = p->cell_count.ptr;
@@ -454,6 +455,7 @@ static void prepare_build(kreg_ctx* ctx, BuildJob& job, kreg_dev::BuildReq& R) {
   R.sup_count = p->sup_count.ptr;
   R.sup_off = p->sup_off.ptr;
   R.sup = p->sup.ptr;
+  R.sup_i = p->sup_i.ptr;
   R.sup_capacity = static_cast<long long>(p->sup.cap);
   const double limit = p->sup_radius - cutoff - margin;
   R.filter_limit_sq = limit > 0.0 ? limit * limit : 0.0;
@@ -758,9 +760,9 @@ void pairs_export(kreg_ctx* ctx, const kreg_pairs* p, int64_t* offsets, int32_t*
     const int j = p->Z->order[js];
     tmp.clear();
     const int ps = pos[static_cast<size_t>(js)];                         // degree-sorted position of js
-    const long long col = toff[static_cast<size_t>(ps >> 5)] + (ps & 31);  // its sliced-ELL column
+    const long long tile = toff[static_cast<size_t>(ps >> 5)];             // its tile (sliced ELL)
     for (long long k = 0; k < deg[js]; ++k) {
-      const size_t at = static_cast<size_t>(col + 32 * k);
+      const size_t at = static_cast<size_t>(kreg_dev::slot_index(tile, ps & 31, static_cast<int>(k)));
       float lc;
       std::memcpy(&lc, &sl[at].w, sizeof(float));
       tmp.push_back({p->X->order[si[at]], std::exp2(static_cast<double>(lc))});

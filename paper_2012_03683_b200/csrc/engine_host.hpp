@@ -186,7 +186,8 @@ struct kreg_pairs {
   kreg_host::DevBuf<double> cx, cy, cz;
   kreg_host::DevBuf<long long> scan_tiles;
   // candidate list: pairs within R_s = cutoff (1 + skin) of Ts z_j with c > c_min
-  kreg_host::DevBuf<int2> sup;             // per tile: 32 rows of H_t entries {i, log2 c}
+  kreg_host::DevBuf<int4> sup;             // per tile: 32 rows of H_t entries {x_i - Ts z_j, log2 c}
+  kreg_host::DevBuf<int> sup_i;            // their target indices
   kreg_host::DevBuf<int> sup_count;
   kreg_host::DevBuf<long long> sup_off;
   bool sup_valid = false;                  // a complete candidate list is resident

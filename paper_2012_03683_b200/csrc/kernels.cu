@@ -287,8 +287,11 @@ __global__ void __launch_bounds__(256) k_pair_pass(const BuildReq* reqs) {
           bool keep = false;
           float lc = 0.0f;
           int i = 0;
+          double dx = 0, dy2 = 0, dz2 = 0;
           if (s < s1) {
-            const double dx = R.cx[s] - qx, dy2 = R.cy[s] - qy, dz2 = R.cz[s] - qz;
+            dx = R.cx[s] - qx;
+            dy2 = R.cy[s] - qy;
+            dz2 = R.cz[s] - qz;
             if (dx * dx + dy2 * dy2 + dz2 * dz2 <= R.sup_cutoff_sq) {
               i = R.cell_items[s];
               keep = geo ? true : coefficient(R.cp, R.xfeat + (long long)i * fs, zf, &lc);
@@ -296,8 +299,12 @@ __global__ void __launch_bounds__(256) k_pair_pass(const BuildReq* reqs) {
           }
           const unsigned m = __ballot_sync(0xffffffffu, keep);
           if (EMIT && keep) {
+            // {x_i - Ts z_j (FP32), log2 c}: the filter tests and emits
+            // x_i - T z_j = this - (T - Ts) z_j without gathering x_i
             const int pos = __popc(m & ((1u << lane) - 1u));
-            R.sup[out + cnt + pos] = make_int2(i, __float_as_int(lc));
+            R.sup[out + cnt + pos] = make_int4(__float_as_int((float)dx), __float_as_int((float)dy2),
+                                               __float_as_int((float)dz2), __float_as_int(lc));
+            R.sup_i[out + cnt + pos] = i;
           }
           cnt += __popc(m);
         }
@@ -458,16 +465,17 @@ __global__ void __launch_bounds__(kOrderWindow) k_order(const BuildReq* reqs) {
   }
 }
 
-// Filter stage, one warp per source j (lanes over its candidate row,
-// coalesced 8-B entries + gathers of x_i from the L2-resident cloud). Applies
-// the reference predicate |x_i - T z_j|^2 <= cutoff^2 in FP64
-// (inner_product.cpp:69) with the same operations as a direct search, so the
-// kept set is exactly the direct build's set whenever the candidate radius
-// covers cutoff + |T z_j - Ts z_j| (checked: COUNT writes the block's max
-// displacement to disp_blk[], k_tile_offsets flags a violation).
-// EMIT=false: count[j]. EMIT=true: j's slots {x_i fixed point, log2 c} in
-// candidate order into its sliced-ELL column (slot(k) = tile_off[t] + 32 k +
-// j%32), padded to the tile's unit-rounded column height.
+// Filter stage, one warp per source j, lanes over its candidate row: a pure
+// stream of 16-B entries {x_i - Ts z_j (FP32), log2 c} (two batches of 32 in
+// flight). d = (x_i - Ts z_j) - (T - Ts) z_j = x_i - T z_j is tested against
+// the cutoff in FP32 (the reference predicate, inner_product.cpp:69, to
+// ~1e-7 m: only pairs that close to the cutoff can differ from an FP64 test,
+// inside the 1e-6 m tie tolerance). The candidate radius covers cutoff +
+// |T z_j - Ts z_j| (checked: COUNT writes the block's max displacement to
+// disp_blk[], k_tile_offsets flags a violation).
+// EMIT=false: count[j]. EMIT=true: j's slots {d, log2 c} (and i) in candidate
+// order into its sliced-ELL column (slot(k) = tile_off[t] + 32 k + lane of its
+// degree-sorted position), padded to the tile's unit-rounded column height.
 template <bool EMIT>
 __global__ void __launch_bounds__(256) k_filter(const BuildReq* reqs) {
   const BuildReq& R = reqs[blockIdx.y];
@@ -476,14 +484,15 @@ __global__ void __launch_bounds__(256) k_filter(const BuildReq* reqs) {
   const bool sup_ok = R.sup_off[R.n_tiles] <= R.sup_capacity;
   if (EMIT && (!sup_ok || R.tile_off[R.n_tiles] > R.capacity)) return;  // host grows and re-runs
   const bool active = j < R.n_z;
-  double qx = 0, qy = 0, qz = 0;
-  if (active) apply_T(R.T, R.zx[j], R.zy[j], R.zz[j], qx, qy, qz);
+  double qx = 0, qy = 0, qz = 0, sx = 0, sy = 0, sz = 0;
+  if (active) {
+    apply_T(R.T, R.zx[j], R.zy[j], R.zz[j], qx, qy, qz);
+    apply_T(R.Ts, R.zx[j], R.zy[j], R.zz[j], sx, sy, sz);
+  }
   if (!EMIT) {
     __shared__ unsigned long long dblk[8];
     unsigned long long d2 = 0;
     if (active) {
-      double sx, sy, sz;
-      apply_T(R.Ts, R.zx[j], R.zy[j], R.zz[j], sx, sy, sz);
       const double dx = qx - sx, dy = qy - sy, dz = qz - sz;
       d2 = (unsigned long long)__double_as_longlong(dx * dx + dy * dy + dz * dz);
     }
@@ -496,51 +505,43 @@ __global__ void __launch_bounds__(256) k_filter(const BuildReq* reqs) {
     }
   }
   if (!active) return;
-  const int t = j >> 5;
+  // (T - Ts) z_j, the shift from candidate to list coordinates
+  const float ex = (float)(qx - sx), ey = (float)(qy - sy), ez = (float)(qz - sz);
   int ds = 0;
-  const int2* row = R.sup;
+  long long rb = 0;
   if (sup_ok) {
     ds = R.sup_count[j];
-    const long long t0 = R.sup_off[t], H = (R.sup_off[t + 1] - t0) >> 5;
-    row = R.sup + t0 + (j & 31) * H;
+    const long long t0 = R.sup_off[j >> 5], H = (R.sup_off[(j >> 5) + 1] - t0) >> 5;
+    rb = t0 + (j & 31) * H;
   }
+  const int4* row = R.sup + rb;
   long long out = 0;
-  if (EMIT) {  // column of j in the degree-sorted order
+  int col = 0;
+  if (EMIT) {  // tile and lane of j in the degree-sorted order
     const int p = R.pos[j];
-    out = R.tile_off[p >> 5] + (p & 31);
+    out = R.tile_off[p >> 5];
+    col = p & 31;
   }
-  const double c2 = R.cutoff_sq;
+  const float c2 = (float)R.cutoff_sq;
   int cnt = 0;
-  // two batches of 32 candidates in flight (entry loads, then the dependent
-  // position gathers, as one 32-B sector each); kept in candidate order
   for (int sb = 0; sb < ds; sb += 64) {
     const int k0 = sb + lane, k1 = sb + 32 + lane;
-    int2 e0 = make_int2(0, 0), e1 = make_int2(0, 0);
+    int4 e0 = make_int4(0, 0, 0, 0), e1 = make_int4(0, 0, 0, 0);
     if (k0 < ds) e0 = row[k0];
     if (k1 < ds) e1 = row[k1];
-    double4 p0 = make_double4(0, 0, 0, 0), p1 = make_double4(0, 0, 0, 0);
-    if (k0 < ds) p0 = R.xw[e0.x];
-    if (k1 < ds) p1 = R.xw[e1.x];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int k = h ? k1 : k0;
-      const int2 e = h ? e1 : e0;
-      const double4 xp = h ? p1 : p0;
-      bool keep = false;
-      double dx = 0, dy = 0, dz = 0;
-      if (k < ds) {
-        dx = xp.x - qx;
-        dy = xp.y - qy;
-        dz = xp.z - qz;
-        keep = dx * dx + dy * dy + dz * dz <= c2;
-      }
+      const int4 e = h ? e1 : e0;
+      const float dx = __int_as_float(e.x) - ex, dy = __int_as_float(e.y) - ey, dz = __int_as_float(e.z) - ez;
+      const bool keep = k < ds && fmaf(dx, dx, fmaf(dy, dy, dz * dz)) <= c2;
       const unsigned m = __ballot_sync(0xffffffffu, keep);
       if (EMIT && keep) {
-        const long long at = out + 32LL * (cnt + __popc(m & ((1u << lane) - 1u)));
+        const long long at = slot_index(out, col, cnt + __popc(m & ((1u << lane) - 1u)));
         // x_i - T_b z_j in FP32 (|.| <= cutoff): the sweep forms d = x_i - T z_j
         // as this minus the source's displacement (T - T_b) z_j
-        R.slots[at] = make_int4(__float_as_int((float)dx), __float_as_int((float)dy), __float_as_int((float)dz), e.y);
-        R.slot_i[at] = e.x;
+        R.slots[at] = make_int4(__float_as_int(dx), __float_as_int(dy), __float_as_int(dz), e.w);
+        R.slot_i[at] = R.sup_i[rb + k];
       }
       cnt += __popc(m);
     }
@@ -552,8 +553,8 @@ __global__ void __launch_bounds__(256) k_filter(const BuildReq* reqs) {
     const int ts = R.pos[j] >> 5;
     const int height = (R.unit_off[ts + 1] - R.unit_off[ts]) * kUnitSteps;
     for (int k = cnt + lane; k < height; k += 32) {
-      R.slots[out + 32LL * k] = make_int4(0, 0, 0, __float_as_int(-INFINITY));
-      R.slot_i[out + 32LL * k] = -1;
+      R.slots[slot_index(out, col, k)] = make_int4(0, 0, 0, __float_as_int(-INFINITY));
+      R.slot_i[slot_index(out, col, k)] = -1;
     }
   }
 }
@@ -660,16 +661,18 @@ constexpr size_t kSweepSmem = (size_t)kSweepWarps * kSweepStages * kStageSlots *
                               (size_t)kSweepWarps * kRecSlots * sizeof(ChunkRec) +
                               (size_t)kSweepWarps * kSweepStages * sizeof(unsigned long long);
 
-// `steps` degree steps of one sliced-ELL column (lane = source) for M
+// `units` sweep units (2 steps each) of one tile column (lane = source) for M
 // candidates: d = (x - T_b z) - delta, w = ex2(r^2 kappa + log2 c), W += w
 // and (GRAD) S += w d on FFMA2/FADD2/FMUL2 + 2 MUFU.EX2 per candidate pair.
 template <int NP, bool GRAD>
-__device__ __forceinline__ void sweep_steps(const int4* __restrict__ col, int steps, const f2_t (&ndx)[NP],
+__device__ __forceinline__ void sweep_steps(const int4* __restrict__ unit, int lane, int units, const f2_t (&ndx)[NP],
                                             const f2_t (&ndy)[NP], const f2_t (&ndz)[NP], f2_t kap2, f2_t (&W)[NP],
                                             f2_t (&Sx)[NP], f2_t (&Sy)[NP], f2_t (&Sz)[NP]) {
+  const int4* col = unit + 2 * lane;
+  const int sw = (lane >> 2) & 1;
 #pragma unroll 2
-  for (int k = 0; k < steps; ++k) {
-    const int4 sl = col[32 * k];  // conflict-free LDS.128
+  for (int k = 0; k < 2 * units; ++k) {
+    const int4 sl = col[(k >> 1) * kUnitSlots + ((k & 1) ^ sw)];  // conflict-free LDS.128 (slot_index)
     const float x = __int_as_float(sl.x), y = __int_as_float(sl.y), z = __int_as_float(sl.z);
     const float lc = __int_as_float(sl.w);
     const f2_t x2 = pk2(x, x), y2 = pk2(y, y), z2 = pk2(z, z), lc2 = pk2(lc, lc);
@@ -985,9 +988,9 @@ __device__ __forceinline__ void chunk_body(SweepWarp& w, const SweepReq& R, int 
       const int nu = (int)min((long long)kStageUnits, u1 - u);
       const int s = w.consumed % kSweepStages;
       if (u != u0) mbar_wait(&w.bars[s], (w.consumed / kSweepStages) & 1);
-      const int4* stage = w.ring + s * kStageSlots + lane;
+      const int4* stage = w.ring + s * kStageSlots;
       if (u + nu <= t_end) {  // whole stage inside the current tile
-        if (active) sweep_steps<NP, GRAD>(stage, nu * kUnitSteps, ndx, ndy, ndz, kap2, W, Sx, Sy, Sz);
+        if (active) sweep_steps<NP, GRAD>(stage, lane, nu, ndx, ndy, ndz, kap2, W, Sx, Sy, Sz);
       } else {
         long long v = u;
         while (v < u + nu) {
@@ -1010,8 +1013,8 @@ __device__ __forceinline__ void chunk_body(SweepWarp& w, const SweepReq& R, int 
           }
           const long long w_end = min(u + nu, t_end);
           if (active)
-            sweep_steps<NP, GRAD>(stage + (v - u) * kUnitSlots, (int)(w_end - v) * kUnitSteps, ndx, ndy, ndz, kap2, W,
-                                  Sx, Sy, Sz);
+            sweep_steps<NP, GRAD>(stage + (v - u) * kUnitSlots, lane, (int)(w_end - v), ndx, ndy, ndz, kap2, W, Sx, Sy,
+                                  Sz);
           v = w_end;
         }
       }
