@@ -176,6 +176,18 @@ kreg_status kreg_ctx_set_candidate_skin(kreg_ctx* ctx, double skin);
 /* Builds so far: {grid searches, candidate-list filters}. */
 kreg_status kreg_ctx_build_stats(const kreg_ctx* ctx, int64_t out[2]);
 
+/* Multi-GPU source-row sharding (configuration C4): every
+ * rank registers the replicated target X against its own rows of the source
+ * Z, and after every device round the host loop combines the per-rank
+ * partial results through this callback: element-wise SUM of `sums` (per
+ * request and candidate: F, omega, v; per build: pair count) and MAX of
+ * `maxes` (per request and candidate: displacement), in place, identical on
+ * all ranks (an all-reduce; NCCL on GPUs). All ranks then make identical
+ * decisions, so the replicated loop stays in lockstep. Return 0 on success.
+ * NULL clears the hook. */
+typedef int32_t (*kreg_collective_fn)(void* user, double* sums, int32_t n_sums, double* maxes, int32_t n_maxes);
+kreg_status kreg_ctx_set_collective(kreg_ctx* ctx, kreg_collective_fn fn, void* user);
+
 /* Upload a cloud into device SoA (replaces constructing kreg::PointCloud,
  * point_cloud.cpp:49-59; same validation and messages). */
 kreg_status kreg_cloud_create(kreg_ctx* ctx, const kreg_cloud_view* view, kreg_cloud** out);
@@ -254,6 +266,16 @@ kreg_status kreg_register_clouds(kreg_ctx* ctx, const kreg_cloud* X, const kreg_
                                  const double initial[12], const kreg_kernel_params* params,
                                  const kreg_registration_config* config,
                                  kreg_registration_result* result);
+/* One rank's share of a row-sharded registration (C4): Z_rows holds this
+ * rank's rows of the source, n_z_total the size of the whole source (the
+ * indicator denominator sqrt(|X| |Z|), registration.cpp:108-109). Per-round
+ * results are combined through the context's collective (kreg_ctx_set_collective);
+ * without one this is register_clouds with that denominator. */
+kreg_status kreg_register_clouds_rows(kreg_ctx* ctx, const kreg_cloud* X, const kreg_cloud* Z_rows,
+                                      int64_t n_z_total, const double initial[12],
+                                      const kreg_kernel_params* params,
+                                      const kreg_registration_config* config,
+                                      kreg_registration_result* result);
 /* Same, from host views: uploads X and Z, registers, frees (end-to-end call). */
 kreg_status kreg_register_clouds_host(kreg_ctx* ctx, const kreg_cloud_view* X,
                                       const kreg_cloud_view* Z, const double initial[12],
@@ -290,6 +312,16 @@ kreg_status kreg_register_sequence_chains(kreg_ctx* ctx, const kreg_cloud* const
                                           const kreg_kernel_params* params,
                                           const kreg_registration_config* config,
                                           kreg_sequence_result* result);
+/* Chains with explicit pair spans [begins[s], ends[s]) (pair p registers frames
+ * p -> p + 1; spans ordered and disjoint): a rank of a multi-GPU sequence runs
+ * its share of the global chain partition. Pairs outside the spans are
+ * returned as identity with fallback = 0 and iterations = 0; the trajectory
+ * is only meaningful when the spans cover every pair. */
+kreg_status kreg_register_sequence_spans(kreg_ctx* ctx, const kreg_cloud* const* frames,
+                                         int32_t n_frames, const int32_t* begins, const int32_t* ends,
+                                         int32_t n_spans, const kreg_kernel_params* params,
+                                         const kreg_registration_config* config,
+                                         kreg_sequence_result* result);
 
 /* ------------------------------------------------------- SE(3) host math */
 /* reference se3.cpp:48-76 exp, 109-120 compose, 122-127 inverse. */

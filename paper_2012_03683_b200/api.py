@@ -32,6 +32,10 @@ VP = C.POINTER(_abi.kreg_cloud_view)
 KP = C.POINTER(_abi.kreg_kernel_params)
 CP = C.POINTER(_abi.kreg_registration_config)
 RP = C.POINTER(_abi.kreg_registration_result)
+VP_ = C.c_void_p
+# kreg_collective_fn: int32 (*)(void*, double* sums, int32 n_sums, double* maxes, int32 n_maxes)
+COLLECTIVE_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.POINTER(C.c_double), C.c_int32, C.POINTER(C.c_double),
+                            C.c_int32)
 
 
 def lib():
@@ -86,6 +90,10 @@ def lib():
         L.kreg_register_sequence.argtypes = [P, C.POINTER(P), C.c_int32, KP, CP, C.POINTER(_abi.kreg_sequence_result)]
         L.kreg_register_sequence_chains.argtypes = [P, C.POINTER(P), C.c_int32, C.c_int32, KP, CP,
                                                     C.POINTER(_abi.kreg_sequence_result)]
+        L.kreg_register_sequence_spans.argtypes = [P, C.POINTER(P), C.c_int32, _abi.i32ptr, _abi.i32ptr, C.c_int32, KP,
+                                                   CP, C.POINTER(_abi.kreg_sequence_result)]
+        L.kreg_register_clouds_rows.argtypes = [P, P, P, C.c_int64, _abi.dptr, KP, CP, RP]
+        L.kreg_ctx_set_collective.argtypes = [P, COLLECTIVE_FN, VP_]
         L.kreg_se3_exp.argtypes = [_abi.dptr, _abi.dptr]
         L.kreg_se3_compose.argtypes = [_abi.dptr, _abi.dptr, _abi.dptr]
         L.kreg_se3_inverse.argtypes = [_abi.dptr, _abi.dptr]
@@ -437,6 +445,45 @@ def register_sequence(frames, params: KernelParams, config: RegistrationConfig, 
         _check(lib().kreg_register_sequence_chains(ctx.h, fh, n, int(chains), params.cstruct(), C.byref(cfg),
                                                    C.byref(sb.struct)))
     return sb.result()
+
+
+def register_sequence_spans(frames, spans, params: KernelParams, config: RegistrationConfig, ctx=None) -> SequenceResult:
+    """Chains over explicit pair spans [(begin, end), ...] (pair p registers
+    frame p -> p + 1): a rank's share of a distributed sequence (parallel.py).
+    Pairs outside the spans come back as identity, fallback 0, 0 iterations."""
+    ctx = ctx or default_context()
+    n = len(frames)
+    ds = [device_cloud(f, ctx) for f in frames]
+    fh = (P * max(n, 1))(*[d.h for d in ds])
+    sb = SequenceBuffers(max(n, 1))
+    cfg = config.cstruct()
+    b = np.ascontiguousarray([s[0] for s in spans], dtype=np.int32)
+    e = np.ascontiguousarray([s[1] for s in spans], dtype=np.int32)
+    _check(lib().kreg_register_sequence_spans(ctx.h, fh, n, _abi.as_ptr(b, C.c_int32), _abi.as_ptr(e, C.c_int32),
+                                              len(spans), params.cstruct(), C.byref(cfg), C.byref(sb.struct)))
+    return sb.result()
+
+
+def register_clouds_rows(X, Z_rows, n_z_total: int, initial, params: KernelParams, config: RegistrationConfig,
+                         ctx=None, collective=None, trace_capacity: int | None = None) -> RegistrationResult:
+    """One rank's share of a row-sharded registration: Z_rows
+    are this rank's source rows, n_z_total the whole source's size. Every
+    round's sums / maxima are combined through `collective` (a kreg_collective_fn
+    wrapper, e.g. parallel.TorchCollective), so all ranks run the identical
+    replicated host loop."""
+    ctx = ctx or default_context()
+    dx, dz = device_cloud(X, ctx), device_cloud(Z_rows, ctx)
+    t, tp = _t12(initial)
+    buf = _abi.TraceBuffers(trace_capacity or config.max_iterations)
+    cfg = config.cstruct()
+    fn = collective.c_fn if collective is not None else COLLECTIVE_FN()
+    _check(lib().kreg_ctx_set_collective(ctx.h, fn, None))
+    try:
+        _check(lib().kreg_register_clouds_rows(ctx.h, dx.h, dz.h, int(n_z_total), tp, params.cstruct(), C.byref(cfg),
+                                               C.byref(buf.struct)))
+    finally:
+        lib().kreg_ctx_set_collective(ctx.h, COLLECTIVE_FN(), None)
+    return RegistrationResult.from_buffers(buf)
 
 
 def se3_exp(xi) -> Isometry:

@@ -126,6 +126,7 @@ void run_chains(kreg_ctx* ctx, const kreg_cloud* const* frames, int n_frames, co
                 kreg_sequence_result* out) {
   const int m = n_frames - 1;
   std::vector<double> rel(static_cast<size_t>(m) * 12);
+  for (int k = 0; k < m; ++k) kreg_se3::identity(rel.data() + 12 * k);  // pairs outside the spans
   std::vector<uint8_t> fb(static_cast<size_t>(m)), cv(static_cast<size_t>(m));
   std::vector<double> fi(static_cast<size_t>(m));
   std::vector<int> it(static_cast<size_t>(m));
@@ -546,6 +547,28 @@ kreg_status kreg_register_clouds(kreg_ctx* ctx, const kreg_cloud* X, const kreg_
   });
 }
 
+kreg_status kreg_register_clouds_rows(kreg_ctx* ctx, const kreg_cloud* X, const kreg_cloud* Z_rows,
+                                      int64_t n_z_total, const double initial[12], const kreg_kernel_params* params,
+                                      const kreg_registration_config* config, kreg_registration_result* result) {
+  return guarded([&] {
+    require(ctx != nullptr, "NULL context");
+    require(Z_rows != nullptr && n_z_total >= Z_rows->n, "n_z_total must cover this rank's rows");
+    std::vector<RegJob> jobs(1);
+    make_jobs(X, Z_rows, initial, params, config, result, jobs[0]);
+    jobs[0].n_z_total = n_z_total;
+    register_many(ctx, jobs, &ctx->collective);
+    if (jobs[0].status != KREG_OK) throw Error(jobs[0].status, jobs[0].error);
+  });
+}
+
+kreg_status kreg_ctx_set_collective(kreg_ctx* ctx, kreg_collective_fn fn, void* user) {
+  return guarded([&] {
+    require(ctx != nullptr, "NULL context");
+    ctx->collective.fn = fn;
+    ctx->collective.user = user;
+  });
+}
+
 kreg_status kreg_register_clouds_host(kreg_ctx* ctx, const kreg_cloud_view* X, const kreg_cloud_view* Z,
                                       const double initial[12], const kreg_kernel_params* params,
                                       const kreg_registration_config* config, kreg_registration_result* result) {
@@ -616,6 +639,24 @@ kreg_status kreg_register_sequence_chains(kreg_ctx* ctx, const kreg_cloud* const
     for (int c = 0; c < nc; ++c) {
       b.push_back(static_cast<int>(static_cast<long long>(m) * c / nc));
       e.push_back(static_cast<int>(static_cast<long long>(m) * (c + 1) / nc));
+    }
+    run_chains(ctx, frames, n_frames, b, e, to_params(params), *config, result);
+  });
+}
+
+kreg_status kreg_register_sequence_spans(kreg_ctx* ctx, const kreg_cloud* const* frames, int32_t n_frames,
+                                         const int32_t* begins, const int32_t* ends, int32_t n_spans,
+                                         const kreg_kernel_params* params, const kreg_registration_config* config,
+                                         kreg_sequence_result* result) {
+  return guarded([&] {
+    if (n_frames < 2) throw Error(KREG_INVALID_ARGUMENT, "register_sequence: need at least 2 frames");
+    require(ctx && frames && params && config && result && begins && ends && n_spans >= 1, "invalid argument");
+    std::vector<int> b, e;
+    for (int s = 0; s < n_spans; ++s) {
+      require(begins[s] >= 0 && begins[s] < ends[s] && ends[s] <= n_frames - 1, "span out of range");
+      if (s) require(begins[s] >= ends[s - 1], "spans must be ordered and disjoint");
+      b.push_back(begins[s]);
+      e.push_back(ends[s]);
     }
     run_chains(ctx, frames, n_frames, b, e, to_params(params), *config, result);
   });

@@ -110,6 +110,12 @@ struct Config {  // RegistrationConfig (registration.hpp:13-40)
 
 struct RoundSlot;
 
+// Cross-rank combination of one round's results (row sharding, solver.cpp).
+struct Collective {
+  kreg_collective_fn fn = nullptr;
+  void* user = nullptr;
+};
+
 }  // namespace kreg_host
 
 struct kreg_ctx {
@@ -143,6 +149,7 @@ struct kreg_ctx {
   // must grow goes straight to the largest size any registration needed
   long long hw_slots = 0, hw_sup = 0, hw_cells = 0;
   long long full_builds = 0, filter_builds = 0;
+  kreg_host::Collective collective;  // row-sharded registrations (kreg_ctx_set_collective)
   // host-side round accounting (seconds)
   long long rounds = 0;
   double t_prepare = 0.0, t_wait = 0.0, t_total = 0.0;

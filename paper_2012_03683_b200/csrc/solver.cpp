@@ -448,7 +448,29 @@ void consume(Reg& r) {
 
 }  // namespace
 
-void register_many(kreg_ctx* ctx, std::vector<RegJob>& jobs) {
+// Combine a finished round across ranks: F, omega, v and pair counts are
+// summed, displacements maxed (each rank holds disjoint source rows).
+void reduce_round(RoundSlot& S, const Collective& coll) {
+  std::vector<double> sums, maxes;
+  for (const EvalJob& e : S.evals)
+    for (int m = 0; m < e.M; ++m) {
+      for (int k = 0; k < 7; ++k) sums.push_back(e.out[m * kreg_dev::kOut + k]);
+      maxes.push_back(e.out[m * kreg_dev::kOut + 7]);
+    }
+  for (const BuildJob& b : S.builds) sums.push_back(static_cast<double>(b.pairs->P));
+  if (coll.fn(coll.user, sums.data(), static_cast<int32_t>(sums.size()), maxes.data(),
+              static_cast<int32_t>(maxes.size())) != 0)
+    throw Error(KREG_CUDA_ERROR, "collective callback failed");
+  size_t a = 0, b = 0;
+  for (EvalJob& e : S.evals)
+    for (int m = 0; m < e.M; ++m) {
+      for (int k = 0; k < 7; ++k) e.out[m * kreg_dev::kOut + k] = sums[a++];
+      e.out[m * kreg_dev::kOut + 7] = maxes[b++];
+    }
+  for (BuildJob& bj : S.builds) bj.pairs->P = static_cast<long long>(sums[a++]);
+}
+
+void register_many(kreg_ctx* ctx, std::vector<RegJob>& jobs, const Collective* coll) {
   const int k_first = std::max(1, std::min(8, env_int("KREG_K_FIRST", 2)));
   const bool fail_grad = env_int("KREG_FAIL_GRAD", 0) != 0;
   std::vector<std::unique_ptr<Reg>> regs;
@@ -473,11 +495,17 @@ void register_many(kreg_ctx* ctx, std::vector<RegJob>& jobs) {
     r->wp = j.params;
     const double diam = j.X->diam;
     r->v_scale = diam > 0.0 ? diam : 1.0;
-    r->denom = std::sqrt(static_cast<double>(std::max(j.X->n, 1)) * static_cast<double>(std::max(j.Z->n, 1)));
+    const long long nz = j.n_z_total > 0 ? j.n_z_total : j.Z->n;
+    r->denom = std::sqrt(static_cast<double>(std::max(j.X->n, 1)) * static_cast<double>(std::max(nz, 1LL)));
     r->lengthscale = j.cfg.init_lengthscale;
     r->wp.lengthscale = r->lengthscale;
     std::memcpy(r->T, j.initial, sizeof(r->T));
     for (double& d : r->dir) d = 0.0;
+    if (j.n_z_total > 0 && j.Z->n == 0) {
+      j.status = KREG_INVALID_ARGUMENT;  // a rank without rows would leave the lockstep
+      j.error = "register_clouds_rows: every rank needs at least one source row";
+      continue;
+    }
     if (j.X->n == 0 || j.Z->n == 0) {
       // empty cloud: build_pairs yields an empty list -> NoOverlapError
       char msg[160];
@@ -516,6 +544,7 @@ void register_many(kreg_ctx* ctx, std::vector<RegJob>& jobs) {
     const auto t0 = clk::now();
     if (G.pending) {
       end_round(ctx, *G.slot);
+      if (coll && coll->fn) reduce_round(*G.slot, *coll);
       G.pending = false;
       const auto t1 = clk::now();
       Reg* last = nullptr;

@@ -16,12 +16,15 @@ struct RegJob {
   kreg_registration_config cfg;
   kreg_registration_result* out = nullptr;
   long long expected_pairs = 0;   // optional capacity hint
+  long long n_z_total = 0;        // row sharding: size of the whole source (0: Z->n)
   kreg_status status = KREG_OK;
   std::string error;
 };
 
 // Runs all jobs to completion; per-job errors land in job.status / job.error.
-void register_many(kreg_ctx* ctx, std::vector<RegJob>& jobs);
+// With a collective, every round's results are summed / maxed across ranks
+// before the state machines consume them.
+void register_many(kreg_ctx* ctx, std::vector<RegJob>& jobs, const Collective* coll = nullptr);
 
 // registration.cpp:36-52
 double anneal_step(double lengthscale, const double* hist, int n, const kreg_registration_config& c);

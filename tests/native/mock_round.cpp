@@ -84,9 +84,23 @@ void end_round(kreg_ctx*, RoundSlot& S) { S.in_flight = false; }
 }  // namespace kreg_host
 
 // registers once through the product solver with the oracle standing in for the device
+extern "C" int mock_register_rows(const kreg_cloud_view* X, const kreg_cloud_view* Z, const double initial[12],
+                                  const kreg_kernel_params* params, const kreg_registration_config* config,
+                                  kreg_registration_result* result, int k_first, long long n_z_total,
+                                  kreg_collective_fn fn, void* user);
+
 extern "C" int mock_register(const kreg_cloud_view* X, const kreg_cloud_view* Z, const double initial[12],
                              const kreg_kernel_params* params, const kreg_registration_config* config,
                              kreg_registration_result* result, int k_first) {
+  return mock_register_rows(X, Z, initial, params, config, result, k_first, 0, nullptr, nullptr);
+}
+
+// registers this rank's source rows Z through the product solver (oracle as
+// the device); per-round results are combined through `fn` (row sharding)
+extern "C" int mock_register_rows(const kreg_cloud_view* X, const kreg_cloud_view* Z, const double initial[12],
+                                  const kreg_kernel_params* params, const kreg_registration_config* config,
+                                  kreg_registration_result* result, int k_first, long long n_z_total,
+                                  kreg_collective_fn fn, void* user) {
   kreg_cloud cx, cz;
   cx.n = X->n;
   cz.n = Z->n;
@@ -103,8 +117,12 @@ extern "C" int mock_register(const kreg_cloud_view* X, const kreg_cloud_view* Z,
   for (int k = 0; k < params->n_channels; ++k) j.params.per_channel.push_back(params->per_channel[k]);
   j.cfg = *config;
   j.out = result;
+  j.n_z_total = n_z_total;
   setenv("KREG_K_FIRST", std::to_string(k_first).c_str(), 1);
-  kreg_host::register_many(nullptr, jobs);
+  kreg_host::Collective coll;
+  coll.fn = fn;
+  coll.user = user;
+  kreg_host::register_many(nullptr, jobs, fn ? &coll : nullptr);
   for (auto& kv : g_pairs) ko_pairs_destroy(kv.second);
   g_pairs.clear();
   g_views.clear();

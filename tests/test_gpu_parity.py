@@ -381,3 +381,40 @@ def test_sequence_fallback_and_chains(ctx):
     # chain 0 covers pairs (0,1),(1,2): identical to the single-chain run
     for k in range(2):
         assert np.array_equal(one.relative[k].as12(), two.relative[k].as12())
+
+    # distributed chains (parallel.py): each "rank" runs its span block; the
+    # assembled result equals the single-process chained run
+    from paper_2012_03683_b200 import parallel
+    spans = parallel.chain_spans(len(frames), 2)
+    parts = []
+    for r in range(2):
+        mine = parallel.rank_spans(spans, r, 2)
+        res = api.register_sequence_spans(frames, mine, p, c2)
+        parts.append([(q, res.relative[q].as12().tolist(), int(res.fallback[q]), int(res.converged[q]),
+                       float(res.final_indicator[q]), int(res.iterations[q])) for b, e in mine for q in range(b, e)])
+        untouched = [q for q in range(len(frames) - 1) if not any(b <= q < e for b, e in mine)]
+        assert all(np.array_equal(res.relative[q].as12(), Isometry().as12()) for q in untouched)
+    merged = parallel.assemble_sequence(len(frames), parts)
+    for k in range(len(frames) - 1):
+        assert np.array_equal(merged.relative[k].as12(), two.relative[k].as12())
+        assert np.allclose(merged.trajectory[k + 1].as12(), two.trajectory[k + 1].as12(), atol=1e-12)
+    assert list(merged.iterations) == list(two.iterations)
+
+
+def test_row_sharded_entry_point_single_rank(ctx):
+    """kreg_register_clouds_rows with all rows and no collective is
+    register_clouds (C4 row sharding degenerates to one rank)."""
+    X, Z, Ts = synth.kitti_pair(23, 6000)
+    p, cfg = synth.kitti_params(), synth.kitti_subsequent_config()
+    init = synth.perturbed(Ts, 4)
+    a = api.register_clouds(X, Z, init, p, cfg)
+    b = api.register_clouds_rows(X, Z, Z.size(), init, p, cfg)
+    assert np.array_equal(a.transform.as12(), b.transform.as12())
+    assert np.array_equal(a.objective_trace, b.objective_trace)
+    # a half-row share with the full denominator: indicator uses sqrt(|X| |Z|)
+    from paper_2012_03683_b200 import parallel
+    half = parallel.shard_rows(Z, 0, 2)
+    c = api.register_clouds_rows(X, half, Z.size(), init, p, cfg)
+    assert c.indicator_trace[0] == pytest.approx(c.objective_trace[0] / math.sqrt(X.size() * Z.size()), rel=1e-12)
+    with pytest.raises(ValueError):
+        api.register_clouds_rows(X, Z, Z.size() - 1, init, p, cfg)
