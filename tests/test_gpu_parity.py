@@ -362,6 +362,13 @@ def test_kitti_registration_end_to_end_vs_reference(ctx, ref):
     err = compose(inverse(g.transform), r.transform)
     assert rotation_angle(err) <= 1e-3 and translation_norm(err) <= 1e-3, (rotation_angle(err), translation_norm(err))
     assert g.converged == r.converged
+    # decision-level parity on this pair: the same iterations, annealing
+    # levels, accepted steps and rebuilds as the reference loop, F within 1e-6
+    assert g.iterations == r.iterations
+    assert np.array_equal(g.lengthscale_trace, r.lengthscale_trace)
+    assert np.array_equal(g.step_trace, r.step_trace)
+    assert np.array_equal(g.rebuild_trace, r.rebuild_trace)
+    assert np.allclose(g.objective_trace, r.objective_trace, rtol=1e-6, atol=0)
 
 
 def test_sequence_fallback_and_chains(ctx):
