@@ -280,8 +280,22 @@ def main():
     hbm = float(peaks.get("hbm_gbs", HBM_PEAK_FALLBACK))
     pairs_bytes = sweep["pairs_streamed"] * 8.0
     achieved = pairs_bytes / (sweep["sweep_ms"] * 1e-3) / 1e9 if sweep["sweep_ms"] > 0 else 0.0
+    # DRAM traffic per sweep launch from the committed ncu --set full capture
+    # (profiles/r01_sweep_traffic.json), scaled to this run's algorithmic bytes
+    # per launch by the measured traffic / algorithmic ratio
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_sweep_traffic.json")) as f:
+            tr = json.load(f)
+        if sweep["sweep_rounds"]:
+            traffic = tr["traffic_over_algorithmic"] * pairs_bytes / sweep["sweep_rounds"]
+    except Exception:
+        tr = None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm, "traffic": None,
+                "frac": achieved / hbm, "traffic": traffic,
+                "traffic_source": ("profiles/r01_sweep_traffic.json: dram__bytes_read+write per k_sweep launch = "
+                                   f"{tr['traffic_over_algorithmic']:.2f} x algorithmic bytes" if tr else None),
+                "algorithmic_bytes_per_launch": pairs_bytes / sweep["sweep_rounds"] if sweep["sweep_rounds"] else None,
                 "kernel": "k_sweep (fused F + SE(3) gradient + displacement)",
                 "algorithmic_bytes_per_pair": 8,
                 "pair_evals_per_s": sweep["pair_evals"] / (sweep["sweep_ms"] * 1e-3) if sweep["sweep_ms"] else 0.0,

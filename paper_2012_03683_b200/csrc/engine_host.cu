@@ -3,6 +3,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <sstream>
@@ -691,13 +693,21 @@ void end_round(kreg_ctx* ctx, RoundSlot& S) {
     end_round(ctx, S);
     return;
   }
+  long long round_pairs = 0, round_slots = 0;
   for (int e = 0; e < ne; ++e) {
     std::memcpy(evals[e].out, res + static_cast<size_t>(e) * kreg_dev::kMaxCandidates * kreg_dev::kOut,
                 sizeof(double) * kreg_dev::kOut * evals[e].M);
     ctx->pair_evals += evals[e].pairs->P * evals[e].M;
-    ctx->pairs_streamed += evals[e].pairs->P;
-    ctx->slots_streamed += evals[e].pairs->slots;
+    round_pairs += evals[e].pairs->P;
+    round_slots += evals[e].pairs->slots;
   }
+  ctx->pairs_streamed += round_pairs;
+  ctx->slots_streamed += round_slots;
+  static const bool trace = std::getenv("KREG_TRACE_ROUNDS") != nullptr;
+  if (trace && ne)  // diagnostic: match profiled sweep launches to their pair / slot counts
+    std::fprintf(stderr, "kreg-round sweeps=%lld requests=%d launches=%d pairs=%lld slots=%lld\n",
+                 ctx->sweep_launches, ne, (ne + kreg_dev::kMaxSweepReqs - 1) / kreg_dev::kMaxSweepReqs, round_pairs,
+                 round_slots);
   if (ne) {
     ctx->sweep_launches += 1;
     if (ctx->profiling) {

@@ -774,6 +774,10 @@ struct WarpQueue {
   int first;         // next stage is the first of chunk pc
 };
 
+// Per-warp queues in static shared memory at file scope, so every access
+// compiles to LDS/STS (a pointer kept in SweepWarp would be generic).
+__shared__ WarpQueue g_wq[kSweepWarps];
+
 // Everything a sweep warp needs across work items.
 struct SweepWarp {
   const SweepReq* reqs;
@@ -785,7 +789,6 @@ struct SweepWarp {
   int4* ring;
   ChunkRec* recs;
   unsigned long long* bars;
-  WarpQueue* Q;
   float* tc;         // transform coefficients of the current chunk (shared)
   int lane;
   unsigned consumed, rec_used;
@@ -805,7 +808,7 @@ __device__ __forceinline__ int locate_item(const SweepWarp& w, int g) {
 
 // lane 0: issue the next stage (grabbing items as needed); false if none
 __device__ __forceinline__ bool produce(SweepWarp& w) {
-  WarpQueue& Q = *w.Q;
+  WarpQueue& Q = g_wq[threadIdx.x >> 5];
   while (Q.pu >= Q.pend) {
     if (Q.done || Q.tail - Q.head >= kQueueDepth) return false;
     const int g = (int)atomicAdd(&w.ctl->next_item, 1u);
@@ -1073,7 +1076,6 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(const SweepReq* reqs
   __shared__ int cbase[kMaxSweepReqs + 1];
   __shared__ int units_s[kMaxSweepReqs];
   __shared__ float tco[kSweepWarps][96];  // per warp: Td (and Ta) of its current chunk
-  __shared__ WarpQueue wq[kSweepWarps];
   extern __shared__ __align__(128) unsigned char dyn_smem[];
   SweepWarp w;
   w.reqs = reqs;
@@ -1087,7 +1089,6 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(const SweepReq* reqs
   w.bars = reinterpret_cast<unsigned long long*>(dyn_smem + (size_t)kSweepWarps * kSweepStages * kStageSlots * sizeof(int4) +
                                                  (size_t)kSweepWarps * kRecSlots * sizeof(ChunkRec)) +
            wid * kSweepStages;
-  w.Q = &wq[wid];
   w.tc = tco[wid];
   w.lane = lane;
   w.consumed = w.rec_used = 0;
@@ -1109,7 +1110,7 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(const SweepReq* reqs
   }
   if (lane < kSweepStages) mbar_init(&w.bars[lane], 1);
   if (lane == 0) {
-    WarpQueue& q = wq[wid];
+    WarpQueue& q = g_wq[wid];
     q.head = q.tail = 0;
     q.done = 0;
     q.pr = q.pc = 0;
@@ -1129,8 +1130,9 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(const SweepReq* reqs
     // next item of this warp (queued in order by lane 0)
     int g = -1;
     if (lane == 0) {
-      if (w.Q->head == w.Q->tail) produce(w);  // grabs the next item (items without stages issue none)
-      if (w.Q->head != w.Q->tail) g = w.Q->ids[w.Q->head % kQueueDepth];
+      WarpQueue& Q = g_wq[wid];
+      if (Q.head == Q.tail) produce(w);  // grabs the next item (items without stages issue none)
+      if (Q.head != Q.tail) g = Q.ids[Q.head % kQueueDepth];
     }
     g = __shfl_sync(0xffffffffu, g, 0);
     if (g < 0) break;
@@ -1144,7 +1146,7 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(const SweepReq* reqs
     else if (R.grad) chunk_body<NPG, true>(w, R, r, c, C, n_items);
     else chunk_body<4, false>(w, R, r, c, C, n_items);
     __syncwarp();
-    if (lane == 0) ++w.Q->head;
+    if (lane == 0) ++g_wq[wid].head;
     __syncwarp();
   }
   // the last CTA to exit resets the launch's item counter
