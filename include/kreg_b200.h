@@ -244,6 +244,14 @@ kreg_status kreg_evaluate_alignment(kreg_ctx* ctx, const kreg_pairs* pairs, cons
 kreg_status kreg_indicator(kreg_ctx* ctx, const kreg_cloud* X, const kreg_cloud* Z,
                            const double T[12], const kreg_kernel_params* params,
                            double cutoff_multiplier, double c_min, double* value);
+/* reference inner_product.cpp:203-236 exact_cosine: dense all-pairs cosine
+ * <f_X, f_TZ> / (||f_X|| ||f_Z||) in FP64 on the device (K4, dense.cu);
+ * parts (optional) = {cross, ||f_X||^2, ||f_Z||^2}. std::invalid_argument
+ * cases map to KREG_INVALID_ARGUMENT (empty clouds, zero-norm functions,
+ * schema / params mismatch). Feature rows up to 32 values. */
+kreg_status kreg_exact_cosine(kreg_ctx* ctx, const kreg_cloud_view* X, const kreg_cloud_view* Z,
+                              const double T[12], const kreg_kernel_params* params, double* cosine,
+                              double parts[3]);
 /* reference inner_product.hpp:86 max_point_displacement. */
 kreg_status kreg_max_point_displacement(kreg_ctx* ctx, const kreg_cloud* Z, const double built[12],
                                         const double now[12], double* value);

@@ -94,6 +94,7 @@ def lib():
                                                    CP, C.POINTER(_abi.kreg_sequence_result)]
         L.kreg_register_clouds_rows.argtypes = [P, P, P, C.c_int64, _abi.dptr, KP, CP, RP]
         L.kreg_ctx_set_collective.argtypes = [P, COLLECTIVE_FN, VP_]
+        L.kreg_exact_cosine.argtypes = [P, VP, VP, _abi.dptr, KP, _abi.dptr, _abi.dptr]
         L.kreg_se3_exp.argtypes = [_abi.dptr, _abi.dptr]
         L.kreg_se3_compose.argtypes = [_abi.dptr, _abi.dptr, _abi.dptr]
         L.kreg_se3_inverse.argtypes = [_abi.dptr, _abi.dptr]
@@ -484,6 +485,18 @@ def register_clouds_rows(X, Z_rows, n_z_total: int, initial, params: KernelParam
     finally:
         lib().kreg_ctx_set_collective(ctx.h, COLLECTIVE_FN(), None)
     return RegistrationResult.from_buffers(buf)
+
+
+def exact_cosine(X: PointCloud, Z: PointCloud, T, params: KernelParams, ctx=None, parts: bool = False):
+    """reference inner_product.cpp:203-236: dense all-pairs cosine between f_X
+    and f_TZ, FP64 on the device (K4). parts=True also returns (cross,
+    |f_X|^2, |f_Z|^2)."""
+    ctx = ctx or default_context()
+    t, tp = _t12(T)
+    out = np.zeros(1)
+    pr = np.zeros(3)
+    _check(lib().kreg_exact_cosine(ctx.h, X.view(), Z.view(), tp, params.cstruct(), _abi.as_ptr(out), _abi.as_ptr(pr)))
+    return (float(out[0]), tuple(pr)) if parts else float(out[0])
 
 
 def se3_exp(xi) -> Isometry:

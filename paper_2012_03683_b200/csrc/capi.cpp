@@ -662,6 +662,104 @@ kreg_status kreg_register_sequence_spans(kreg_ctx* ctx, const kreg_cloud* const*
   });
 }
 
+kreg_status kreg_exact_cosine(kreg_ctx* ctx, const kreg_cloud_view* X, const kreg_cloud_view* Z, const double T[12],
+                              const kreg_kernel_params* params, double* cosine, double parts[3]) {
+  return guarded([&] {
+    // inner_product.cpp:203-236
+    require(ctx && X && Z && T && params && cosine, "NULL argument");
+    std::unique_ptr<kreg_cloud> cx(cloud_describe(ctx, X)), cz(cloud_describe(ctx, Z));
+    check_same_schema(cx.get(), cz.get(), "");
+    const Params p = to_params(params);
+    check_kernel_params(p, cx.get());
+    if (X->n == 0 || Z->n == 0) throw Error(KREG_INVALID_ARGUMENT, "exact_cosine: clouds must be non-empty");
+    const int D = X->dim;
+    if (D > kreg_dev::kMaxDenseDim)
+      throw Error(KREG_INVALID_ARGUMENT, "exact_cosine: feature rows longer than 32 are not supported");
+    KREG_CUDA(cudaSetDevice(ctx->device));
+    // Z transformed on the host in FP64 exactly as apply(T, p) (se3.cpp:129-131)
+    std::vector<double> tz(static_cast<size_t>(Z->n) * 3);
+    for (int j = 0; j < Z->n; ++j) {
+      const double* q = Z->xyz + 3 * j;
+      for (int r = 0; r < 3; ++r)
+        tz[3 * j + r] = T[4 * r] * q[0] + T[4 * r + 1] * q[1] + T[4 * r + 2] * q[2] + T[4 * r + 3];
+    }
+    const size_t nx = static_cast<size_t>(X->n), nz = static_cast<size_t>(Z->n);
+    kreg_host::DevBuf<double> dx, dz, dtz, dfx, dfz, part;
+    kreg_host::DevBuf<kreg_dev::DenseReq> dreq;
+    dx.ensure(3 * nx, false, 1.0);
+    dz.ensure(3 * nz, false, 1.0);
+    dtz.ensure(3 * nz, false, 1.0);
+    dfx.ensure(nx * D + 1, false, 1.0);
+    dfz.ensure(nz * D + 1, false, 1.0);
+    KREG_CUDA(cudaMemcpyAsync(dx.ptr, X->xyz, sizeof(double) * 3 * nx, cudaMemcpyHostToDevice, ctx->stream));
+    KREG_CUDA(cudaMemcpyAsync(dz.ptr, Z->xyz, sizeof(double) * 3 * nz, cudaMemcpyHostToDevice, ctx->stream));
+    KREG_CUDA(cudaMemcpyAsync(dtz.ptr, tz.data(), sizeof(double) * 3 * nz, cudaMemcpyHostToDevice, ctx->stream));
+    if (D) {
+      KREG_CUDA(cudaMemcpyAsync(dfx.ptr, X->features, sizeof(double) * nx * D, cudaMemcpyHostToDevice, ctx->stream));
+      KREG_CUDA(cudaMemcpyAsync(dfz.ptr, Z->features, sizeof(double) * nz * D, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    const int b_chunks = 8;
+    const int nb_a = kreg_dev::dense_blocks_a(static_cast<int>(std::max(nx, nz)));
+    const size_t per = static_cast<size_t>(nb_a) * b_chunks;
+    part.ensure(3 * per, false, 1.0);
+    kreg_dev::DenseReq h[3];
+    std::memset(h, 0, sizeof(h));
+    const double* apos[3] = {dx.ptr, dx.ptr, dz.ptr};
+    const double* bpos[3] = {dtz.ptr, dx.ptr, dz.ptr};
+    const double* afe[3] = {dfx.ptr, dfx.ptr, dfz.ptr};
+    const double* bfe[3] = {dfz.ptr, dfx.ptr, dfz.ptr};
+    const int na[3] = {X->n, X->n, Z->n}, nb[3] = {Z->n, X->n, Z->n};
+    double pref = p.sigma * p.sigma;
+    int off = 0;
+    for (size_t k = 0; k < p.per_channel.size(); ++k) {
+      const kreg_channel_params& cp = p.per_channel[k];
+      if (cp.form != KREG_FORM_LINEAR) pref *= cp.sigma * cp.sigma;
+    }
+    for (int r = 0; r < 3; ++r) {
+      h[r].a = apos[r];
+      h[r].b = bpos[r];
+      h[r].af = afe[r];
+      h[r].bf = bfe[r];
+      h[r].n_a = na[r];
+      h[r].n_b = nb[r];
+      h[r].D = D;
+      h[r].n_channels = static_cast<int>(p.per_channel.size());
+      off = 0;
+      for (int k = 0; k < h[r].n_channels; ++k) {
+        const kreg_channel_params& cp = p.per_channel[static_cast<size_t>(k)];
+        h[r].ch[k].offset = off;
+        h[r].ch[k].dim = cx->schema[static_cast<size_t>(k)].dim;
+        h[r].ch[k].linear = cp.form == KREG_FORM_LINEAR ? 1 : 0;
+        h[r].ch[k].neg_inv_2l2 = cp.form == KREG_FORM_LINEAR ? 0.0 : -1.0 / (2.0 * cp.lengthscale * cp.lengthscale);
+        off += h[r].ch[k].dim;
+      }
+      h[r].neg_inv_2l2 = -1.0 / (2.0 * p.lengthscale * p.lengthscale);
+      h[r].pref = pref;
+      h[r].partials = part.ptr + r * per;
+    }
+    dreq.ensure(3, false, 1.0);
+    KREG_CUDA(cudaMemcpyAsync(dreq.ptr, h, sizeof(h), cudaMemcpyHostToDevice, ctx->stream));
+    kreg_dev::dense_sums(h, dreq.ptr, 3, b_chunks, ctx->stream);
+    KREG_CUDA(cudaGetLastError());
+    std::vector<double> hp(3 * per);
+    KREG_CUDA(cudaMemcpyAsync(hp.data(), part.ptr, sizeof(double) * 3 * per, cudaMemcpyDeviceToHost, ctx->stream));
+    KREG_CUDA(cudaStreamSynchronize(ctx->stream));
+    double s[3];
+    for (int r = 0; r < 3; ++r) {
+      double t = 0.0;
+      for (size_t k = 0; k < per; ++k) t += hp[r * per + k];  // fixed order
+      s[r] = t;
+    }
+    if (!(s[1] > 0.0) || !(s[2] > 0.0)) throw Error(KREG_INVALID_ARGUMENT, "exact_cosine: zero-norm cloud function");
+    *cosine = s[0] / std::sqrt(s[1] * s[2]);
+    if (parts) {
+      parts[0] = s[0];
+      parts[1] = s[1];
+      parts[2] = s[2];
+    }
+  });
+}
+
 kreg_status kreg_se3_exp(const double xi[6], double out[12]) {
   return guarded([&] {
     if (!kreg_se3::exp(xi, out)) throw Error(KREG_INVALID_ARGUMENT, "exp: twist has non-finite components");

@@ -172,6 +172,27 @@ void sweep_batched(const SweepReq* h_reqs, const SweepReq* d_reqs, int n, int sm
 void displacement(const double* zx, const double* zy, const double* zz, int n, const double* d_T2,
                   unsigned long long* d_out, cudaStream_t stream);
 
+// K4 dense double sum over all pairs (a, b) of two clouds (dense.cu).
+constexpr int kMaxDenseDim = 32;
+struct DenseChannel {
+  int offset, dim, linear;
+  double neg_inv_2l2;  // SE: -1 / (2 l_k^2)
+};
+struct DenseReq {
+  const double* a;   // n_a x 3 positions
+  const double* af;  // n_a x D features
+  const double* b;   // n_b x 3 positions (already transformed)
+  const double* bf;  // n_b x D features
+  int n_a, n_b, D;
+  int n_channels;
+  DenseChannel ch[kMaxChannels];
+  double neg_inv_2l2;  // geometric -1 / (2 l^2)
+  double pref;         // sigma^2 x prod over SE channels sigma_k^2
+  double* partials;    // dense_blocks_a(max n_a) x b_chunks
+};
+void dense_sums(const DenseReq* h_reqs, const DenseReq* d_reqs, int n, int b_chunks, cudaStream_t stream);
+int dense_blocks_a(int n_a);
+
 void interleave_positions(const double* x, const double* y, const double* z, int n, double4* out, cudaStream_t stream);
 
 long long kernel_launch_count();

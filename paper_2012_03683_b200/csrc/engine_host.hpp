@@ -237,6 +237,8 @@ std::string describe_schema(const kreg_cloud* c);
 void check_config(const kreg_registration_config& c);
 
 kreg_cloud* cloud_create(kreg_ctx* ctx, const kreg_cloud_view* v);
+// Validation + metadata only (no device copies).
+kreg_cloud* cloud_describe(kreg_ctx* ctx, const kreg_cloud_view* v);
 // Many clouds: host staging on worker threads, device copies into a context
 // arena (valid until the next call of this function on the context).
 std::vector<std::unique_ptr<kreg_cloud>> cloud_create_many(kreg_ctx* ctx, const kreg_cloud_view* const* views,

@@ -425,3 +425,36 @@ def test_row_sharded_entry_point_single_rank(ctx):
     assert c.indicator_trace[0] == pytest.approx(c.objective_trace[0] / math.sqrt(X.size() * Z.size()), rel=1e-12)
     with pytest.raises(ValueError):
         api.register_clouds_rows(X, Z, Z.size() - 1, init, p, cfg)
+
+
+# -------------------------------------------- K4 dense exact cosine
+def test_exact_cosine_reference_cases(ctx, ref):
+    # test_inner_product.cpp:314-350 on the device
+    C_ = synth.random_labeled_cloud(71, 60, 1.0, True, 3)
+    p = synth.params_for(C_, 0.3, 0.3)
+    assert api.exact_cosine(C_, C_, Isometry(), p) == pytest.approx(1.0, abs=1e-14)
+    a, b = PointCloud([[0.0, 0.0, 0.0]]), PointCloud([[0.5, 0.0, 0.0]])
+    assert api.exact_cosine(a, b, Isometry(), KernelParams(lengthscale=0.5)) == pytest.approx(0.6065306597126334,
+                                                                                            rel=1e-12)
+    X = synth.random_labeled_cloud(81, 100, 1.0, True, 3)
+    Z = synth.random_labeled_cloud(82, 100, 1.0, True, 3)
+    T = synth.random_isometry(synth.SplitMix64(83), 0.3, 0.2)
+    p = synth.params_for(X, 0.25, 0.3)
+    assert api.exact_cosine(X, Z, T, p) == pytest.approx(ref.exact_cosine(X, Z, T, p), rel=1e-12)
+    schema = FeatureSchema([Channel("sem", 2, ChannelKind.semantic)])
+    zero = PointCloud([[0.0, 0.0, 0.0]], schema, np.zeros((1, 2)))
+    with pytest.raises(ValueError):
+        api.exact_cosine(zero, zero, Isometry(), KernelParams(lengthscale=0.5,
+                                                              per_channel=[ChannelParams(1.0, 1.0, KernelForm.linear)]))
+    with pytest.raises(ValueError):
+        api.exact_cosine(PointCloud(np.zeros((0, 3))), a, Isometry(), KernelParams())
+
+
+def test_exact_cosine_kitti_vs_reference(ctx, ref):
+    X, Z, Ts = synth.kitti_pair(9, 3000)
+    p = synth.kitti_params()
+    for T in (Ts, synth.perturbed(Ts, 2, 0.05, 0.2)):
+        got, parts = api.exact_cosine(X, Z, T, p, parts=True)
+        want = ref.exact_cosine(X, Z, T, p)
+        assert got == pytest.approx(want, rel=1e-12)
+        assert 0.0 < got < 1.0 and all(v > 0 for v in parts)
