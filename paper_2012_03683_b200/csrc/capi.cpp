@@ -265,6 +265,7 @@ kreg_status kreg_ctx_host_stats(const kreg_ctx* ctx, double out[8]) {
     out[5] = ctx->t_total;
     out[6] = static_cast<double>(g_device_allocs);
     out[7] = g_device_alloc_seconds;
+    if (ctx->t_stage > 0.0) out[4] = ctx->t_stage;  // end-to-end runs: host staging replaces sweep prep
   });
 }
 
@@ -302,6 +303,7 @@ kreg_status kreg_ctx_reset_stats(kreg_ctx* ctx) {
     ctx->rounds = 0;
     ctx->t_prepare = ctx->t_wait = ctx->t_total = 0.0;
     ctx->t_build_prep = ctx->t_sweep_prep = 0.0;
+    ctx->t_stage = ctx->t_upload_issue = 0.0;
     ctx->launches_base = kreg_dev::kernel_launch_count();
     ctx->full_builds = ctx->filter_builds = 0;
   });
@@ -607,11 +609,22 @@ kreg_status kreg_register_batch_host(kreg_ctx* ctx, int32_t n, const kreg_cloud_
       views.push_back(&X[k]);
       views.push_back(&Z[k]);
     }
-    std::vector<std::unique_ptr<kreg_cloud>> clouds = cloud_create_many(ctx, views.data(), 2 * n);
+    // clouds are staged and uploaded on worker threads while earlier
+    // registrations already run (job k starts once its copies are enqueued)
+    std::unique_ptr<AsyncUpload> up = cloud_upload_async(ctx, views.data(), n);
     std::vector<RegJob> jobs(static_cast<size_t>(n));
-    for (int k = 0; k < n; ++k)
-      make_jobs(clouds[2 * k].get(), clouds[2 * k + 1].get(), initials + 12 * k, params, config, &results[k], jobs[k]);
-    register_many(ctx, jobs);
+    for (int k = 0; k < n; ++k) {
+      make_jobs(up->clouds[2 * k].get(), up->clouds[2 * k + 1].get(), initials + 12 * k, params, config, &results[k],
+                jobs[k]);
+      jobs[k].ready = &up->ready[static_cast<size_t>(k)];
+    }
+    try {
+      register_many(ctx, jobs);
+    } catch (...) {
+      up.reset();  // join the workers before the clouds go away
+      throw;
+    }
+    up.reset();
     for (int k = 0; k < n; ++k) statuses[k] = jobs[k].status;
   });
 }

@@ -8,6 +8,7 @@
 #include <cstring>
 #include <numeric>
 #include <sstream>
+#include <mutex>
 #include <thread>
 
 #include "engine_host.hpp"
@@ -251,20 +252,21 @@ size_t cloud_stage_floats(const kreg_cloud* c) { return static_cast<size_t>(c->n
 // Device copies (async on the context stream) into dx/dy/dz/df, or into
 // buffers owned by the cloud when dx == nullptr.
 void cloud_upload(kreg_ctx* ctx, kreg_cloud* c, const double* sx, const double* sy, const double* sz, const float* sf,
-                  double* dx, double* dy, double* dz, float* df) {
+                  double* dx, double* dy, double* dz, float* df, double4* dw) {
   const int n = c->n;
   if (dx) {
     c->x.borrow(dx, n);
     c->y.borrow(dy, n);
     c->z.borrow(dz, n);
     c->feat.borrow(df, cloud_stage_floats(c));
+    c->xw.borrow(dw, static_cast<size_t>(n) + 1);
   } else {
     c->x.ensure(n, false, 1.0);
     c->y.ensure(n, false, 1.0);
     c->z.ensure(n, false, 1.0);
     c->feat.ensure(cloud_stage_floats(c), false, 1.0);
+    c->xw.ensure(static_cast<size_t>(n) + 1, false, 1.0);
   }
-  c->xw.ensure(static_cast<size_t>(n) + 1, false, 1.0);
   if (n) {
     KREG_CUDA(cudaMemcpyAsync(c->x.ptr, sx, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
     KREG_CUDA(cudaMemcpyAsync(c->y.ptr, sy, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
@@ -283,7 +285,8 @@ kreg_cloud* cloud_create(kreg_ctx* ctx, const kreg_cloud_view* v) {
   std::vector<float> f(cloud_stage_floats(c.get()));
   const int n = c->n;
   cloud_stage(v, c.get(), h.data(), h.data() + n, h.data() + 2 * n, f.data());
-  cloud_upload(ctx, c.get(), h.data(), h.data() + n, h.data() + 2 * n, f.data(), nullptr, nullptr, nullptr, nullptr);
+  cloud_upload(ctx, c.get(), h.data(), h.data() + n, h.data() + 2 * n, f.data(), nullptr, nullptr, nullptr, nullptr,
+               nullptr);
   KREG_CUDA(cudaStreamSynchronize(ctx->stream));  // host staging vectors go out of scope
   return c.release();
 }
@@ -293,12 +296,16 @@ kreg_cloud* cloud_create(kreg_ctx* ctx, const kreg_cloud_view* v) {
 // context arena (no per-cloud allocation), all on the context stream.
 std::vector<std::unique_ptr<kreg_cloud>> cloud_create_many(kreg_ctx* ctx, const kreg_cloud_view* const* views,
                                                            int n) {
+  using clk = std::chrono::steady_clock;
+  const auto t_begin = clk::now();
   std::vector<std::unique_ptr<kreg_cloud>> out(static_cast<size_t>(n));
   for (int k = 0; k < n; ++k) out[k].reset(cloud_describe(ctx, views[k]));
-  std::vector<size_t> doff(static_cast<size_t>(n) + 1, 0), foff(static_cast<size_t>(n) + 1, 0);
+  std::vector<size_t> doff(static_cast<size_t>(n) + 1, 0), foff(static_cast<size_t>(n) + 1, 0),
+      woff(static_cast<size_t>(n) + 1, 0);
   for (int k = 0; k < n; ++k) {
     doff[k + 1] = doff[k] + (cloud_stage_doubles(out[k].get()) + 1) / 2 * 2;  // 16-B aligned slices
     foff[k + 1] = foff[k] + (cloud_stage_floats(out[k].get()) + 3) / 4 * 4;
+    woff[k + 1] = woff[k] + static_cast<size_t>(out[k]->n) + 1;
   }
   KREG_CUDA(cudaSetDevice(ctx->device));
   KREG_CUDA(cudaStreamSynchronize(ctx->stream));  // staging / arena may still be in use
@@ -306,6 +313,7 @@ std::vector<std::unique_ptr<kreg_cloud>> cloud_create_many(kreg_ctx* ctx, const 
   ctx->stage_f.ensure(foff[n] + 4);
   ctx->arena_d.ensure(doff[n] + 2, false, 1.25);
   ctx->arena_f.ensure(foff[n] + 4, false, 1.25);
+  ctx->arena_w.ensure(woff[n] + 1, false, 1.25);
   const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
   const int workers = static_cast<int>(std::min<unsigned>(std::min<unsigned>(hw, 32u), static_cast<unsigned>(n)));
   std::vector<std::exception_ptr> err(static_cast<size_t>(std::max(workers, 1)));
@@ -326,14 +334,82 @@ std::vector<std::unique_ptr<kreg_cloud>> cloud_create_many(kreg_ctx* ctx, const 
   for (auto& t : pool) t.join();
   for (auto& e : err)
     if (e) std::rethrow_exception(e);
+  const auto t_staged = clk::now();
   for (int k = 0; k < n; ++k) {
     const int m = out[k]->n;
     const double* d = ctx->stage_d.ptr + doff[k];
     double* a = ctx->arena_d.ptr + doff[k];
     cloud_upload(ctx, out[k].get(), d, d + m, d + 2 * m, ctx->stage_f.ptr + foff[k], a, a + m, a + 2 * m,
-                 ctx->arena_f.ptr + foff[k]);
+                 ctx->arena_f.ptr + foff[k], ctx->arena_w.ptr + woff[k]);
   }
+  ctx->t_stage += std::chrono::duration<double>(t_staged - t_begin).count();
+  ctx->t_upload_issue += std::chrono::duration<double>(clk::now() - t_staged).count();
   return out;
+}
+
+// Asynchronous variant for end-to-end batches: cloud pairs (2k, 2k + 1) are
+// staged and their copies enqueued on the context stream by worker threads in
+// job order; ready[k] turns 1 once job k's copies are enqueued (the solver
+// starts job k only then, so stream order puts the copies first).
+AsyncUpload::~AsyncUpload() {
+  for (auto& t : workers)
+    if (t.joinable()) t.join();
+}
+
+std::unique_ptr<AsyncUpload> cloud_upload_async(kreg_ctx* ctx, const kreg_cloud_view* const* views, int n_jobs) {
+  auto up = std::make_unique<AsyncUpload>();
+  const int n = 2 * n_jobs;
+  up->clouds.resize(static_cast<size_t>(n));
+  for (int k = 0; k < n; ++k) up->clouds[k].reset(cloud_describe(ctx, views[k]));
+  std::vector<size_t> doff(static_cast<size_t>(n) + 1, 0), foff(static_cast<size_t>(n) + 1, 0),
+      woff(static_cast<size_t>(n) + 1, 0);
+  for (int k = 0; k < n; ++k) {
+    doff[k + 1] = doff[k] + (cloud_stage_doubles(up->clouds[k].get()) + 1) / 2 * 2;
+    foff[k + 1] = foff[k] + (cloud_stage_floats(up->clouds[k].get()) + 3) / 4 * 4;
+    woff[k + 1] = woff[k] + static_cast<size_t>(up->clouds[k]->n) + 1;
+  }
+  KREG_CUDA(cudaSetDevice(ctx->device));
+  KREG_CUDA(cudaStreamSynchronize(ctx->stream));  // staging / arena may still be in use
+  ctx->stage_d.ensure(doff[n] + 2);
+  ctx->stage_f.ensure(foff[n] + 4);
+  ctx->arena_d.ensure(doff[n] + 2, false, 1.25);
+  ctx->arena_f.ensure(foff[n] + 4, false, 1.25);
+  ctx->arena_w.ensure(woff[n] + 1, false, 1.25);
+  up->ready = std::vector<std::atomic<int>>(static_cast<size_t>(n_jobs));
+  for (auto& r : up->ready) r.store(0);
+  const unsigned hw = std::max(2u, std::thread::hardware_concurrency());
+  const int workers = static_cast<int>(std::min<unsigned>(std::min<unsigned>(hw - 1, 31u), static_cast<unsigned>(n_jobs)));
+  auto next = std::make_shared<std::atomic<int>>(0);
+  AsyncUpload* U = up.get();
+  const int device = ctx->device;
+  auto work = [U, ctx, views, doff, foff, woff, next, n_jobs, device]() {
+    cudaSetDevice(device);
+    for (;;) {
+      const int job = next->fetch_add(1);
+      if (job >= n_jobs) return;
+      try {
+        for (int h = 0; h < 2; ++h) {
+          const int k = 2 * job + h;
+          kreg_cloud* c = U->clouds[k].get();
+          const int m = c->n;
+          double* d = ctx->stage_d.ptr + doff[k];
+          cloud_stage(views[k], c, d, d + m, d + 2 * m, ctx->stage_f.ptr + foff[k]);
+          double* a = ctx->arena_d.ptr + doff[k];
+          cloud_upload(ctx, c, d, d + m, d + 2 * m, ctx->stage_f.ptr + foff[k], a, a + m, a + 2 * m,
+                       ctx->arena_f.ptr + foff[k], ctx->arena_w.ptr + woff[k]);
+        }
+        U->ready[job].store(1, std::memory_order_release);
+      } catch (...) {
+        {
+          std::lock_guard<std::mutex> lk(U->mu);
+          if (!U->error) U->error = std::current_exception();
+        }
+        U->ready[job].store(-1, std::memory_order_release);
+      }
+    }
+  };
+  for (int w = 0; w < workers; ++w) up->workers.emplace_back(work);
+  return up;
 }
 
 // ------------------------------------------------------------ build setup
@@ -424,29 +500,14 @@ static void prepare_build(kreg_ctx* ctx, BuildJob& job, kreg_dev::BuildReq& R) {
     R.n_cells = g[0] * g[1] * g[2];
     p->n_cells = R.n_cells;
     p->gx = R.gx; p->gy = R.gy; p->gz = R.gz;
-    ctx->hw_cells = std::max(ctx->hw_cells, R.n_cells + 1);
-    p->cell_count.ensure(static_cast<size_t>(ctx->hw_cells), /*zero=*/true);
-    p->cell_start.ensure(static_cast<size_t>(ctx->hw_cells));
-    p->cell_of.ensure(nx + 1);
-    p->tmp_items.ensure(nx + 1);
-    p->cell_items.ensure(nx + 1);
-    p->cx.ensure(nx + 1);
-    p->cy.ensure(nx + 1);
-    p->cz.ensure(nx + 1);
-    p->scan_tiles.ensure(static_cast<size_t>(R.n_cells / kreg_dev::kScanTile + 4));
+    // grid buffers live in the round's arena (assign_grid_arena): they are
+    // only needed by this build's kernels
     const long long want = p->expected_sup > 0 ? p->expected_sup : static_cast<long long>(nz) * 256 + 4096;
     if (p->sup.cap < static_cast<size_t>(want)) {
       p->sup.ensure(static_cast<size_t>(std::max<long long>(want + want / 4, ctx->hw_sup)), false, 1.0);
       p->sup_i.ensure(p->sup.cap, false, 1.0);
       ctx->hw_sup = std::max<long long>(ctx->hw_sup, static_cast<long long>(p->sup.cap));
     }
-    R.cell_count = p->cell_count.ptr;
-    R.cell_start = p->cell_start.ptr;
-    R.cell_of = p->cell_of.ptr;
-    R.tmp_items = p->tmp_items.ptr;
-    R.cell_items = p->cell_items.ptr;
-    R.cx = p->cx.ptr; R.cy = p->cy.ptr; R.cz = p->cz.ptr;
-    R.scan_tiles = p->scan_tiles.ptr;
   } else {
     ++ctx->filter_builds;
     ++p->filter_builds;
@@ -546,6 +607,42 @@ static void prepare_sweep(EvalJob& job, kreg_dev::SweepReq& R, double* partials,
   R.disp_bits = disp_bits;
 }
 
+// Grid buffers of the round's grid searches, carved from one arena per round
+// slot (cell counts stay zero between rounds: k_scatter consumes them).
+static void assign_grid_arena(RoundSlot& S, kreg_dev::BuildReq* reqs, int nb) {
+  size_t cells = 0, pts = 0, tiles = 0;
+  for (int b = 0; b < nb; ++b) {
+    if (!reqs[b].full) continue;
+    cells += static_cast<size_t>(reqs[b].n_cells) + 2;
+    pts += static_cast<size_t>(reqs[b].n_x) + 2;
+    tiles += static_cast<size_t>(reqs[b].n_cells / kreg_dev::kScanTile) + 4;
+  }
+  if (!cells) return;
+  S.g_count.ensure(cells, /*zero=*/true, 1.5);
+  S.g_start.ensure(cells, false, 1.5);
+  S.g_int.ensure(3 * pts, false, 1.5);
+  S.g_pos.ensure(3 * pts, false, 1.5);
+  S.g_scan.ensure(tiles, false, 1.5);
+  size_t oc = 0, op = 0, ot = 0;
+  for (int b = 0; b < nb; ++b) {
+    kreg_dev::BuildReq& R = reqs[b];
+    if (!R.full) continue;
+    const size_t np = static_cast<size_t>(R.n_x) + 2;
+    R.cell_count = S.g_count.ptr + oc;
+    R.cell_start = S.g_start.ptr + oc;
+    R.cell_of = S.g_int.ptr + 3 * op;
+    R.tmp_items = R.cell_of + np;
+    R.cell_items = R.tmp_items + np;
+    R.cx = S.g_pos.ptr + 3 * op;
+    R.cy = R.cx + np;
+    R.cz = R.cy + np;
+    R.scan_tiles = S.g_scan.ptr + ot;
+    oc += static_cast<size_t>(R.n_cells) + 2;
+    op += np;
+    ot += static_cast<size_t>(R.n_cells / kreg_dev::kScanTile) + 4;
+  }
+}
+
 RoundSlot* round_slot(kreg_ctx* ctx, int i) {
   if (!ctx->rs[i]) {
     auto* S = new RoundSlot;
@@ -589,6 +686,7 @@ void begin_round(kreg_ctx* ctx, RoundSlot& S, std::vector<BuildJob>&& builds_in,
     S.h_build.ptr[b].status = S.d_results.ptr + static_cast<size_t>(ne) * kreg_dev::kMaxCandidates * kreg_dev::kOut +
                               kreg_dev::kBuildStatus * b;
   }
+  assign_grid_arena(S, S.h_build.ptr, nb);
   const auto tb = clk::now();
   ctx->t_build_prep += std::chrono::duration<double>(tb - t0).count();
   // F-only requests first (their chunks are the heaviest; see sweep_batched)

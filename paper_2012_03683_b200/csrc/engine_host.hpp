@@ -6,7 +6,13 @@
 #include <cuda_runtime.h>
 
 #include <chrono>
+#include <atomic>
 #include <cstdint>
+#include <exception>
+#include <mutex>
+#include <thread>
+#include <cstdio>
+#include <cstdlib>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -64,6 +70,8 @@ struct DevBuf {
     size_t want = n < 16 ? 16 : static_cast<size_t>(static_cast<double>(n) * slack);
     ++g_device_allocs;
     g_device_alloc_bytes += static_cast<long long>(want * sizeof(T));
+    static const bool trace = std::getenv("KREG_TRACE_ALLOC") != nullptr;
+    if (trace) std::fprintf(stderr, "kreg-alloc elem=%zu n=%zu old_cap=%zu\n", sizeof(T), want, cap);
     cudaError_t e = cudaMalloc(&ptr, want * sizeof(T));
     if (e != cudaSuccess) {
       cudaGetLastError();
@@ -140,6 +148,7 @@ struct kreg_ctx {
   kreg_host::PinnedBuf<float> stage_f;
   kreg_host::DevBuf<double> arena_d;
   kreg_host::DevBuf<float> arena_f;
+  kreg_host::DevBuf<double4> arena_w;
   // pair-list workspaces kept across registrations (device buffers keep capacity)
   std::vector<kreg_pairs*> pool;
   int max_active = 0;  // lockstep window of kreg_register_batch (0 = all at once)
@@ -147,13 +156,14 @@ struct kreg_ctx {
   double skin = 0.25;
   // capacity high-water marks over all workspaces: a pooled workspace that
   // must grow goes straight to the largest size any registration needed
-  long long hw_slots = 0, hw_sup = 0, hw_cells = 0;
+  long long hw_slots = 0, hw_sup = 0;
   long long full_builds = 0, filter_builds = 0;
   kreg_host::Collective collective;  // row-sharded registrations (kreg_ctx_set_collective)
   // host-side round accounting (seconds)
   long long rounds = 0;
   double t_prepare = 0.0, t_wait = 0.0, t_total = 0.0;
   double t_build_prep = 0.0, t_sweep_prep = 0.0;
+  double t_stage = 0.0, t_upload_issue = 0.0;  // end-to-end calls: host staging, copy issue
   ~kreg_ctx();
 };
 
@@ -189,9 +199,6 @@ struct kreg_pairs {
   // grid (candidate stage)
   long long n_cells = 0;
   int gx = 0, gy = 0, gz = 0;
-  kreg_host::DevBuf<int> cell_count, cell_start, cell_of, tmp_items, cell_items;
-  kreg_host::DevBuf<double> cx, cy, cz;
-  kreg_host::DevBuf<long long> scan_tiles;
   // candidate list: pairs within R_s = cutoff (1 + skin) of Ts z_j with c > c_min
   kreg_host::DevBuf<int4> sup;             // per tile: 32 rows of H_t entries {x_i - Ts z_j, log2 c}
   kreg_host::DevBuf<int> sup_i;            // their target indices
@@ -239,6 +246,18 @@ void check_config(const kreg_registration_config& c);
 kreg_cloud* cloud_create(kreg_ctx* ctx, const kreg_cloud_view* v);
 // Validation + metadata only (no device copies).
 kreg_cloud* cloud_describe(kreg_ctx* ctx, const kreg_cloud_view* v);
+// End-to-end batch: clouds (2k, 2k + 1) of job k staged and uploaded by
+// worker threads in job order while the solver runs (see ready).
+struct AsyncUpload {
+  std::vector<std::unique_ptr<kreg_cloud>> clouds;
+  std::vector<std::atomic<int>> ready;  // per job: 0 pending, 1 enqueued, -1 failed
+  std::vector<std::thread> workers;
+  std::mutex mu;
+  std::exception_ptr error;
+  ~AsyncUpload();
+};
+std::unique_ptr<AsyncUpload> cloud_upload_async(kreg_ctx* ctx, const kreg_cloud_view* const* views, int n_jobs);
+
 // Many clouds: host staging on worker threads, device copies into a context
 // arena (valid until the next call of this function on the context).
 std::vector<std::unique_ptr<kreg_cloud>> cloud_create_many(kreg_ctx* ctx, const kreg_cloud_view* const* views,
@@ -281,6 +300,12 @@ struct RoundSlot {
   DevBuf<double> part_arena;                // sweep chunk partials (one slice per request)
   DevBuf<unsigned int> counter_arena;       // sweep chunk counters, self-resetting
   DevBuf<unsigned long long> disp_arena;    // displacement maxima, self-resetting
+  // grid searches of the round: cell counts (zero between rounds), cell
+  // starts, per-point ints (cell_of, tmp_items, cell_items), cell-ordered
+  // positions, scan tiles
+  DevBuf<int> g_count, g_start, g_int;
+  DevBuf<double> g_pos;
+  DevBuf<long long> g_scan;
   cudaEvent_t done = nullptr, ev0 = nullptr, ev1 = nullptr;
   std::vector<BuildJob> builds;
   std::vector<EvalJob> evals;

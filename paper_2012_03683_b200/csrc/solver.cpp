@@ -25,6 +25,7 @@
 #include <cstdio>
 #include <cstring>
 #include <memory>
+#include <thread>
 #include <vector>
 
 #include "engine_host.hpp"
@@ -560,6 +561,17 @@ void register_many(kreg_ctx* ctx, std::vector<RegJob>& jobs, const Collective* c
       G.active.erase(std::remove_if(G.active.begin(), G.active.end(), [](Reg* r) { return r->phase == Phase::kDone; }),
                      G.active.end());
       while (G.active.size() < per_group && started < regs.size()) {
+        // end-to-end batches: start a job once its clouds' copies are enqueued
+        const std::atomic<int>* rd = regs[started]->job->ready;
+        if (rd) {
+          int v = rd->load(std::memory_order_acquire);
+          while (v == 0 && G.active.empty()) {  // nothing else to run: wait for the upload
+            std::this_thread::yield();
+            v = rd->load(std::memory_order_acquire);
+          }
+          if (v < 0) throw Error(KREG_CUDA_ERROR, "cloud upload failed");
+          if (v == 0) break;
+        }
         Reg* r = regs[started++].get();
         r->pairs.ctx = ctx;
         r->pairs.p = acquire_workspace(ctx);

@@ -17,6 +17,7 @@ struct RegJob {
   kreg_registration_result* out = nullptr;
   long long expected_pairs = 0;   // optional capacity hint
   long long n_z_total = 0;        // row sharding: size of the whole source (0: Z->n)
+  const std::atomic<int>* ready = nullptr;  // end-to-end: clouds enqueued (1), failed (-1); null = ready
   kreg_status status = KREG_OK;
   std::string error;
 };
