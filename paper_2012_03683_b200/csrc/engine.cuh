@@ -128,7 +128,8 @@ struct BuildReq {
   float4* zs;            // n_z: sources in degree-sorted order (FP32)
   ChunkRec* chunks;      // kMaxChunks sweep chunk records
   int4* slots;           // capacity slots {x_i - T_b z_j (3 x FP32), log2 c (FP32)}
-  int* slot_i;           // capacity: target index i of every slot (export / debug only)
+  int* slot_i;           // capacity: target index i of every slot (export only)
+  int write_index;       // emit also writes slot_i (export re-runs the emit with it set)
   long long capacity;
   unsigned long long* disp_blk;   // ceil(n_z / 8): per filter block max |T z - Ts z|^2 (bits)
   double* status;        // kBuildStatus: {P, slots > cap, slots, cand > cap, cand, |T-Ts| disp, invalid, -}
@@ -193,6 +194,8 @@ struct DenseReq {
 void dense_sums(const DenseReq* h_reqs, const DenseReq* d_reqs, int n, int b_chunks, cudaStream_t stream);
 int dense_blocks_a(int n_a);
 
+// Re-run a list's emit pass with write_index set (pairs_export).
+void filter_emit_index(const BuildReq* d_req, int n_z, cudaStream_t stream);
 void interleave_positions(const double* x, const double* y, const double* z, int n, double4* out, cudaStream_t stream);
 
 long long kernel_launch_count();

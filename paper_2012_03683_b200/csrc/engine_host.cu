@@ -687,6 +687,10 @@ void begin_round(kreg_ctx* ctx, RoundSlot& S, std::vector<BuildJob>&& builds_in,
                               kreg_dev::kBuildStatus * b;
   }
   assign_grid_arena(S, S.h_build.ptr, nb);
+  for (int b = 0; b < nb; ++b) {
+    builds[b].pairs->last_req = S.h_build.ptr[b];
+    builds[b].pairs->index_valid = false;
+  }
   const auto tb = clk::now();
   ctx->t_build_prep += std::chrono::duration<double>(tb - t0).count();
   // F-only requests first (their chunks are the heaviest; see sweep_batched)
@@ -840,9 +844,26 @@ double max_point_displacement_dev(kreg_ctx* ctx, const kreg_cloud* Z, const doub
   return std::sqrt(d2);
 }
 
-void pairs_export(kreg_ctx* ctx, const kreg_pairs* p, int64_t* offsets, int32_t* x_index, double* coeff) {
+void pairs_export(kreg_ctx* ctx, const kreg_pairs* pc, int64_t* offsets, int32_t* x_index, double* coeff) {
   // reference layout: CSR by ORIGINAL source index j, ascending ORIGINAL i
+  kreg_pairs* p = const_cast<kreg_pairs*>(pc);
   const int nz = p->Z ? p->Z->n : 0;
+  if (nz && p->slots && !p->index_valid) {
+    // builds skip the target indices; the emit is deterministic, so re-run it
+    // with write_index set on the unchanged candidate list
+    kreg_dev::BuildReq R = p->last_req;
+    R.write_index = 1;
+    DevBuf<kreg_dev::BuildReq> d;
+    d.ensure(1, false, 1.0);
+    DevBuf<double> status;
+    status.ensure(kreg_dev::kBuildStatus, false, 1.0);
+    R.status = status.ptr;
+    KREG_CUDA(cudaMemcpyAsync(d.ptr, &R, sizeof(R), cudaMemcpyHostToDevice, ctx->stream));
+    kreg_dev::filter_emit_index(d.ptr, nz, ctx->stream);
+    KREG_CUDA(cudaGetLastError());
+    KREG_CUDA(cudaStreamSynchronize(ctx->stream));
+    p->index_valid = true;
+  }
   std::vector<int> deg(static_cast<size_t>(nz) + 1, 0), pos(static_cast<size_t>(nz) + 1, 0);
   std::vector<long long> toff(static_cast<size_t>(p->n_tiles) + 1, 0);
   std::vector<int4> sl(static_cast<size_t>(p->slots));

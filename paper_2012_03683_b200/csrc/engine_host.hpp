@@ -228,6 +228,9 @@ struct kreg_pairs {
   bool counts_valid = false;               // P / slots known on the host
   double anchor[3] = {0, 0, 0};
   long long expected_pairs = 0;  // capacity hint
+  // the last build's request (pairs_export re-runs its emit to recover slot_i)
+  kreg_dev::BuildReq last_req{};
+  bool index_valid = false;
   // statistics
   long long full_builds = 0, filter_builds = 0;
 };

@@ -541,7 +541,7 @@ __global__ void __launch_bounds__(256) k_filter(const BuildReq* reqs) {
         // x_i - T_b z_j in FP32 (|.| <= cutoff): the sweep forms d = x_i - T z_j
         // as this minus the source's displacement (T - T_b) z_j
         R.slots[at] = make_int4(__float_as_int(dx), __float_as_int(dy), __float_as_int(dz), e.w);
-        R.slot_i[at] = R.sup_i[rb + k];
+        if (R.write_index) R.slot_i[at] = R.sup_i[rb + k];  // export only
       }
       cnt += __popc(m);
     }
@@ -554,7 +554,7 @@ __global__ void __launch_bounds__(256) k_filter(const BuildReq* reqs) {
     const int height = (R.unit_off[ts + 1] - R.unit_off[ts]) * kUnitSteps;
     for (int k = cnt + lane; k < height; k += 32) {
       R.slots[slot_index(out, col, k)] = make_int4(0, 0, 0, __float_as_int(-INFINITY));
-      R.slot_i[slot_index(out, col, k)] = -1;
+      if (R.write_index) R.slot_i[slot_index(out, col, k)] = -1;
     }
   }
 }
@@ -1263,6 +1263,11 @@ void sweep_batched(const SweepReq* h, const SweepReq* d, int n, int sm_count, un
 void displacement(const double* zx, const double* zy, const double* zz, int n, const double* d_T2,
                   unsigned long long* d_out, cudaStream_t st) {
   k_displacement<<<(n + 255) / 256, 256, 0, st>>>(zx, zy, zz, n, d_T2, d_out);
+  count_launch();
+}
+
+void filter_emit_index(const BuildReq* d, int n_z, cudaStream_t st) {
+  k_filter<true><<<dim3(max(1, (n_z + 7) / 8), 1), 256, 0, st>>>(d);
   count_launch();
 }
 
