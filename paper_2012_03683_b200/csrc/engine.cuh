@@ -35,8 +35,14 @@ constexpr int kSweepThreads = 256;  // threads per persistent sweep CTA (2 CTAs 
 constexpr int kUnitSteps = KREG_UNIT_STEPS;      // degree steps per sweep unit (x 32 lanes x 16 B)
 constexpr int kStageUnits = 4;                   // units per TMA stage (4 KB at 2 steps)
 constexpr int kSweepStages = KREG_SWEEP_STAGES;  // per-warp TMA ring depth (stages)
-constexpr int kMaxChunks = 1184;                 // chunks per request (8 x 148)
-constexpr int kMinChunkUnits = 8;                // >= 2 stages per chunk
+#ifndef KREG_MAX_CHUNKS
+#define KREG_MAX_CHUNKS 2048
+#endif
+constexpr int kMaxChunks = KREG_MAX_CHUNKS;      // chunks per request at most (64 groups of 32)
+#ifndef KREG_PREF_CHUNK_UNITS
+#define KREG_PREF_CHUNK_UNITS 48
+#endif
+constexpr int kPrefChunkUnits = KREG_PREF_CHUNK_UNITS;  // preferred chunk size (units)
 constexpr int kQueueDepth = 8;                   // chunks a warp may hold in its prefetch queue
 constexpr int kMaxSweepReqs = kSweepThreads;     // requests per sweep launch
 constexpr int kChunkGroup = 32;                  // chunk partials summed per group (first reduction level)

@@ -77,10 +77,13 @@ constexpr int kUnitSlots = 32 * kUnitSteps;  // slots per sweep work unit
 
 // Sweep chunks of a request with U units: chunk_count(U) chunks of
 // chunk_units(U) units (a function of the pair list only).
+// Chunks of kPrefChunkUnits units (per-chunk costs amortised over ~48 KB of
+// slots) unless the list needs more than kMaxChunks of them (C4-size lists
+// then use kMaxChunks larger chunks, keeping every warp busy).
 __host__ __device__ __forceinline__ long long chunk_units(long long U) {
   long long cu = (U + kMaxChunks - 1) / kMaxChunks;
-  cu = (cu + kStageUnits - 1) / kStageUnits * kStageUnits;
-  return cu < kMinChunkUnits ? kMinChunkUnits : cu;
+  if (cu < kPrefChunkUnits) cu = kPrefChunkUnits;
+  return (cu + kStageUnits - 1) / kStageUnits * kStageUnits;
 }
 __host__ __device__ __forceinline__ int chunk_count(long long U) {
   return U <= 0 ? 1 : (int)((U + chunk_units(U) - 1) / chunk_units(U));
@@ -661,6 +664,11 @@ constexpr size_t kSweepSmem = (size_t)kSweepWarps * kSweepStages * kStageSlots *
                               (size_t)kSweepWarps * kRecSlots * sizeof(ChunkRec) +
                               (size_t)kSweepWarps * kSweepStages * sizeof(unsigned long long);
 
+#ifndef KREG_STEP_UNROLL
+#define KREG_STEP_UNROLL 2
+#endif
+constexpr int kStepUnroll = KREG_STEP_UNROLL;
+
 // `units` sweep units (2 steps each) of one tile column (lane = source) for M
 // candidates: d = (x - T_b z) - delta, w = ex2(r^2 kappa + log2 c), W += w
 // and (GRAD) S += w d on FFMA2/FADD2/FMUL2 + 2 MUFU.EX2 per candidate pair.
@@ -670,7 +678,7 @@ __device__ __forceinline__ void sweep_steps(const int4* __restrict__ unit, int l
                                             f2_t (&Sx)[NP], f2_t (&Sy)[NP], f2_t (&Sz)[NP]) {
   const int4* col = unit + 2 * lane;
   const int sw = (lane >> 2) & 1;
-#pragma unroll 2
+#pragma unroll kStepUnroll
   for (int k = 0; k < 2 * units; ++k) {
     const int4 sl = col[(k >> 1) * kUnitSlots + ((k & 1) ^ sw)];  // conflict-free LDS.128 (slot_index)
     const float x = __int_as_float(sl.x), y = __int_as_float(sl.y), z = __int_as_float(sl.z);
@@ -710,16 +718,26 @@ struct SweepCtl {
   unsigned grp_done[kMaxSweepReqs][kMaxChunkGroups];  // finished chunks per group
 };
 
+// Counter increment with acquire-release semantics at GPU scope: after a
+// __syncwarp it publishes the whole warp's prior stores (release is
+// cumulative) and, for the last arriver, orders its later loads (acquire).
+__device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
 // A request's work item (chunk group or displacement slice) is complete; the
 // warp completing its last item adds the group partials in a fixed order and
 // writes F, the gradient (inner_product.cpp:121-157, assembled in FP64) and
 // the displacement; resets the request's counters and displacement bits.
 __device__ __noinline__ void item_done(const SweepReq& R, SweepCtl* ctl, int r, int n_items, int lane) {
+  __syncwarp();
   unsigned old = 0;
-  if (lane == 0) old = atomicAdd(&ctl->req_done[r], 1u);
+  if (lane == 0) old = atom_add_acq_rel(&ctl->req_done[r], 1u);
   old = __shfl_sync(0xffffffffu, old, 0);
+  __syncwarp();
   if ((int)old != n_items - 1) return;
-  __threadfence();
   const int M = R.M, NV = R.grad ? 7 : 1, MV = M * NV;
   const int C = chunk_count(request_units(R));
   const int NG = (C + kChunkGroup - 1) / kChunkGroup;
@@ -791,6 +809,7 @@ struct SweepWarp {
   unsigned long long* bars;
   float* tc;         // transform coefficients of the current chunk (shared)
   int lane;
+  int tc_r;          // request whose coefficients tc holds
   unsigned consumed, rec_used;
 };
 
@@ -898,7 +917,8 @@ __device__ __forceinline__ void chunk_body(SweepWarp& w, const SweepReq& R, int 
   // start); 96 floats hold Td for 8 candidates or Td + Ta for 4
   constexpr bool kStage = !GRAD || NP <= 2;
   float* tc = w.tc;
-  if (kStage) {
+  if (kStage && w.tc_r != r) {  // consecutive chunks of one request keep them
+    w.tc_r = r;
     __syncwarp();
     for (int i = lane; i < M * 12; i += 32) {
       tc[i] = (&R.Td[0][0])[i];
@@ -1044,15 +1064,14 @@ __device__ __forceinline__ void chunk_body(SweepWarp& w, const SweepReq& R, int 
     }
   }
   // chunk group done? its last chunk sums the group's partials in order
-  __threadfence();
   __syncwarp();
   const int grp = c / kChunkGroup;
   unsigned old = 0;
-  if (lane == 0) old = atomicAdd(&w.ctl->grp_done[r][grp], 1u);
+  if (lane == 0) old = atom_add_acq_rel(&w.ctl->grp_done[r][grp], 1u);
   old = __shfl_sync(0xffffffffu, old, 0);
+  __syncwarp();
   const int gsize = min(kChunkGroup, C - grp * kChunkGroup);
   if ((int)old == gsize - 1) {
-    __threadfence();
     double* gpart = R.partials + (size_t)kMaxChunks * MV + (size_t)grp * MV;
     // lane l loads chunk (group base + l); fixed-order shuffle tree per value
     const double* src = R.partials + ((size_t)grp * kChunkGroup + lane) * MV;
@@ -1061,8 +1080,6 @@ __device__ __forceinline__ void chunk_body(SweepWarp& w, const SweepReq& R, int 
       if (lane == 0) gpart[v] = x;
     }
     if (lane == 0) w.ctl->grp_done[r][grp] = 0u;
-    __threadfence();
-    __syncwarp();
     item_done(R, w.ctl, r, n_items, lane);
   }
 }
@@ -1091,6 +1108,7 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(const SweepReq* reqs
            wid * kSweepStages;
   w.tc = tco[wid];
   w.lane = lane;
+  w.tc_r = -1;
   w.consumed = w.rec_used = 0;
 
   // work items of request r: disp_s[r] displacement slices, then its chunks;
