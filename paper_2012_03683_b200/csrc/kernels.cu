@@ -584,6 +584,11 @@ __device__ __forceinline__ f2_t add2(f2_t a, f2_t b) {
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
   return r;
 }
+// in-place accumulation (the accumulator register is tied, no copies)
+__device__ __forceinline__ void fma2_acc(f2_t& acc, f2_t a, f2_t b) {
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(a), "l"(b));
+}
+__device__ __forceinline__ void add2_acc(f2_t& acc, f2_t a) { asm("add.rn.f32x2 %0, %0, %1;" : "+l"(acc) : "l"(a)); }
 __device__ __forceinline__ f2_t mul2(f2_t a, f2_t b) {
   f2_t r;
   asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
@@ -664,11 +669,6 @@ constexpr size_t kSweepSmem = (size_t)kSweepWarps * kSweepStages * kStageSlots *
                               (size_t)kSweepWarps * kRecSlots * sizeof(ChunkRec) +
                               (size_t)kSweepWarps * kSweepStages * sizeof(unsigned long long);
 
-#ifndef KREG_STEP_UNROLL
-#define KREG_STEP_UNROLL 2
-#endif
-constexpr int kStepUnroll = KREG_STEP_UNROLL;
-
 // `units` sweep units (2 steps each) of one tile column (lane = source) for M
 // candidates: d = (x - T_b z) - delta, w = ex2(r^2 kappa + log2 c), W += w
 // and (GRAD) S += w d on FFMA2/FADD2/FMUL2 + 2 MUFU.EX2 per candidate pair.
@@ -676,11 +676,11 @@ template <int NP, bool GRAD>
 __device__ __forceinline__ void sweep_steps(const int4* __restrict__ unit, int lane, int units, const f2_t (&ndx)[NP],
                                             const f2_t (&ndy)[NP], const f2_t (&ndz)[NP], f2_t kap2, f2_t (&W)[NP],
                                             f2_t (&Sx)[NP], f2_t (&Sy)[NP], f2_t (&Sz)[NP]) {
-  const int4* col = unit + 2 * lane;
+  // slot s of unit u sits at 2 lane + (s ^ sw) (slot_index): two swizzled bases
   const int sw = (lane >> 2) & 1;
-#pragma unroll kStepUnroll
-  for (int k = 0; k < 2 * units; ++k) {
-    const int4 sl = col[(k >> 1) * kUnitSlots + ((k & 1) ^ sw)];  // conflict-free LDS.128 (slot_index)
+  const int4* p0 = unit + 2 * lane + sw;
+  const int4* p1 = unit + 2 * lane + (1 - sw);
+  auto step = [&](const int4 sl) {
     const float x = __int_as_float(sl.x), y = __int_as_float(sl.y), z = __int_as_float(sl.z);
     const float lc = __int_as_float(sl.w);
     const f2_t x2 = pk2(x, x), y2 = pk2(y, y), z2 = pk2(z, z), lc2 = pk2(lc, lc);
@@ -693,12 +693,25 @@ __device__ __forceinline__ void sweep_steps(const int4* __restrict__ unit, int l
       float e0, e1;
       upk2(fma2(r2, kap2, lc2), e0, e1);
       const f2_t w = pk2(ex2_approx(e0), ex2_approx(e1));
-      W[p] = add2(W[p], w);
+      add2_acc(W[p], w);
       if (GRAD) {
-        Sx[p] = fma2(w, dx, Sx[p]);
-        Sy[p] = fma2(w, dy, Sy[p]);
-        Sz[p] = fma2(w, dz, Sz[p]);
+        fma2_acc(Sx[p], w, dx);
+        fma2_acc(Sy[p], w, dy);
+        fma2_acc(Sz[p], w, dz);
       }
+    }
+  };
+  if (units == kStageUnits) {  // a full stage: straight-line code, constant offsets
+#pragma unroll
+    for (int u = 0; u < kStageUnits; ++u) {
+      step(p0[u * kUnitSlots]);  // conflict-free LDS.128
+      step(p1[u * kUnitSlots]);
+    }
+  } else {
+#pragma unroll 1
+    for (int u = 0; u < units; ++u) {
+      step(p0[u * kUnitSlots]);
+      step(p1[u * kUnitSlots]);
     }
   }
 }
