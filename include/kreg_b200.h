@@ -173,6 +173,12 @@ kreg_status kreg_ctx_reset_stats(kreg_ctx* ctx);
  * R_s - cutoff (exact: same FP64 predicate); 0 = always search the grid.
  * Default 0.25 (env KREG_SKIN). Engine extension, no reference counterpart. */
 kreg_status kreg_ctx_set_candidate_skin(kreg_ctx* ctx, double skin);
+/* Sweep chunk size (in 2-step units) of pair lists built from now on:
+ * larger chunks amortise per-chunk costs (throughput, default 48), smaller
+ * ones spread one list over more warps (single-registration latency).
+ * Results are bitwise reproducible for a given setting (env KREG_CHUNK_UNITS).
+ * Engine extension, no reference counterpart. */
+kreg_status kreg_ctx_set_chunk_units(kreg_ctx* ctx, int32_t units);
 /* Builds so far: {grid searches, candidate-list filters}. */
 kreg_status kreg_ctx_build_stats(const kreg_ctx* ctx, int64_t out[2]);
 

@@ -62,6 +62,7 @@ def lib():
         L.kreg_ctx_stats.argtypes = [P, _abi.dptr]
         L.kreg_ctx_reset_stats.argtypes = [P]
         L.kreg_ctx_set_candidate_skin.argtypes = [P, D]
+        L.kreg_ctx_set_chunk_units.argtypes = [P, C.c_int32]
         L.kreg_ctx_build_stats.argtypes = [P, _abi.i64ptr]
         L.kreg_rebuild_pairs.argtypes = [P, P, _abi.dptr, KP, D, D, _abi.i64ptr]
         L.kreg_cloud_create.argtypes = [P, VP, C.POINTER(P)]
@@ -153,6 +154,11 @@ class Context:
     def set_candidate_skin(self, skin: float):
         """Candidate-list radius R_s = cutoff * (1 + skin); 0 = grid search every build."""
         _check(lib().kreg_ctx_set_candidate_skin(self.h, float(skin)))
+
+    def set_chunk_units(self, units: int):
+        """Sweep chunk size (2-step units) of lists built from now on: 48 for
+        throughput (default), ~10 for single-registration latency."""
+        _check(lib().kreg_ctx_set_chunk_units(self.h, int(units)))
 
     def build_stats(self):
         out = np.zeros(2, dtype=np.int64)

@@ -209,7 +209,16 @@ kreg_status kreg_ctx_create(int32_t device, kreg_ctx** out) {
     KREG_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
     ctx->launches_base = kreg_dev::kernel_launch_count();
     if (const char* sk = std::getenv("KREG_SKIN")) ctx->skin = std::atof(sk);
+    if (const char* cu = std::getenv("KREG_CHUNK_UNITS")) ctx->chunk_pref = std::max(1, std::atoi(cu));
     *out = ctx.release();
+  });
+}
+
+kreg_status kreg_ctx_set_chunk_units(kreg_ctx* ctx, int32_t units) {
+  return guarded([&] {
+    require(ctx != nullptr, "ctx must not be NULL");
+    require(units >= 1 && units <= 4096, "chunk units must lie in [1, 4096]");
+    ctx->chunk_pref = units;
   });
 }
 

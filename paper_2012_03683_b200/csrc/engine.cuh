@@ -42,7 +42,7 @@ constexpr int kMaxChunks = KREG_MAX_CHUNKS;      // chunks per request at most (
 #ifndef KREG_PREF_CHUNK_UNITS
 #define KREG_PREF_CHUNK_UNITS 48
 #endif
-constexpr int kPrefChunkUnits = KREG_PREF_CHUNK_UNITS;  // preferred chunk size (units)
+constexpr int kPrefChunkUnits = KREG_PREF_CHUNK_UNITS;  // default preferred chunk size (units)
 constexpr int kQueueDepth = 8;                   // chunks a warp may hold in its prefetch queue
 constexpr int kMaxSweepReqs = kSweepThreads;     // requests per sweep launch
 constexpr int kChunkGroup = 32;                  // chunk partials summed per group (first reduction level)
@@ -138,6 +138,7 @@ struct BuildReq {
   int write_index;       // emit also writes slot_i (export re-runs the emit with it set)
   long long capacity;
   unsigned long long* disp_blk;   // ceil(n_z / 8): per filter block max |T z - Ts z|^2 (bits)
+  int chunk_pref;        // sweep chunking of this list (chunk_units)
   double* status;        // kBuildStatus: {P, slots > cap, slots, cand > cap, cand, |T-Ts| disp, invalid, -}
 };
 constexpr int kBuildStatus = 8;
@@ -153,6 +154,7 @@ struct alignas(16) SweepReq {
   const int4* slots;
   long long capacity;    // slot capacity (an overflowed build is skipped)
   int grad;              // 0: F (+ displacement) only, 1: F + gradient
+  int chunk_pref;        // the list's sweep chunking (chunk_units)
   const double* zx; const double* zy; const double* zz;  // source, sorted
   int n_z;
   int M;

@@ -554,6 +554,8 @@ static void prepare_build(kreg_ctx* ctx, BuildJob& job, kreg_dev::BuildReq& R) {
   R.slot_i = p->slot_i.ptr;
   R.capacity = static_cast<long long>(p->slot_buf.cap);
   R.disp_blk = p->disp_blk.ptr;
+  p->chunk_pref = ctx->chunk_pref;
+  R.chunk_pref = p->chunk_pref;
 }
 
 // Scratch of request e lives in per-round arenas of the context (several
@@ -585,6 +587,7 @@ static void prepare_sweep(EvalJob& job, kreg_dev::SweepReq& R, double* partials,
   R.slots = p->slot_buf.ptr;
   R.capacity = static_cast<long long>(p->slot_buf.cap);
   R.grad = job.grad ? 1 : 0;
+  R.chunk_pref = p->chunk_pref;
   R.zx = p->Z->x.ptr; R.zy = p->Z->y.ptr; R.zz = p->Z->z.ptr;
   R.n_z = nz;
   R.M = job.M;

@@ -157,6 +157,7 @@ struct kreg_ctx {
   // capacity high-water marks over all workspaces: a pooled workspace that
   // must grow goes straight to the largest size any registration needed
   long long hw_slots = 0, hw_sup = 0;
+  int chunk_pref = kreg_dev::kPrefChunkUnits;  // sweep chunk size of new lists (kreg_ctx_set_chunk_units)
   long long full_builds = 0, filter_builds = 0;
   kreg_host::Collective collective;  // row-sharded registrations (kreg_ctx_set_collective)
   // host-side round accounting (seconds)
@@ -227,6 +228,7 @@ struct kreg_pairs {
   long long slots = 0;                     // valid after the build round
   bool counts_valid = false;               // P / slots known on the host
   double anchor[3] = {0, 0, 0};
+  int chunk_pref = kreg_dev::kPrefChunkUnits;  // sweep chunking of this list
   long long expected_pairs = 0;  // capacity hint
   // the last build's request (pairs_export re-runs its emit to recover slot_i)
   kreg_dev::BuildReq last_req{};

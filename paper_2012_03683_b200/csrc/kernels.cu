@@ -80,13 +80,13 @@ constexpr int kUnitSlots = 32 * kUnitSteps;  // slots per sweep work unit
 // Chunks of kPrefChunkUnits units (per-chunk costs amortised over ~48 KB of
 // slots) unless the list needs more than kMaxChunks of them (C4-size lists
 // then use kMaxChunks larger chunks, keeping every warp busy).
-__host__ __device__ __forceinline__ long long chunk_units(long long U) {
+__host__ __device__ __forceinline__ long long chunk_units(long long U, int pref) {
   long long cu = (U + kMaxChunks - 1) / kMaxChunks;
-  if (cu < kPrefChunkUnits) cu = kPrefChunkUnits;
+  if (cu < pref) cu = pref;
   return (cu + kStageUnits - 1) / kStageUnits * kStageUnits;
 }
-__host__ __device__ __forceinline__ int chunk_count(long long U) {
-  return U <= 0 ? 1 : (int)((U + chunk_units(U) - 1) / chunk_units(U));
+__host__ __device__ __forceinline__ int chunk_count(long long U, int pref) {
+  return U <= 0 ? 1 : (int)((U + chunk_units(U, pref) - 1) / chunk_units(U, pref));
 }
 
 // Candidate stage, grid over X (requests with full == 0 exit at once).
@@ -408,8 +408,8 @@ __global__ void k_chunk_records(const BuildReq* reqs) {
   const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (R.tile_off[R.n_tiles] > R.capacity) return;
   const long long U = R.unit_off[R.n_tiles];
-  if (U == 0 || c >= chunk_count(U)) return;
-  const long long u0 = (long long)c * chunk_units(U);
+  if (U == 0 || c >= chunk_count(U, R.chunk_pref)) return;
+  const long long u0 = (long long)c * chunk_units(U, R.chunk_pref);
   int lo = 0, hi = R.n_tiles - 1;  // last tile t with unit_off[t] <= u0 (it has units)
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
@@ -752,7 +752,7 @@ __device__ __noinline__ void item_done(const SweepReq& R, SweepCtl* ctl, int r, 
   __syncwarp();
   if ((int)old != n_items - 1) return;
   const int M = R.M, NV = R.grad ? 7 : 1, MV = M * NV;
-  const int C = chunk_count(request_units(R));
+  const int C = chunk_count(request_units(R), R.chunk_pref);
   const int NG = (C + kChunkGroup - 1) / kChunkGroup;
   const double* gpart = R.partials + (size_t)kMaxChunks * MV;
   // group partials: lane l holds groups l and l + 32 (NG <= 64), fixed-order
@@ -853,7 +853,7 @@ __device__ __forceinline__ bool produce(SweepWarp& w) {
     ++Q.tail;
     const int i = g - w.cbase[r] - disp_items(w.reqs[r]);
     if (i < 0) continue;  // displacement item: no stages
-    const long long U = w.units[r], cu = chunk_units(U);
+    const long long U = w.units[r], cu = chunk_units(U, w.reqs[r].chunk_pref);
     Q.pr = r;
     Q.pc = i;
     Q.pu = (int)(Q.pc * cu);
@@ -923,7 +923,7 @@ __device__ __forceinline__ void chunk_body(SweepWarp& w, const SweepReq& R, int 
   const int lane = w.lane;
   const int M = R.M;
   const int MV = M * (GRAD ? 7 : 1);
-  const long long U = w.units[r], cu = chunk_units(U);
+  const long long U = w.units[r], cu = chunk_units(U, R.chunk_pref);
   const long long u0 = (long long)c * cu, u1 = min(U, u0 + cu);
   const f2_t kap2 = pk2(R.kappa, R.kappa);
   // this chunk's transform coefficients in shared memory (read at every tile
@@ -1131,7 +1131,7 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(const SweepReq* reqs
     if (threadIdx.x < n_req) {
       const SweepReq& Rq = reqs[threadIdx.x];
       const long long U = request_units(Rq);
-      C = chunk_count(U) + disp_items(Rq);
+      C = chunk_count(U, Rq.chunk_pref) + disp_items(Rq);
       units_s[threadIdx.x] = (int)U;
     }
     int tot;
@@ -1273,13 +1273,20 @@ void sweep_batched(const SweepReq* h, const SweepReq* d, int n, int sm_count, un
   // reduction over all requests
   // one persistent launch per kMaxSweepReqs requests (F-only requests first:
   // their chunks are the heaviest, so they are grabbed first)
-  const int grid = 2 * sm_count;
   int launches = 0;
   for (int r0 = 0; r0 < n; r0 += kMaxSweepReqs) {
     const int r1 = min(n, r0 + kMaxSweepReqs);
     int max_mg = 1;
-    for (int r = r0; r < r1; ++r)
+    // persistent grid of 2 CTAs per SM, fewer when the work items of the
+    // launch are known on the host (lists built in earlier rounds): every
+    // warp then has at least one item and idle CTAs are not launched
+    long long items = 0;
+    for (int r = r0; r < r1; ++r) {
       if (h[r].grad) max_mg = max(max_mg, h[r].M);
+      items += h[r].units >= 0 ? chunk_count(h[r].units, h[r].chunk_pref) + (h[r].n_z + kDispItem - 1) / kDispItem
+                               : (1LL << 40);
+    }
+    const int grid = (int)max(1LL, min((long long)2 * sm_count, (items + kSweepWarps - 1) / kSweepWarps));
     const SweepReq* dr = d + r0;
     SweepCtl* ctl = reinterpret_cast<SweepCtl*>(d_ctl) + launches;
     if (max_mg <= 2) k_sweep<1><<<grid, kSweepThreads, kSweepSmem, st>>>(dr, r1 - r0, ctl);
