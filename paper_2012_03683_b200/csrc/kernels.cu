@@ -1100,9 +1100,23 @@ __device__ __forceinline__ void chunk_body(SweepWarp& w, const SweepReq& R, int 
 // Persistent sweep over the work items (displacement slices + chunks) of up
 // to kMaxSweepReqs requests; gradient requests with M <= 2 NPG candidates,
 // F-only requests (line-search failure path) with M <= 8.
+#ifdef KREG_TIMELINE
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
+
 template <int NPG>
 __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(const SweepReq* reqs, int n_req, SweepCtl* ctl) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#ifdef KREG_TIMELINE
+  const unsigned long long tl0 = gtimer();
+  __shared__ unsigned tl_items;
+  __shared__ unsigned long long tl_last;
+  if (threadIdx.x == 0) tl_items = 0, tl_last = 0;
+#endif
   __shared__ int cbase[kMaxSweepReqs + 1];
   __shared__ int units_s[kMaxSweepReqs];
   __shared__ float tco[kSweepWarps][96];  // per warp: Td (and Ta) of its current chunk
@@ -1179,9 +1193,20 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(const SweepReq* reqs
     __syncwarp();
     if (lane == 0) ++g_wq[wid].head;
     __syncwarp();
+#ifdef KREG_TIMELINE
+    if (lane == 0) {
+      atomicAdd(&tl_items, 1u);
+      atomicMax(&tl_last, gtimer());
+    }
+#endif
   }
   // the last CTA to exit resets the launch's item counter
   __syncthreads();
+#ifdef KREG_TIMELINE
+  if (threadIdx.x == 0)
+    printf("TL cta %d sm %d start %llu last_item %llu end %llu items %u\n", blockIdx.x, 0, tl0, tl_last, gtimer(),
+           tl_items);
+#endif
   if (threadIdx.x == 0) {
     __threadfence();
     if (atomicAdd(&ctl->exited, 1u) == gridDim.x - 1) {
