@@ -255,6 +255,15 @@ kreg_status kreg_indicator(kreg_ctx* ctx, const kreg_cloud* X, const kreg_cloud*
  * parts (optional) = {cross, ||f_X||^2, ||f_Z||^2}. std::invalid_argument
  * cases map to KREG_INVALID_ARGUMENT (empty clouds, zero-norm functions,
  * schema / params mismatch). Feature rows up to 32 values. */
+/* reference eval.cpp:198-235 indicator_sweep (SweepAxis rotation: about z
+ * through the centroid; translation: along +x): indicators of `cloud`
+ * against perturbed copies at `steps` magnitudes evenly spaced over [0, range]
+ * (one magnitude when range == 0). magnitudes / indicators hold max(steps, 1)
+ * entries. All pair builds and evaluations run in one batched device round. */
+enum { KREG_SWEEP_ROTATION = 0, KREG_SWEEP_TRANSLATION = 1 };
+kreg_status kreg_indicator_sweep(kreg_ctx* ctx, const kreg_cloud_view* cloud, const kreg_kernel_params* params,
+                                 int32_t axis, double range, int32_t steps, double cutoff_multiplier,
+                                 double c_min, double* magnitudes, double* indicators);
 kreg_status kreg_exact_cosine(kreg_ctx* ctx, const kreg_cloud_view* X, const kreg_cloud_view* Z,
                               const double T[12], const kreg_kernel_params* params, double* cosine,
                               double parts[3]);

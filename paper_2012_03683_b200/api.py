@@ -96,6 +96,7 @@ def lib():
         L.kreg_register_clouds_rows.argtypes = [P, P, P, C.c_int64, _abi.dptr, KP, CP, RP]
         L.kreg_ctx_set_collective.argtypes = [P, COLLECTIVE_FN, VP_]
         L.kreg_exact_cosine.argtypes = [P, VP, VP, _abi.dptr, KP, _abi.dptr, _abi.dptr]
+        L.kreg_indicator_sweep.argtypes = [P, VP, KP, C.c_int32, D, C.c_int32, D, D, _abi.dptr, _abi.dptr]
         L.kreg_se3_exp.argtypes = [_abi.dptr, _abi.dptr]
         L.kreg_se3_compose.argtypes = [_abi.dptr, _abi.dptr, _abi.dptr]
         L.kreg_se3_inverse.argtypes = [_abi.dptr, _abi.dptr]
@@ -491,6 +492,23 @@ def register_clouds_rows(X, Z_rows, n_z_total: int, initial, params: KernelParam
     finally:
         lib().kreg_ctx_set_collective(ctx.h, COLLECTIVE_FN(), None)
     return RegistrationResult.from_buffers(buf)
+
+
+def indicator_sweep(cloud: PointCloud, params: KernelParams, axis: str, range_: float, steps: int,
+                    cutoff_multiplier: float = 3.0, c_min: float = 1e-4, ctx=None):
+    """reference eval.cpp:198-235: [(magnitude, indicator)] of the cloud against
+    perturbed copies of itself (axis "rotation" about z through the centroid, or
+    "translation" along +x); one batched device round."""
+    ctx = ctx or default_context()
+    if axis not in ("rotation", "translation"):
+        raise ValueError("indicator_sweep: axis must be 'rotation' or 'translation'")
+    n = max(int(steps), 1)
+    mags, inds = np.zeros(n), np.zeros(n)
+    _check(lib().kreg_indicator_sweep(ctx.h, cloud.view(), params.cstruct(), 0 if axis == "rotation" else 1,
+                                      float(range_), int(steps), float(cutoff_multiplier), float(c_min),
+                                      _abi.as_ptr(mags), _abi.as_ptr(inds)))
+    k = 1 if range_ == 0.0 else int(steps)
+    return list(zip(mags[:k].tolist(), inds[:k].tolist()))
 
 
 def exact_cosine(X: PointCloud, Z: PointCloud, T, params: KernelParams, ctx=None, parts: bool = False):

@@ -684,6 +684,76 @@ kreg_status kreg_register_sequence_spans(kreg_ctx* ctx, const kreg_cloud* const*
   });
 }
 
+kreg_status kreg_indicator_sweep(kreg_ctx* ctx, const kreg_cloud_view* cloud, const kreg_kernel_params* params,
+                                int32_t axis, double range, int32_t steps, double cutoff_multiplier, double c_min,
+                                double* magnitudes, double* indicators) {
+  return guarded([&] {
+    // eval.cpp:198-235: indicator(cloud, perturb(cloud), I) at `steps`
+    // magnitudes; indicator(X, P Z, I) == indicator(X, Z, P) (same FP64
+    // apply), so every magnitude is one pair build + one evaluation at P,
+    // all issued in one batched device round
+    require(ctx && cloud && params && magnitudes && indicators, "NULL argument");
+    require(axis == KREG_SWEEP_ROTATION || axis == KREG_SWEEP_TRANSLATION, "indicator_sweep: unknown axis");
+    if (steps < 2 && range != 0.0) throw Error(KREG_INVALID_ARGUMENT, "indicator_sweep: steps must be >= 2");
+    if (range < 0.0) throw Error(KREG_INVALID_ARGUMENT, "indicator_sweep: range must be >= 0");
+    double centroid[3] = {0, 0, 0};
+    for (int i = 0; i < cloud->n; ++i)
+      for (int k = 0; k < 3; ++k) centroid[k] += cloud->xyz[3 * i + k];
+    if (cloud->n > 0)
+      for (double& v : centroid) v /= cloud->n;
+    std::vector<double> mags;
+    if (range == 0.0) {
+      mags.push_back(0.0);
+    } else {
+      for (int k = 0; k < steps; ++k) mags.push_back(range * static_cast<double>(k) / static_cast<double>(steps - 1));
+    }
+    std::unique_ptr<kreg_cloud> c(cloud_create(ctx, cloud));
+    const Params p = to_params(params);
+    check_build_args(c.get(), c.get(), p, cutoff_multiplier, c_min);
+    if (c->n == 0) throw Error(KREG_INVALID_ARGUMENT, "indicator: clouds must be non-empty");
+    const size_t K = mags.size();
+    std::vector<std::unique_ptr<kreg_pairs>> lists(K);
+    std::vector<double> Ts(12 * K), outs(8 * K, 0.0);
+    std::vector<BuildJob> builds;
+    std::vector<EvalJob> evals;
+    for (size_t k = 0; k < K; ++k) {
+      double* T = Ts.data() + 12 * k;
+      if (axis == KREG_SWEEP_ROTATION) {
+        const double xi[6] = {0, 0, mags[k], 0, 0, 0};
+        kreg_se3::exp(xi, T);  // rotation about z through the centroid
+        for (int r = 0; r < 3; ++r)
+          T[4 * r + 3] = centroid[r] - (T[4 * r] * centroid[0] + T[4 * r + 1] * centroid[1] + T[4 * r + 2] * centroid[2]);
+      } else {
+        kreg_se3::identity(T);
+        T[3] = mags[k];
+      }
+      lists[k] = std::make_unique<kreg_pairs>();
+      BuildJob b;
+      b.pairs = lists[k].get();
+      b.X = c.get();
+      b.Z = c.get();
+      std::memcpy(b.T, T, sizeof(b.T));
+      b.params = p;
+      b.cutoff_multiplier = cutoff_multiplier;
+      b.c_min = c_min;
+      builds.push_back(b);
+      EvalJob e;
+      e.pairs = lists[k].get();
+      e.M = 1;
+      std::memcpy(e.T[0], T, sizeof(double) * 12);
+      e.lengthscale = p.lengthscale;
+      e.out = outs.data() + 8 * k;
+      evals.push_back(e);
+    }
+    run_round(ctx, builds, evals);
+    const double denom = static_cast<double>(c->n);  // sqrt(|X| |Z|) with X == Z
+    for (size_t k = 0; k < K; ++k) {
+      magnitudes[k] = mags[k];
+      indicators[k] = lists[k]->P > 0 ? outs[8 * k] / denom : 0.0;
+    }
+  });
+}
+
 kreg_status kreg_exact_cosine(kreg_ctx* ctx, const kreg_cloud_view* X, const kreg_cloud_view* Z, const double T[12],
                               const kreg_kernel_params* params, double* cosine, double parts[3]) {
   return guarded([&] {

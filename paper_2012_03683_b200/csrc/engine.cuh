@@ -33,7 +33,10 @@ constexpr int kSweepThreads = 256;  // threads per persistent sweep CTA (2 CTAs 
 #define KREG_SWEEP_STAGES 3
 #endif
 constexpr int kUnitSteps = KREG_UNIT_STEPS;      // degree steps per sweep unit (x 32 lanes x 16 B)
-constexpr int kStageUnits = 4;                   // units per TMA stage (4 KB at 2 steps)
+#ifndef KREG_STAGE_UNITS
+#define KREG_STAGE_UNITS 4
+#endif
+constexpr int kStageUnits = KREG_STAGE_UNITS;    // units per TMA stage (4 KB at 2 steps)
 constexpr int kSweepStages = KREG_SWEEP_STAGES;  // per-warp TMA ring depth (stages)
 #ifndef KREG_MAX_CHUNKS
 #define KREG_MAX_CHUNKS 2048
@@ -44,7 +47,10 @@ constexpr int kMaxChunks = KREG_MAX_CHUNKS;      // chunks per request at most (
 #endif
 constexpr int kPrefChunkUnits = KREG_PREF_CHUNK_UNITS;  // default preferred chunk size (units)
 constexpr int kQueueDepth = 8;                   // chunks a warp may hold in its prefetch queue
-constexpr int kMaxSweepReqs = kSweepThreads;     // requests per sweep launch
+#ifndef KREG_MAX_SWEEP_REQS
+#define KREG_MAX_SWEEP_REQS 256
+#endif
+constexpr int kMaxSweepReqs = KREG_MAX_SWEEP_REQS;  // requests per sweep launch (<= kSweepThreads)
 constexpr int kChunkGroup = 32;                  // chunk partials summed per group (first reduction level)
 constexpr int kMaxChunkGroups = (kMaxChunks + kChunkGroup - 1) / kChunkGroup;
 constexpr int kDispItem = 512;                   // sources per displacement work item

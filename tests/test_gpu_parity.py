@@ -458,3 +458,29 @@ def test_exact_cosine_kitti_vs_reference(ctx, ref):
         want = ref.exact_cosine(X, Z, T, p)
         assert got == pytest.approx(want, rel=1e-12)
         assert 0.0 < got < 1.0 and all(v > 0 for v in parts)
+
+
+def test_indicator_sweep_vs_reference(ctx, ref):
+    """eval.cpp:198-235 indicator_sweep: indicator(cloud, P cloud, I) at evenly
+    spaced magnitudes == the reference's indicator(cloud, cloud, P)."""
+    X, _, _ = synth.kitti_pair(13, 4000)
+    p = synth.kitti_params()
+    cen = X.positions.mean(axis=0)
+    for axis, rng_ in (("rotation", 0.05), ("translation", 0.2)):
+        rows = api.indicator_sweep(X, p, axis, rng_, 5)
+        assert [m for m, _ in rows] == pytest.approx([rng_ * k / 4 for k in range(5)], abs=1e-15)
+        for m, ind in rows:
+            if axis == "rotation":
+                R = api.se3_exp([0, 0, m, 0, 0, 0])
+                P = Isometry(R.rotation, cen - R.rotation @ cen)
+            else:
+                P = Isometry(np.eye(3), np.array([m, 0.0, 0.0]))
+            want = ref.indicator(X, X, P, p)
+            assert ind == pytest.approx(want, rel=1e-4)
+        inds = [v for _, v in rows]
+        assert inds[0] > inds[-1]  # misalignment lowers the indicator
+    assert len(api.indicator_sweep(X, p, "translation", 0.0, 1)) == 1
+    with pytest.raises(ValueError):
+        api.indicator_sweep(X, p, "rotation", 0.1, 1)
+    with pytest.raises(ValueError):
+        api.indicator_sweep(X, p, "rotation", -0.1, 3)
