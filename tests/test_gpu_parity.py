@@ -484,3 +484,18 @@ def test_indicator_sweep_vs_reference(ctx, ref):
         api.indicator_sweep(X, p, "rotation", 0.1, 1)
     with pytest.raises(ValueError):
         api.indicator_sweep(X, p, "rotation", -0.1, 3)
+
+
+def test_tum_registration_vs_reference(ctx, ref):
+    """C2 (TUM-shaped 20k, colour dim 5) registration: same decisions as the
+    reference loop (iterations, levels) and the same pose to 1e-3."""
+    X, Z, Ts = synth.tum_pair(5, 20000)
+    p, cfg = synth.tum_params(), synth.tum_subsequent_config()
+    ref.set_threads(max(1, os.cpu_count() or 1))
+    r = ref.register_clouds(X, Z, Isometry(), p, cfg)
+    g = api.register_clouds(X, Z, Isometry(), p, cfg)
+    err = compose(inverse(g.transform), r.transform)
+    assert rotation_angle(err) <= 1e-3 and translation_norm(err) <= 1e-3, (rotation_angle(err), translation_norm(err))
+    assert g.converged == r.converged
+    assert abs(g.iterations - r.iterations) <= max(2, r.iterations // 50)
+    assert np.allclose(g.objective_trace[:20], r.objective_trace[:20], rtol=1e-6, atol=0)
