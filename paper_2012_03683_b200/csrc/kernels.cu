@@ -879,37 +879,30 @@ __device__ __forceinline__ bool produce(SweepWarp& w) {
 // Displacement slice of request r: max_j |T_m z_j - T_b z_j| in FP64 over the
 // original coordinates (order-free max).
 __device__ __noinline__ void displacement_item(SweepWarp& w, const SweepReq& R, int r, int item, int n_items) {
+  // |T_m z - T_b z| = |(R_m - R_b) z + (t_m - t_b)|: one 3x4 product per
+  // candidate and source (equal to the reference's difference of two
+  // transforms up to the last bit)
   const int lane = w.lane, M = R.M;
   const int j0 = item * kDispItem, j1 = min(R.n_z, j0 + kDispItem);
-  unsigned long long dmax[kMaxCandidates];
+  for (int m = 0; m < M; ++m) {
+    double D[12];
 #pragma unroll
-  for (int m = 0; m < kMaxCandidates; ++m) dmax[m] = 0ull;
-  for (int j = j0 + lane; j < j1; j += 32) {
-    const double zx = R.zx[j], zy = R.zy[j], zz = R.zz[j];
-    double bx, by, bz;
-    apply_T(R.Tb, zx, zy, zz, bx, by, bz);
-#pragma unroll
-    for (int m = 0; m < kMaxCandidates; ++m) {
-      if (m < M) {
-        double x, y, z;
-        apply_T(R.T[m], zx, zy, zz, x, y, z);
-        const double dx = x - bx, dy = y - by, dz = z - bz;
-        const unsigned long long d2 = (unsigned long long)__double_as_longlong(dx * dx + dy * dy + dz * dz);
-        dmax[m] = d2 > dmax[m] ? d2 : dmax[m];
-      }
+    for (int k = 0; k < 12; ++k) D[k] = R.T[m][k] - R.Tb[k];
+    unsigned long long d = 0ull;
+    for (int j = j0 + lane; j < j1; j += 32) {
+      const double zx = R.zx[j], zy = R.zy[j], zz = R.zz[j];
+      const double dx = D[0] * zx + D[1] * zy + D[2] * zz + D[3];
+      const double dy = D[4] * zx + D[5] * zy + D[6] * zz + D[7];
+      const double dz = D[8] * zx + D[9] * zy + D[10] * zz + D[11];
+      const unsigned long long d2 = (unsigned long long)__double_as_longlong(dx * dx + dy * dy + dz * dz);
+      d = d2 > d ? d2 : d;
     }
-  }
 #pragma unroll
-  for (int m = 0; m < kMaxCandidates; ++m) {
-    if (m < M) {
-      unsigned long long d = dmax[m];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const unsigned long long other = __shfl_xor_sync(0xffffffffu, d, o);
-        d = other > d ? other : d;
-      }
-      if (lane == 0 && d) atomicMax(&R.disp_bits[m], d);
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long other = __shfl_xor_sync(0xffffffffu, d, o);
+      d = other > d ? other : d;
     }
+    if (lane == 0 && d) atomicMax(&R.disp_bits[m], d);
   }
   item_done(R, w.ctl, r, n_items, lane);
 }
