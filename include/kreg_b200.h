@@ -181,6 +181,11 @@ kreg_status kreg_ctx_set_candidate_skin(kreg_ctx* ctx, double skin);
 kreg_status kreg_ctx_set_chunk_units(kreg_ctx* ctx, int32_t units);
 /* Builds so far: {grid searches, candidate-list filters}. */
 kreg_status kreg_ctx_build_stats(const kreg_ctx* ctx, int64_t out[2]);
+/* Build-stage profile since the last reset (needs kreg_ctx_set_profiling):
+ * out = {device ms of build launches, rounds with builds, candidate entries
+ * scanned by the builds, sweep-list slots emitted}. Diagnostic; no reference
+ * counterpart. */
+kreg_status kreg_ctx_build_profile(const kreg_ctx* ctx, double out[4]);
 
 /* Multi-GPU source-row sharding (configuration C4): every
  * rank registers the replicated target X against its own rows of the source

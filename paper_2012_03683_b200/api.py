@@ -64,6 +64,7 @@ def lib():
         L.kreg_ctx_set_candidate_skin.argtypes = [P, D]
         L.kreg_ctx_set_chunk_units.argtypes = [P, C.c_int32]
         L.kreg_ctx_build_stats.argtypes = [P, _abi.i64ptr]
+        L.kreg_ctx_build_profile.argtypes = [P, _abi.dptr]
         L.kreg_rebuild_pairs.argtypes = [P, P, _abi.dptr, KP, D, D, _abi.i64ptr]
         L.kreg_cloud_create.argtypes = [P, VP, C.POINTER(P)]
         L.kreg_cloud_destroy.argtypes = [P]
@@ -164,7 +165,10 @@ class Context:
     def build_stats(self):
         out = np.zeros(2, dtype=np.int64)
         _check(lib().kreg_ctx_build_stats(self.h, _abi.as_ptr(out, C.c_int64)))
-        return {"grid_builds": int(out[0]), "filter_builds": int(out[1])}
+        prof = np.zeros(4)
+        _check(lib().kreg_ctx_build_profile(self.h, _abi.as_ptr(prof)))
+        return {"grid_builds": int(out[0]), "filter_builds": int(out[1]), "build_ms": float(prof[0]),
+                "build_rounds": int(prof[1]), "filter_entries": int(prof[2]), "built_slots": int(prof[3])}
 
     def host_stats(self):
         out = np.zeros(8)

@@ -238,6 +238,16 @@ kreg_status kreg_ctx_build_stats(const kreg_ctx* ctx, int64_t out[2]) {
   });
 }
 
+kreg_status kreg_ctx_build_profile(const kreg_ctx* ctx, double out[4]) {
+  return guarded([&] {
+    require(ctx != nullptr && out != nullptr, "NULL argument");
+    out[0] = ctx->build_ms;
+    out[1] = static_cast<double>(ctx->build_rounds);
+    out[2] = static_cast<double>(ctx->filter_entries);
+    out[3] = static_cast<double>(ctx->built_slots);
+  });
+}
+
 kreg_status kreg_ctx_destroy(kreg_ctx* ctx) {
   return guarded([&] {
     if (!ctx) return;
@@ -315,6 +325,8 @@ kreg_status kreg_ctx_reset_stats(kreg_ctx* ctx) {
     ctx->t_stage = ctx->t_upload_issue = 0.0;
     ctx->launches_base = kreg_dev::kernel_launch_count();
     ctx->full_builds = ctx->filter_builds = 0;
+    ctx->build_ms = 0.0;
+    ctx->build_rounds = ctx->filter_entries = ctx->built_slots = 0;
   });
 }
 

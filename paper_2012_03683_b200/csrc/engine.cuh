@@ -53,6 +53,9 @@ constexpr int kQueueDepth = 8;                   // chunks a warp may hold in it
 constexpr int kMaxSweepReqs = KREG_MAX_SWEEP_REQS;  // requests per sweep launch (<= kSweepThreads)
 constexpr int kChunkGroup = 32;                  // chunk partials summed per group (first reduction level)
 constexpr int kMaxChunkGroups = (kMaxChunks + kChunkGroup - 1) / kChunkGroup;
+constexpr int kFilterWarp = 8;       // sources per warp of the filter stage
+constexpr int kFilterThreads = 128;  // threads per filter block
+constexpr int kFilterBlock = kFilterThreads / 32 * kFilterWarp;  // sources per filter block (one disp_blk entry)
 constexpr int kDispItem = 512;                   // sources per displacement work item
 // Sliced-ELL slot of step k of the source in lane l of a tile starting at slot
 // tile_off: units of kUnitSteps = 2 steps x 32 sources, source-major inside a
@@ -143,7 +146,7 @@ struct BuildReq {
   int* slot_i;           // capacity: target index i of every slot (export only)
   int write_index;       // emit also writes slot_i (export re-runs the emit with it set)
   long long capacity;
-  unsigned long long* disp_blk;   // ceil(n_z / 8): per filter block max |T z - Ts z|^2 (bits)
+  unsigned long long* disp_blk;   // ceil(n_z / kFilterBlock): per filter block max |T z - Ts z|^2 (bits)
   int chunk_pref;        // sweep chunking of this list (chunk_units)
   double* status;        // kBuildStatus: {P, slots > cap, slots, cand > cap, cand, |T-Ts| disp, invalid, -}
 };

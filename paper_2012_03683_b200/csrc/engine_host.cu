@@ -652,6 +652,8 @@ RoundSlot* round_slot(kreg_ctx* ctx, int i) {
     KREG_CUDA(cudaEventCreateWithFlags(&S->done, cudaEventDisableTiming));
     KREG_CUDA(cudaEventCreate(&S->ev0));
     KREG_CUDA(cudaEventCreate(&S->ev1));
+    KREG_CUDA(cudaEventCreate(&S->evb0));
+    KREG_CUDA(cudaEventCreate(&S->evb1));
     ctx->rs[i] = S;
   }
   return ctx->rs[i];
@@ -661,6 +663,8 @@ RoundSlot::~RoundSlot() {
   if (done) cudaEventDestroy(done);
   if (ev0) cudaEventDestroy(ev0);
   if (ev1) cudaEventDestroy(ev1);
+  if (evb0) cudaEventDestroy(evb0);
+  if (evb1) cudaEventDestroy(evb1);
 }
 
 void begin_round(kreg_ctx* ctx, RoundSlot& S, std::vector<BuildJob>&& builds_in, std::vector<EvalJob>&& evals_in) {
@@ -722,7 +726,11 @@ void begin_round(kreg_ctx* ctx, RoundSlot& S, std::vector<BuildJob>&& builds_in,
   if (ne)
     KREG_CUDA(cudaMemcpyAsync(S.d_sweep.ptr, S.h_sweep.ptr, sizeof(kreg_dev::SweepReq) * ne, cudaMemcpyHostToDevice,
                               ctx->stream));
-  if (nb) kreg_dev::build_pairs_batched(S.h_build.ptr, S.d_build.ptr, nb, ctx->stream);
+  if (nb) {
+    if (ctx->profiling) KREG_CUDA(cudaEventRecord(S.evb0, ctx->stream));
+    kreg_dev::build_pairs_batched(S.h_build.ptr, S.d_build.ptr, nb, ctx->stream);
+    if (ctx->profiling) KREG_CUDA(cudaEventRecord(S.evb1, ctx->stream));
+  }
   if (ne) {
     kreg_dev::sweep_batched(S.h_sweep.ptr, S.d_sweep.ptr, ne, ctx->sm_count, S.counter_arena.ptr, ctx->stream,
                             ctx->profiling ? S.ev0 : nullptr, ctx->profiling ? S.ev1 : nullptr);
@@ -797,6 +805,16 @@ void end_round(kreg_ctx* ctx, RoundSlot& S) {
     begin_round(ctx, S, std::move(b2), std::move(e2));
     end_round(ctx, S);
     return;
+  }
+  if (nb && ctx->profiling) {
+    float ms = 0.0f;
+    KREG_CUDA(cudaEventElapsedTime(&ms, S.evb0, S.evb1));
+    ctx->build_ms += ms;
+    ctx->build_rounds += 1;
+    for (int b = 0; b < nb; ++b) {
+      ctx->filter_entries += builds[b].pairs->sup_entries;
+      ctx->built_slots += builds[b].pairs->slots;
+    }
   }
   long long round_pairs = 0, round_slots = 0;
   for (int e = 0; e < ne; ++e) {

@@ -159,6 +159,10 @@ struct kreg_ctx {
   long long hw_slots = 0, hw_sup = 0;
   int chunk_pref = kreg_dev::kPrefChunkUnits;  // sweep chunk size of new lists (kreg_ctx_set_chunk_units)
   long long full_builds = 0, filter_builds = 0;
+  // build-stage profile (profiling on): device ms of the build launches,
+  // rounds with builds, candidate entries the filters scanned, slots emitted
+  double build_ms = 0.0;
+  long long build_rounds = 0, filter_entries = 0, built_slots = 0;
   kreg_host::Collective collective;  // row-sharded registrations (kreg_ctx_set_collective)
   // host-side round accounting (seconds)
   long long rounds = 0;
@@ -311,7 +315,7 @@ struct RoundSlot {
   DevBuf<int> g_count, g_start, g_int;
   DevBuf<double> g_pos;
   DevBuf<long long> g_scan;
-  cudaEvent_t done = nullptr, ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t done = nullptr, ev0 = nullptr, ev1 = nullptr, evb0 = nullptr, evb1 = nullptr;
   std::vector<BuildJob> builds;
   std::vector<EvalJob> evals;
   size_t n_res = 0;

@@ -377,7 +377,8 @@ __global__ void __launch_bounds__(1024) k_tile_offsets(const BuildReq* reqs) {
     if (threadIdx.x == 0) dmax_s = 0;
     __syncthreads();
     unsigned long long d = 0;
-    for (int b = threadIdx.x; b < (R.n_z + 7) / 8; b += blockDim.x) d = R.disp_blk[b] > d ? R.disp_blk[b] : d;
+    for (int b = threadIdx.x; b < (R.n_z + kFilterBlock - 1) / kFilterBlock; b += blockDim.x)
+      d = R.disp_blk[b] > d ? R.disp_blk[b] : d;
     atomicMax(&dmax_s, d);
     __syncthreads();
   }
@@ -468,96 +469,162 @@ __global__ void __launch_bounds__(kOrderWindow) k_order(const BuildReq* reqs) {
   }
 }
 
-// Filter stage, one warp per source j, lanes over its candidate row: a pure
-// stream of 16-B entries {x_i - Ts z_j (FP32), log2 c} (two batches of 32 in
-// flight). d = (x_i - Ts z_j) - (T - Ts) z_j = x_i - T z_j is tested against
-// the cutoff in FP32 (the reference predicate, inner_product.cpp:69, to
-// ~1e-7 m: only pairs that close to the cutoff can differ from an FP64 test,
-// inside the 1e-6 m tie tolerance). The candidate radius covers cutoff +
-// |T z_j - Ts z_j| (checked: COUNT writes the block's max displacement to
-// disp_blk[], k_tile_offsets flags a violation).
+// Filter stage. A block takes kFilterBlock consecutive sources, a warp
+// kFilterWarp of them: lanes 0..kFilterWarp-1 set up one source each (FP64
+// transforms, candidate row, sweep column). The warp then walks its sources'
+// candidate rows as one sequence of units of kFilterUnit 16-B entries
+// {x_i - Ts z_j (FP32), log2 c}, staged through shared memory by cp.async
+// kFilterStages - 1 units ahead of the unit being tested, so a row's loads
+// overlap the previous rows' tests. d = (x_i - Ts z_j) - (T - Ts) z_j =
+// x_i - T z_j is tested against the cutoff in FP32 (the reference predicate,
+// inner_product.cpp:69, to ~1e-7 m: only pairs that close to the cutoff can
+// differ from an FP64 test, inside the 1e-6 m tie tolerance). The candidate
+// radius covers cutoff + |T z_j - Ts z_j| (checked: COUNT writes the block's
+// max displacement to disp_blk[], k_tile_offsets flags a violation).
 // EMIT=false: count[j]. EMIT=true: j's slots {d, log2 c} (and i) in candidate
 // order into its sliced-ELL column (slot(k) = tile_off[t] + 32 k + lane of its
 // degree-sorted position), padded to the tile's unit-rounded column height.
+constexpr int kFilterUnit = 128;
+constexpr int kFilterStages = 3;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int bytes) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 template <bool EMIT>
-__global__ void __launch_bounds__(256) k_filter(const BuildReq* reqs) {
+__global__ void __launch_bounds__(kFilterThreads) k_filter(const BuildReq* reqs) {
   const BuildReq& R = reqs[blockIdx.y];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int j = blockIdx.x * 8 + wid;
+  if (blockIdx.x * kFilterBlock >= R.n_z) return;
   const bool sup_ok = R.sup_off[R.n_tiles] <= R.sup_capacity;
   if (EMIT && (!sup_ok || R.tile_off[R.n_tiles] > R.capacity)) return;  // host grows and re-runs
-  const bool active = j < R.n_z;
-  double qx = 0, qy = 0, qz = 0, sx = 0, sy = 0, sz = 0;
-  if (active) {
-    apply_T(R.T, R.zx[j], R.zy[j], R.zz[j], qx, qy, qz);
-    apply_T(R.Ts, R.zx[j], R.zy[j], R.zz[j], sx, sy, sz);
+  __shared__ int4 buf[kFilterThreads / 32][kFilterStages][kFilterUnit];
+  const int j = blockIdx.x * kFilterBlock + wid * kFilterWarp + lane;  // lanes < kFilterWarp own a source
+  const bool own = lane < kFilterWarp && j < R.n_z;
+  float ex = 0.f, ey = 0.f, ez = 0.f;
+  int ds = 0, col = 0, height = 0;
+  long long rb = 0, out = 0;
+  unsigned long long d2 = 0;
+  if (own) {
+    double qx, qy, qz, sx, sy, sz;
+    const double zx = R.zx[j], zy = R.zy[j], zz = R.zz[j];
+    apply_T(R.T, zx, zy, zz, qx, qy, qz);
+    apply_T(R.Ts, zx, zy, zz, sx, sy, sz);
+    const double dx = qx - sx, dy = qy - sy, dz = qz - sz;  // (T - Ts) z_j
+    d2 = (unsigned long long)__double_as_longlong(dx * dx + dy * dy + dz * dz);
+    ex = (float)dx; ey = (float)dy; ez = (float)dz;
+    if (sup_ok) {
+      ds = R.sup_count[j];
+      const long long t0 = R.sup_off[j >> 5], H = (R.sup_off[(j >> 5) + 1] - t0) >> 5;
+      rb = t0 + (j & 31) * H;
+    }
+    if (EMIT) {  // tile and lane of j in the degree-sorted order
+      const int p = R.pos[j], ts = p >> 5;
+      out = R.tile_off[ts];
+      col = p & 31;
+      height = (R.unit_off[ts + 1] - R.unit_off[ts]) * kUnitSteps;
+    }
   }
-  if (!EMIT) {
-    __shared__ unsigned long long dblk[8];
-    unsigned long long d2 = 0;
-    if (active) {
-      const double dx = qx - sx, dy = qy - sy, dz = qz - sz;
-      d2 = (unsigned long long)__double_as_longlong(dx * dx + dy * dy + dz * dz);
+  if (!EMIT) {  // block max of |T z - Ts z|^2 (bit patterns of non-negative doubles)
+    __shared__ unsigned long long dblk[kFilterThreads / 32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long v = __shfl_xor_sync(0xffffffffu, d2, o);
+      d2 = v > d2 ? v : d2;
     }
     if (lane == 0) dblk[wid] = d2;
     __syncthreads();
     if (threadIdx.x == 0) {
       unsigned long long m = 0;
-      for (int w = 0; w < 8; ++w) m = dblk[w] > m ? dblk[w] : m;
+      for (int w = 0; w < kFilterThreads / 32; ++w) m = dblk[w] > m ? dblk[w] : m;
       R.disp_blk[blockIdx.x] = m;
     }
   }
-  if (!active) return;
-  // (T - Ts) z_j, the shift from candidate to list coordinates
-  const float ex = (float)(qx - sx), ey = (float)(qy - sy), ez = (float)(qz - sz);
-  int ds = 0;
-  long long rb = 0;
-  if (sup_ok) {
-    ds = R.sup_count[j];
-    const long long t0 = R.sup_off[j >> 5], H = (R.sup_off[(j >> 5) + 1] - t0) >> 5;
-    rb = t0 + (j & 31) * H;
-  }
-  const int4* row = R.sup + rb;
-  long long out = 0;
-  int col = 0;
-  if (EMIT) {  // tile and lane of j in the degree-sorted order
-    const int p = R.pos[j];
-    out = R.tile_off[p >> 5];
-    col = p & 31;
+  // units: (source s, first entry sb) over the sources with candidates
+  const unsigned live = __ballot_sync(0xffffffffu, own && ds > 0);
+  auto next_unit = [&](int& us, int& usb) {
+    usb += kFilterUnit;
+    if (usb >= __shfl_sync(0xffffffffu, ds, us)) {
+      const unsigned rest = live & ~((2u << us) - 1u);
+      us = rest ? __ffs(rest) - 1 : kFilterWarp;
+      usb = 0;
+    }
+  };
+  auto issue = [&](int stage, int us, int usb) {
+    if (us < kFilterWarp) {
+      const int d = __shfl_sync(0xffffffffu, ds, us);
+      const int4* row = R.sup + __shfl_sync(0xffffffffu, rb, us);
+#pragma unroll
+      for (int q = 0; q < kFilterUnit / 32; ++q) {
+        const int k = usb + 32 * q + lane;
+        cp_async16(&buf[wid][stage][32 * q + lane], row + (k < d ? k : 0), k < d ? 16 : 0);
+      }
+    }
+    cp_async_commit();
+  };
+  int is = live ? __ffs(live) - 1 : kFilterWarp, isb = 0;  // issue cursor
+  int ps = is, psb = 0;                                    // test cursor
+#pragma unroll
+  for (int st = 0; st < kFilterStages - 1; ++st) {
+    issue(st, is, isb);
+    if (is < kFilterWarp) next_unit(is, isb);
   }
   const float c2 = (float)R.cutoff_sq;
-  int cnt = 0;
-  for (int sb = 0; sb < ds; sb += 64) {
-    const int k0 = sb + lane, k1 = sb + 32 + lane;
-    int4 e0 = make_int4(0, 0, 0, 0), e1 = make_int4(0, 0, 0, 0);
-    if (k0 < ds) e0 = row[k0];
-    if (k1 < ds) e1 = row[k1];
+  int my_cnt = 0, stage = 0;
+  while (ps < kFilterWarp) {
+    issue((stage + kFilterStages - 1) % kFilterStages, is, isb);
+    if (is < kFilterWarp) next_unit(is, isb);
+    cp_async_wait<kFilterStages - 1>();
+    const int dss = __shfl_sync(0xffffffffu, ds, ps);
+    const float fx = __shfl_sync(0xffffffffu, ex, ps), fy = __shfl_sync(0xffffffffu, ey, ps),
+                fz = __shfl_sync(0xffffffffu, ez, ps);
+    int cnt = __shfl_sync(0xffffffffu, my_cnt, ps);
+    long long outs = 0, rbs = 0;
+    int cols = 0;
+    if (EMIT) {
+      outs = __shfl_sync(0xffffffffu, out, ps);
+      cols = __shfl_sync(0xffffffffu, col, ps);
+      if (R.write_index) rbs = __shfl_sync(0xffffffffu, rb, ps);
+    }
+    const int c0 = cnt;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int k = h ? k1 : k0;
-      const int4 e = h ? e1 : e0;
-      const float dx = __int_as_float(e.x) - ex, dy = __int_as_float(e.y) - ey, dz = __int_as_float(e.z) - ez;
-      const bool keep = k < ds && fmaf(dx, dx, fmaf(dy, dy, dz * dz)) <= c2;
+    for (int q = 0; q < kFilterUnit / 32; ++q) {
+      const int k = psb + 32 * q + lane;
+      const int4 e = buf[wid][stage][32 * q + lane];
+      const float dx = __int_as_float(e.x) - fx, dy = __int_as_float(e.y) - fy, dz = __int_as_float(e.z) - fz;
+      const bool keep = k < dss && fmaf(dx, dx, fmaf(dy, dy, dz * dz)) <= c2;
       const unsigned m = __ballot_sync(0xffffffffu, keep);
       if (EMIT && keep) {
-        const long long at = slot_index(out, col, cnt + __popc(m & ((1u << lane) - 1u)));
+        const long long at = slot_index(outs, cols, cnt + __popc(m & ((1u << lane) - 1u)));
         // x_i - T_b z_j in FP32 (|.| <= cutoff): the sweep forms d = x_i - T z_j
         // as this minus the source's displacement (T - T_b) z_j
         R.slots[at] = make_int4(__float_as_int(dx), __float_as_int(dy), __float_as_int(dz), e.w);
-        if (R.write_index) R.slot_i[at] = R.sup_i[rb + k];  // export only
+        if (R.write_index) R.slot_i[at] = R.sup_i[rbs + k];  // export only
       }
       cnt += __popc(m);
     }
+    if (lane == ps) my_cnt += cnt - c0;
+    next_unit(ps, psb);
+    stage = (stage + 1) % kFilterStages;
   }
+  cp_async_wait<0>();
   if (!EMIT) {
-    if (lane == 0) R.count[j] = cnt;
+    if (own) R.count[j] = my_cnt;
   } else {
-    // pad the column to the tile's unit-rounded height: w = ex2(-inf) = 0
-    const int ts = R.pos[j] >> 5;
-    const int height = (R.unit_off[ts + 1] - R.unit_off[ts]) * kUnitSteps;
-    for (int k = cnt + lane; k < height; k += 32) {
-      R.slots[slot_index(out, col, k)] = make_int4(0, 0, 0, __float_as_int(-INFINITY));
-      if (R.write_index) R.slot_i[slot_index(out, col, k)] = -1;
+    // pad each column to its tile's unit-rounded height: w = ex2(-inf) = 0
+#pragma unroll 1
+    for (int s = 0; s < kFilterWarp; ++s) {
+      const int hs = __shfl_sync(0xffffffffu, height, s), cs = __shfl_sync(0xffffffffu, my_cnt, s);
+      const long long outs = __shfl_sync(0xffffffffu, out, s);
+      const int cols = __shfl_sync(0xffffffffu, col, s);
+      for (int k = cs + lane; k < hs; k += 32) {
+        R.slots[slot_index(outs, cols, k)] = make_int4(0, 0, 0, __float_as_int(-INFINITY));
+        if (R.write_index) R.slot_i[slot_index(outs, cols, k)] = -1;
+      }
     }
   }
 }
@@ -1264,11 +1331,11 @@ void build_pairs_batched(const BuildReq* h, const BuildReq* d, int n, cudaStream
     k_pair_pass<true><<<gz, 256, 0, st>>>(d);
     launches += 9;
   }
-  const dim3 gt(max(1, (max_nz + 7) / 8), n);  // warp per source
-  k_filter<false><<<gt, 256, 0, st>>>(d);
+  const dim3 gt(max(1, (max_nz + kFilterBlock - 1) / kFilterBlock), n);
+  k_filter<false><<<gt, kFilterThreads, 0, st>>>(d);
   k_order<<<dim3(max(1, (max_nz + kOrderWindow - 1) / kOrderWindow), n), kOrderWindow, 0, st>>>(d);
   k_tile_offsets<false><<<n, 1024, 0, st>>>(d);
-  k_filter<true><<<gt, 256, 0, st>>>(d);
+  k_filter<true><<<gt, kFilterThreads, 0, st>>>(d);
   k_chunk_records<<<dim3(kMaxChunks / 8, n), 256, 0, st>>>(d);
   count_launch(launches + 5);
 }
@@ -1323,7 +1390,7 @@ void displacement(const double* zx, const double* zy, const double* zz, int n, c
 }
 
 void filter_emit_index(const BuildReq* d, int n_z, cudaStream_t st) {
-  k_filter<true><<<dim3(max(1, (n_z + 7) / 8), 1), 256, 0, st>>>(d);
+  k_filter<true><<<dim3(max(1, (n_z + kFilterBlock - 1) / kFilterBlock), 1), kFilterThreads, 0, st>>>(d);
   count_launch();
 }
 
