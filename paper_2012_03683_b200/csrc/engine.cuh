@@ -53,8 +53,14 @@ constexpr int kQueueDepth = 8;                   // chunks a warp may hold in it
 constexpr int kMaxSweepReqs = KREG_MAX_SWEEP_REQS;  // requests per sweep launch (<= kSweepThreads)
 constexpr int kChunkGroup = 32;                  // chunk partials summed per group (first reduction level)
 constexpr int kMaxChunkGroups = (kMaxChunks + kChunkGroup - 1) / kChunkGroup;
-constexpr int kFilterWarp = 8;       // sources per warp of the filter stage
-constexpr int kFilterThreads = 128;  // threads per filter block
+#ifndef KREG_FILTER_WARP
+#define KREG_FILTER_WARP 8
+#endif
+#ifndef KREG_FILTER_THREADS
+#define KREG_FILTER_THREADS 128
+#endif
+constexpr int kFilterWarp = KREG_FILTER_WARP;        // sources per warp of the filter stage
+constexpr int kFilterThreads = KREG_FILTER_THREADS;  // threads per filter block
 constexpr int kFilterBlock = kFilterThreads / 32 * kFilterWarp;  // sources per filter block (one disp_blk entry)
 constexpr int kDispItem = 512;                   // sources per displacement work item
 // Sliced-ELL slot of step k of the source in lane l of a tile starting at slot
@@ -124,6 +130,7 @@ struct BuildReq {
   int* tmp_items;        // n_x
   int* cell_items;       // n_x
   double* cx; double* cy; double* cz;  // n_x cell-ordered positions
+  float* cfeat;          // n_x x fstride cell-ordered feature rows (16-B aligned)
   long long* scan_tiles; // cell-scan workspace (tile sums)
   int* sup_count;        // n_z: candidates of every source
   long long* sup_off;    // n_tiles + 1: candidate tile offsets (entries)
@@ -142,7 +149,7 @@ struct BuildReq {
   int* unit_off;         // n_tiles + 1: sweep work-unit offsets
   float4* zs;            // n_z: sources in degree-sorted order (FP32)
   ChunkRec* chunks;      // kMaxChunks sweep chunk records
-  int4* slots;           // capacity slots {x_i - T_b z_j (3 x FP32), log2 c (FP32)}
+  int4* slots;           // capacity slots {x_i - Ts z_j (3 x FP32), log2 c (FP32)}
   int* slot_i;           // capacity: target index i of every slot (export only)
   int write_index;       // emit also writes slot_i (export re-runs the emit with it set)
   long long capacity;
@@ -169,7 +176,7 @@ struct alignas(16) SweepReq {
   int M;
   double T[kMaxCandidates][12];
   double Tb[12];         // pair-list build transform (displacement reference)
-  float Td[kMaxCandidates][12];  // {R_m - R_b, t_m - t_b}: source displacement (T_m - T_b) z
+  float Td[kMaxCandidates][12];  // {R_m - R_s, t_m - t_s}: (T_m - T_s) z, T_s the slots' frame
   float Ta[kMaxCandidates][12];  // {R_m, t_m - anchor}: T_m z - anchor (torque arm)
   double anchor[3];
   float kappa;           // -log2(e) / (2 l^2): ex2 argument per m^2

@@ -470,6 +470,12 @@ static void prepare_build(kreg_ctx* ctx, BuildJob& job, kreg_dev::BuildReq& R) {
   if (!reuse) {
     R.full = 1;
     ++ctx->full_builds;
+    // why: 0 no resident list, 1 forced (overflow / guard), 2 moved beyond
+    // the candidate radius, 3 other (clouds, coefficients, skin)
+    const int why = !p->sup_valid ? 0 : job.force_full ? 1
+                    : (p->sup_X == X && p->sup_Z == Z && job.disp_hint >= 0.0 && ctx->skin > 0.0 &&
+                       std::memcmp(&p->sup_cp, &R.cp, sizeof(R.cp)) == 0) ? 2 : 3;
+    ++ctx->full_why[why];
     ++p->full_builds;
     const double rs = cutoff * (1.0 + std::max(0.0, ctx->skin));
     p->sup_valid = false;  // until this round's results are read back
@@ -515,6 +521,7 @@ static void prepare_build(kreg_ctx* ctx, BuildJob& job, kreg_dev::BuildReq& R) {
   p->sup_count.ensure(nz + 1);
   p->sup_off.ensure(n_tiles + 2);
   std::memcpy(R.Ts, p->sup_T, sizeof(R.Ts));
+  std::memcpy(p->slot_T, p->sup_T, sizeof(p->slot_T));
   R.sup_count = p->sup_count.ptr;
   R.sup_off = p->sup_off.ptr;
   R.sup = p->sup.ptr;
@@ -595,10 +602,10 @@ static void prepare_sweep(EvalJob& job, kreg_dev::SweepReq& R, double* partials,
   std::memcpy(R.Tb, p->T_build, sizeof(R.Tb));
   for (int k = 0; k < 3; ++k) R.anchor[k] = p->anchor[k];
   for (int m = 0; m < job.M; ++m) {
-    // {R_m - R_b, t_m - t_b} and {R_m, t_m - anchor} in FP32 (the sweep
-    // forms (T_m - T_b) z and T_m z - anchor per source)
+    // {R_m - R_s, t_m - t_s} (s: the slots' frame) and {R_m, t_m - anchor}
+    // in FP32 (the sweep forms (T_m - T_s) z and T_m z - anchor per source)
     for (int k = 0; k < 12; ++k) {
-      R.Td[m][k] = static_cast<float>(job.T[m][k] - p->T_build[k]);
+      R.Td[m][k] = static_cast<float>(job.T[m][k] - p->slot_T[k]);
       R.Ta[m][k] = static_cast<float>(job.T[m][k] - ((k % 4) == 3 ? p->anchor[k / 4] : 0.0));
     }
   }
@@ -613,9 +620,10 @@ static void prepare_sweep(EvalJob& job, kreg_dev::SweepReq& R, double* partials,
 // Grid buffers of the round's grid searches, carved from one arena per round
 // slot (cell counts stay zero between rounds: k_scatter consumes them).
 static void assign_grid_arena(RoundSlot& S, kreg_dev::BuildReq* reqs, int nb) {
-  size_t cells = 0, pts = 0, tiles = 0;
+  size_t cells = 0, pts = 0, tiles = 0, feats = 0;
   for (int b = 0; b < nb; ++b) {
     if (!reqs[b].full) continue;
+    feats += static_cast<size_t>(reqs[b].n_x) * reqs[b].cp.fstride + 4;
     cells += static_cast<size_t>(reqs[b].n_cells) + 2;
     pts += static_cast<size_t>(reqs[b].n_x) + 2;
     tiles += static_cast<size_t>(reqs[b].n_cells / kreg_dev::kScanTile) + 4;
@@ -626,7 +634,8 @@ static void assign_grid_arena(RoundSlot& S, kreg_dev::BuildReq* reqs, int nb) {
   S.g_int.ensure(3 * pts, false, 1.5);
   S.g_pos.ensure(3 * pts, false, 1.5);
   S.g_scan.ensure(tiles, false, 1.5);
-  size_t oc = 0, op = 0, ot = 0;
+  S.g_feat.ensure(feats + 4, false, 1.5);
+  size_t oc = 0, op = 0, ot = 0, of = 0;
   for (int b = 0; b < nb; ++b) {
     kreg_dev::BuildReq& R = reqs[b];
     if (!R.full) continue;
@@ -640,6 +649,8 @@ static void assign_grid_arena(RoundSlot& S, kreg_dev::BuildReq* reqs, int nb) {
     R.cy = R.cx + np;
     R.cz = R.cy + np;
     R.scan_tiles = S.g_scan.ptr + ot;
+    R.cfeat = S.g_feat.ptr + of;  // fstride is a multiple of 4: rows stay 16-B aligned
+    of += (static_cast<size_t>(R.n_x) * R.cp.fstride + 3) / 4 * 4;
     oc += static_cast<size_t>(R.n_cells) + 2;
     op += np;
     ot += static_cast<size_t>(R.n_cells / kreg_dev::kScanTile) + 4;
@@ -837,6 +848,15 @@ void end_round(kreg_ctx* ctx, RoundSlot& S) {
       float ms = 0.0f;
       KREG_CUDA(cudaEventElapsedTime(&ms, S.ev0, S.ev1));
       ctx->sweep_ms += ms;
+      if (trace) {
+        int n_grad = 0, m_sum = 0;
+        for (int e = 0; e < ne; ++e) {
+          n_grad += evals[e].grad ? 1 : 0;
+          m_sum += evals[e].M;
+        }
+        std::fprintf(stderr, "kreg-sweep ms=%.4f requests=%d grad=%d m=%d slots=%lld builds=%d\n", ms, ne, n_grad,
+                     m_sum, round_slots, nb);
+      }
     }
   }
 }

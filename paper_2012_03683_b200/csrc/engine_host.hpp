@@ -163,6 +163,7 @@ struct kreg_ctx {
   // rounds with builds, candidate entries the filters scanned, slots emitted
   double build_ms = 0.0;
   long long build_rounds = 0, filter_entries = 0, built_slots = 0;
+  long long full_why[4] = {0, 0, 0, 0};  // grid builds by cause (prepare_build)
   kreg_host::Collective collective;  // row-sharded registrations (kreg_ctx_set_collective)
   // host-side round accounting (seconds)
   long long rounds = 0;
@@ -214,6 +215,9 @@ struct kreg_pairs {
   const kreg_cloud* sup_Z = nullptr;
   kreg_dev::CoeffParams sup_cp{};          // coefficient parameters it was built with
   double sup_T[12] = {1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1, 0};
+  // frame of the sweep-list slots: a slot holds x_i - slot_T z_j (the
+  // candidate entry it was filtered from); the sweep subtracts (T - slot_T) z_j
+  double slot_T[12] = {1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1, 0};
   double sup_radius = 0.0;                 // R_s
   double sup_disp = 0.0;                   // max_j |T_build z_j - sup_T z_j|
   long long sup_entries = 0;
@@ -314,6 +318,7 @@ struct RoundSlot {
   // positions, scan tiles
   DevBuf<int> g_count, g_start, g_int;
   DevBuf<double> g_pos;
+  DevBuf<float> g_feat;
   DevBuf<long long> g_scan;
   cudaEvent_t done = nullptr, ev0 = nullptr, ev1 = nullptr, evb0 = nullptr, evb1 = nullptr;
   std::vector<BuildJob> builds;

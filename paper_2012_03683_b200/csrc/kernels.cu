@@ -134,6 +134,12 @@ __global__ void k_rank(const BuildReq* reqs) {
   R.cx[dst] = R.xx[i];
   R.cy[dst] = R.xy[i];
   R.cz[dst] = R.xz[i];
+  // feature rows in cell order: the candidate search reads a stencil row's
+  // features contiguously instead of gathering them by point index
+  const int fs = R.cp.fstride;
+  const float4* src = reinterpret_cast<const float4*>(R.xfeat + (long long)i * fs);
+  float4* dstf = reinterpret_cast<float4*>(R.cfeat + (long long)dst * fs);
+  for (int d = 0; d < (fs >> 2); ++d) dstf[d] = src[d];
 }
 
 // ---------------------------------------- exclusive scan of the cell counts
@@ -297,7 +303,7 @@ __global__ void __launch_bounds__(256) k_pair_pass(const BuildReq* reqs) {
             dz2 = R.cz[s] - qz;
             if (dx * dx + dy2 * dy2 + dz2 * dz2 <= R.sup_cutoff_sq) {
               i = R.cell_items[s];
-              keep = geo ? true : coefficient(R.cp, R.xfeat + (long long)i * fs, zf, &lc);
+              keep = geo ? true : coefficient(R.cp, R.cfeat + (long long)s * fs, zf, &lc);
             }
           }
           const unsigned m = __ballot_sync(0xffffffffu, keep);
@@ -484,8 +490,11 @@ __global__ void __launch_bounds__(kOrderWindow) k_order(const BuildReq* reqs) {
 // EMIT=false: count[j]. EMIT=true: j's slots {d, log2 c} (and i) in candidate
 // order into its sliced-ELL column (slot(k) = tile_off[t] + 32 k + lane of its
 // degree-sorted position), padded to the tile's unit-rounded column height.
+#ifndef KREG_FILTER_STAGES
+#define KREG_FILTER_STAGES 3
+#endif
 constexpr int kFilterUnit = 128;
-constexpr int kFilterStages = 3;
+constexpr int kFilterStages = KREG_FILTER_STAGES;
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int bytes) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
@@ -600,9 +609,10 @@ __global__ void __launch_bounds__(kFilterThreads) k_filter(const BuildReq* reqs)
       const unsigned m = __ballot_sync(0xffffffffu, keep);
       if (EMIT && keep) {
         const long long at = slot_index(outs, cols, cnt + __popc(m & ((1u << lane) - 1u)));
-        // x_i - T_b z_j in FP32 (|.| <= cutoff): the sweep forms d = x_i - T z_j
-        // as this minus the source's displacement (T - T_b) z_j
-        R.slots[at] = make_int4(__float_as_int(dx), __float_as_int(dy), __float_as_int(dz), e.w);
+        // the candidate entry itself, x_i - Ts z_j: the sweep forms
+        // d = x_i - T z_j as this minus (T - Ts) z_j, and a later filter of
+        // this list reproduces a filter of the candidate list bit for bit
+        R.slots[at] = e;
         if (R.write_index) R.slot_i[at] = R.sup_i[rbs + k];  // export only
       }
       cnt += __popc(m);
@@ -670,8 +680,8 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 
 // Fused F + gradient sweep over the sliced-ELL pair list.
 //  * Work unit = one tile of 32 degree-sorted sources x kUnitSteps degree
-//    steps = kUnitSlots contiguous 16-B slots {x_i - T_b z_j (FP32 x3),
-//    log2 c_ij}; lane l owns the source at sorted position 32 t + l, so the
+//    steps = kUnitSlots contiguous 16-B slots {x_i - T_s z_j (FP32 x3),
+//    log2 c_ij} (T_s: the candidate list's transform); lane l owns the source at sorted position 32 t + l, so the
 //    per-source moments stay in registers.
 //  * A request's units are cut into chunk_count(U) chunks. The chunks of all
 //    requests of a launch form one queue; every warp of a persistent grid
@@ -680,8 +690,8 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 //    chunk boundaries. A chunk's first stage also carries its ChunkRec (first
 //    tile + its sources), later tiles' sources are prefetched one tile ahead:
 //    the stream has no dependent global loads.
-//  * Per tile and candidate m (FP32): delta = (R_m - R_b) z_j + (t_m - t_b)
-//    and the torque arm a_j = T_m z_j - anchor. Per slot: d = (x_i - T_b z_j)
+//  * Per tile and candidate m (FP32): delta = (R_m - R_s) z_j + (t_m - t_s)
+//    and the torque arm a_j = T_m z_j - anchor. Per slot: d = (x_i - T_s z_j)
 //    - delta = x_i - T_m z_j, r^2, w = ex2(r^2 kappa + log2 c) on MUFU, W += w,
 //    S += w d; candidates in pairs on FFMA2/FADD2/FMUL2. Per tile: torque +=
 //    a_j x S_j (sum_j q_j x S_j = sum_j (q_j - a) x S_j + a x sum S).

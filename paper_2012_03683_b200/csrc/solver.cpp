@@ -169,9 +169,12 @@ void finish(Reg& r) {
 // histogram (index 21 = search failed), printed to stderr at exit.
 struct SearchStats {
   long long hist[22] = {};
+  long long level_builds = 0, level_subset = 0;  // level-change rebuilds; of them, new pairs within the old list
   bool on = std::getenv("KREG_STATS") != nullptr;
   ~SearchStats() {
     if (!on) return;
+    std::fprintf(stderr, "kreg level-change rebuilds %lld, of which moved < cutoff shrink: %lld\n", level_builds,
+                 level_subset);
     std::fprintf(stderr, "kreg line-search accepted-k histogram:");
     for (int k = 0; k < 22; ++k) std::fprintf(stderr, " %lld", hist[k]);
     std::fprintf(stderr, "\n");
@@ -287,6 +290,11 @@ void plan(Reg& r, std::vector<BuildJob>& builds, std::vector<EvalJob>& evals, st
             !r.have_eval) {
           const bool must = r.pairs->built_at_lengthscale != r.lengthscale || r.ev[7] > 0.5 * r.pairs->cutoff_radius;
           if (must) {
+            if (g_search_stats.on && r.pairs->built_at_lengthscale != r.lengthscale && r.have_eval) {
+              ++g_search_stats.level_builds;
+              if (r.ev[7] <= r.pairs->cutoff_radius - r.cfg.cutoff_multiplier * r.lengthscale)
+                ++g_search_stats.level_subset;
+            }
             r.rebuilt = true;
             schedule_build_eval(r, builds, evals, owners);
             r.phase = Phase::kAwaitEval;

@@ -12,6 +12,8 @@ from paper_2012_03683_b200 import api, synth
 B = int(os.environ.get("B", "32"))
 skins = [float(s) for s in os.environ.get("SKINS", "0,0.25,0.5,1.0").split(",")]
 ctx = api.default_context()
+if os.environ.get("W"):
+    ctx.set_max_active(int(os.environ["W"]))
 Xs, Zs, inits = bench.make_workload(0, B, 40000)
 p, cfg = synth.kitti_params(), synth.kitti_subsequent_config()
 dX = [api.DeviceCloud(x, ctx) for x in Xs]
