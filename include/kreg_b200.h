@@ -185,9 +185,9 @@ kreg_status kreg_ctx_build_stats(const kreg_ctx* ctx, int64_t out[2]);
  * out = {device ms of build launches, rounds with builds, candidate entries
  * scanned by the builds, sweep-list slots emitted, grid builds without a
  * resident candidate list, forced by an overflow or guard, after moving beyond
- * the candidate radius, for other causes}. Diagnostic; no reference
- * counterpart. */
-kreg_status kreg_ctx_build_profile(const kreg_ctx* ctx, double out[8]);
+ * the candidate radius, for other causes, filter builds that read the
+ * resident sweep list}. Diagnostic; no reference counterpart. */
+kreg_status kreg_ctx_build_profile(const kreg_ctx* ctx, double out[9]);
 
 /* Multi-GPU source-row sharding (configuration C4): every
  * rank registers the replicated target X against its own rows of the source

@@ -165,12 +165,12 @@ class Context:
     def build_stats(self):
         out = np.zeros(2, dtype=np.int64)
         _check(lib().kreg_ctx_build_stats(self.h, _abi.as_ptr(out, C.c_int64)))
-        prof = np.zeros(8)
+        prof = np.zeros(9)
         _check(lib().kreg_ctx_build_profile(self.h, _abi.as_ptr(prof)))
         return {"grid_builds": int(out[0]), "filter_builds": int(out[1]), "build_ms": float(prof[0]),
                 "build_rounds": int(prof[1]), "filter_entries": int(prof[2]), "built_slots": int(prof[3]),
                 "grid_why": {"no_list": int(prof[4]), "forced": int(prof[5]), "moved": int(prof[6]),
-                             "other": int(prof[7])}}
+                             "other": int(prof[7])}, "refilter_builds": int(prof[8])}
 
     def host_stats(self):
         out = np.zeros(8)

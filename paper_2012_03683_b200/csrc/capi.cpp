@@ -238,7 +238,7 @@ kreg_status kreg_ctx_build_stats(const kreg_ctx* ctx, int64_t out[2]) {
   });
 }
 
-kreg_status kreg_ctx_build_profile(const kreg_ctx* ctx, double out[8]) {
+kreg_status kreg_ctx_build_profile(const kreg_ctx* ctx, double out[9]) {
   return guarded([&] {
     require(ctx != nullptr && out != nullptr, "NULL argument");
     out[0] = ctx->build_ms;
@@ -246,6 +246,7 @@ kreg_status kreg_ctx_build_profile(const kreg_ctx* ctx, double out[8]) {
     out[2] = static_cast<double>(ctx->filter_entries);
     out[3] = static_cast<double>(ctx->built_slots);
     for (int k = 0; k < 4; ++k) out[4 + k] = static_cast<double>(ctx->full_why[k]);
+    out[8] = static_cast<double>(ctx->refilter_builds);
   });
 }
 
@@ -329,6 +330,7 @@ kreg_status kreg_ctx_reset_stats(kreg_ctx* ctx) {
     ctx->build_ms = 0.0;
     ctx->build_rounds = ctx->filter_entries = ctx->built_slots = 0;
     for (long long& w : ctx->full_why) w = 0;
+    ctx->refilter_builds = 0;
   });
 }
 

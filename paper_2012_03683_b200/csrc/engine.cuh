@@ -62,6 +62,7 @@ constexpr int kMaxChunkGroups = (kMaxChunks + kChunkGroup - 1) / kChunkGroup;
 constexpr int kFilterWarp = KREG_FILTER_WARP;        // sources per warp of the filter stage
 constexpr int kFilterThreads = KREG_FILTER_THREADS;  // threads per filter block
 constexpr int kFilterBlock = kFilterThreads / 32 * kFilterWarp;  // sources per filter block (one disp_blk entry)
+static_assert(kFilterBlock == 32, "the sweep-list refilter writes one disp_blk entry per 32-source tile");
 constexpr int kDispItem = 512;                   // sources per displacement work item
 // Sliced-ELL slot of step k of the source in lane l of a tile starting at slot
 // tile_off: units of kUnitSteps = 2 steps x 32 sources, source-major inside a
@@ -155,6 +156,17 @@ struct BuildReq {
   long long capacity;
   unsigned long long* disp_blk;   // ceil(n_z / kFilterBlock): per filter block max |T z - Ts z|^2 (bits)
   int chunk_pref;        // sweep chunking of this list (chunk_units)
+  // refilter = 1: the filter stage reads the resident sweep list (old_*,
+  // built at old_T with a cutoff that covers this one: new pairs are a
+  // subset) instead of the candidate list; same predicate on the same
+  // entries, so the result equals a candidate-list filter bit for bit
+  int refilter;
+  double old_T[12];
+  const int4* old_slots;
+  const int* old_perm;
+  const int* old_deg_s;
+  const long long* old_tile_off;
+  const int* old_unit_off;
   double* status;        // kBuildStatus: {P, slots > cap, slots, cand > cap, cand, |T-Ts| disp, invalid, -}
 };
 constexpr int kBuildStatus = 8;

@@ -446,6 +446,16 @@ static void prepare_build(kreg_ctx* ctx, BuildJob& job, kreg_dev::BuildReq& R) {
   const bool reuse = !job.force_full && ctx->skin > 0.0 && p->sup_valid && p->sup_X == X && p->sup_Z == Z &&
                      std::memcmp(&p->sup_cp, &R.cp, sizeof(R.cp)) == 0 && job.disp_hint >= 0.0 &&
                      p->sup_disp + job.disp_hint + cutoff <= p->sup_radius - 2.0 * margin;
+  // ... and the resident sweep list, filtered from that candidate list at
+  // T_build with the old cutoff, holds every pair of the new list when
+  // max_j |T z_j - T_build z_j| + cutoff <= old cutoff (annealing shrinks the
+  // cutoff; guard: FP32 rounding of the two predicates). Checked in-kernel.
+  const double guard = 1e-5 * p->cutoff_radius;
+  const double sub_limit = p->cutoff_radius - cutoff - guard;
+  const bool refilter = reuse && ctx->refilter && !job.no_refilter && p->counts_valid && p->slots > 0 &&
+                        p->n_tiles == (Z->n + 31) / 32 && job.disp_hint <= sub_limit;
+  double old_T[12];
+  std::memcpy(old_T, p->T_build, sizeof(old_T));
 
   p->ctx = ctx;
   p->X = X;
@@ -518,6 +528,34 @@ static void prepare_build(kreg_ctx* ctx, BuildJob& job, kreg_dev::BuildReq& R) {
     ++ctx->filter_builds;
     ++p->filter_builds;
   }
+  if (refilter) {
+    // the current sweep list becomes the source (alt_*), the build writes
+    // the other buffer set
+    ++ctx->refilter_builds;
+    p->alt_slot_buf.ensure(p->slot_buf.cap, false, 1.0);
+    p->alt_perm.ensure(p->perm.cap, false, 1.0);
+    p->alt_pos.ensure(p->pos.cap, false, 1.0);
+    p->alt_deg_s.ensure(p->deg_s.cap, false, 1.0);
+    p->alt_tile_off.ensure(p->tile_off.cap, false, 1.0);
+    p->alt_unit_off.ensure(p->unit_off.cap, false, 1.0);
+    p->alt_zs.ensure(p->zs.cap, false, 1.0);
+    p->alt_chunks.ensure(p->chunks.cap, false, 1.0);
+    p->slot_buf.swap(p->alt_slot_buf);
+    p->perm.swap(p->alt_perm);
+    p->pos.swap(p->alt_pos);
+    p->deg_s.swap(p->alt_deg_s);
+    p->tile_off.swap(p->alt_tile_off);
+    p->unit_off.swap(p->alt_unit_off);
+    p->zs.swap(p->alt_zs);
+    p->chunks.swap(p->alt_chunks);
+    R.refilter = 1;
+    std::memcpy(R.old_T, old_T, sizeof(R.old_T));
+    R.old_slots = p->alt_slot_buf.ptr;
+    R.old_perm = p->alt_perm.ptr;
+    R.old_deg_s = p->alt_deg_s.ptr;
+    R.old_tile_off = p->alt_tile_off.ptr;
+    R.old_unit_off = p->alt_unit_off.ptr;
+  }
   p->sup_count.ensure(nz + 1);
   p->sup_off.ensure(n_tiles + 2);
   std::memcpy(R.Ts, p->sup_T, sizeof(R.Ts));
@@ -527,7 +565,7 @@ static void prepare_build(kreg_ctx* ctx, BuildJob& job, kreg_dev::BuildReq& R) {
   R.sup = p->sup.ptr;
   R.sup_i = p->sup_i.ptr;
   R.sup_capacity = static_cast<long long>(p->sup.cap);
-  const double limit = p->sup_radius - cutoff - margin;
+  const double limit = refilter ? sub_limit : p->sup_radius - cutoff - margin;
   R.filter_limit_sq = limit > 0.0 ? limit * limit : 0.0;
 
   // torque arm origin of the sweep (FP32 arms T z - anchor stay small)
@@ -706,7 +744,10 @@ void begin_round(kreg_ctx* ctx, RoundSlot& S, std::vector<BuildJob>&& builds_in,
   }
   assign_grid_arena(S, S.h_build.ptr, nb);
   for (int b = 0; b < nb; ++b) {
+    // (a refilter's list equals the candidate-list filter's: the export
+    // re-runs the latter's emit)
     builds[b].pairs->last_req = S.h_build.ptr[b];
+    builds[b].pairs->last_req.refilter = 0;
     builds[b].pairs->index_valid = false;
   }
   const auto tb = clk::now();
@@ -788,22 +829,30 @@ void end_round(kreg_ctx* ctx, RoundSlot& S) {
         p->expected_sup = std::max(p->expected_sup, p->sup_entries);
       }
     }
-    if (ok && st[6] != 0.0) {  // candidate radius did not cover the move (rounding guard)
-      p->sup_valid = false;
-      job.force_full = true;
+    const bool refilter = S.h_build.ptr[b].refilter != 0;
+    if (ok && st[6] != 0.0) {
+      if (refilter) {  // the sweep list did not cover the new cutoff: filter the candidate list
+        job.no_refilter = true;
+      } else {  // candidate radius did not cover the move (rounding guard)
+        p->sup_valid = false;
+        job.force_full = true;
+      }
       ok = false;
     }
     p->P = static_cast<long long>(st[0]);
     p->slots = static_cast<long long>(st[2]);
     if (st[1] != 0.0) {
       p->expected_pairs = static_cast<long long>(st[2] * 1.15) + 1024;
+      if (refilter) job.no_refilter = true;
       ok = false;
     } else {
       p->expected_pairs = std::max(p->expected_pairs, p->slots);
     }
     p->counts_valid = ok;
     if (ok) {
-      p->sup_disp = st[5];
+      // max_j |T_build z_j - Ts z_j|: measured by a candidate-list filter; a
+      // refilter measured |T_build z_j - old T_build z_j| (triangle bound)
+      p->sup_disp = refilter ? p->sup_disp + st[5] : st[5];
     } else {
       redo.push_back(b);
     }

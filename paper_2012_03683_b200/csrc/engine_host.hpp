@@ -15,6 +15,7 @@
 #include <cstdlib>
 #include <memory>
 #include <stdexcept>
+#include <utility>
 #include <string>
 #include <vector>
 
@@ -56,6 +57,11 @@ struct DevBuf {
     owned = true;
   }
   bool owned = true;  // false: points into memory owned elsewhere (a context arena)
+  void swap(DevBuf& o) {
+    std::swap(ptr, o.ptr);
+    std::swap(cap, o.cap);
+    std::swap(owned, o.owned);
+  }
   void borrow(T* p, size_t n) {
     release();
     ptr = p;
@@ -164,6 +170,11 @@ struct kreg_ctx {
   double build_ms = 0.0;
   long long build_rounds = 0, filter_entries = 0, built_slots = 0;
   long long full_why[4] = {0, 0, 0, 0};  // grid builds by cause (prepare_build)
+  long long refilter_builds = 0;         // filter builds that read the resident sweep list
+  // sweep-list refilters (opt-in, KREG_REFILTER=1: equal results, but their
+  // warp-per-tile kernels are load-imbalanced and measured slower than the
+  // candidate-list filter on the KITTI batch)
+  bool refilter = std::getenv("KREG_REFILTER") != nullptr;
   kreg_host::Collective collective;  // row-sharded registrations (kreg_ctx_set_collective)
   // host-side round accounting (seconds)
   long long rounds = 0;
@@ -232,6 +243,13 @@ struct kreg_pairs {
   kreg_host::DevBuf<float4> zs;                 // sources in sweep order (FP32)
   kreg_host::DevBuf<kreg_dev::ChunkRec> chunks; // sweep chunk records
   kreg_host::DevBuf<unsigned long long> disp_blk;
+  // the previous sweep list while a refilter build reads it (swapped with
+  // the buffers above at every refilter build)
+  kreg_host::DevBuf<int> alt_perm, alt_pos, alt_deg_s, alt_unit_off;
+  kreg_host::DevBuf<long long> alt_tile_off;
+  kreg_host::DevBuf<int4> alt_slot_buf;
+  kreg_host::DevBuf<float4> alt_zs;
+  kreg_host::DevBuf<kreg_dev::ChunkRec> alt_chunks;
   int n_tiles = 0;
   long long slots = 0;                     // valid after the build round
   bool counts_valid = false;               // P / slots known on the host
@@ -290,6 +308,7 @@ struct BuildJob {
   // unknown); lets the build reuse the resident candidate list
   double disp_hint = -1.0;
   bool force_full = false;
+  bool no_refilter = false;  // filter the candidate list even if the sweep list covers the new one
 };
 
 // One evaluation request: M (<= 8) transforms against a built pair list.

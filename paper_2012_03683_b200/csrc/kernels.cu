@@ -504,11 +504,30 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+// The filter predicate on one candidate entry e = {x_i - Ts z_j, log2 c}
+// given the source shift (T - Ts) z_j in FP32; shared by both filter paths so
+// they decide identically.
+__device__ __forceinline__ void filter_shift(const BuildReq& R, int j, float& ex, float& ey, float& ez,
+                                             unsigned long long& d2) {
+  double qx, qy, qz, sx, sy, sz;
+  const double zx = R.zx[j], zy = R.zy[j], zz = R.zz[j];
+  apply_T(R.T, zx, zy, zz, qx, qy, qz);
+  apply_T(R.Ts, zx, zy, zz, sx, sy, sz);
+  const double dx = qx - sx, dy = qy - sy, dz = qz - sz;  // (T - Ts) z_j
+  d2 = (unsigned long long)__double_as_longlong(dx * dx + dy * dy + dz * dz);
+  ex = (float)dx; ey = (float)dy; ez = (float)dz;
+}
+__device__ __forceinline__ bool filter_keep(const int4& e, float ex, float ey, float ez, float c2) {
+  const float dx = __fsub_rn(__int_as_float(e.x), ex), dy = __fsub_rn(__int_as_float(e.y), ey),
+              dz = __fsub_rn(__int_as_float(e.z), ez);
+  return __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz))) <= c2;
+}
+
 template <bool EMIT>
 __global__ void __launch_bounds__(kFilterThreads) k_filter(const BuildReq* reqs) {
   const BuildReq& R = reqs[blockIdx.y];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  if (blockIdx.x * kFilterBlock >= R.n_z) return;
+  if (R.refilter || blockIdx.x * kFilterBlock >= R.n_z) return;
   const bool sup_ok = R.sup_off[R.n_tiles] <= R.sup_capacity;
   if (EMIT && (!sup_ok || R.tile_off[R.n_tiles] > R.capacity)) return;  // host grows and re-runs
   __shared__ int4 buf[kFilterThreads / 32][kFilterStages][kFilterUnit];
@@ -519,13 +538,7 @@ __global__ void __launch_bounds__(kFilterThreads) k_filter(const BuildReq* reqs)
   long long rb = 0, out = 0;
   unsigned long long d2 = 0;
   if (own) {
-    double qx, qy, qz, sx, sy, sz;
-    const double zx = R.zx[j], zy = R.zy[j], zz = R.zz[j];
-    apply_T(R.T, zx, zy, zz, qx, qy, qz);
-    apply_T(R.Ts, zx, zy, zz, sx, sy, sz);
-    const double dx = qx - sx, dy = qy - sy, dz = qz - sz;  // (T - Ts) z_j
-    d2 = (unsigned long long)__double_as_longlong(dx * dx + dy * dy + dz * dz);
-    ex = (float)dx; ey = (float)dy; ez = (float)dz;
+    filter_shift(R, j, ex, ey, ez, d2);
     if (sup_ok) {
       ds = R.sup_count[j];
       const long long t0 = R.sup_off[j >> 5], H = (R.sup_off[(j >> 5) + 1] - t0) >> 5;
@@ -604,8 +617,7 @@ __global__ void __launch_bounds__(kFilterThreads) k_filter(const BuildReq* reqs)
     for (int q = 0; q < kFilterUnit / 32; ++q) {
       const int k = psb + 32 * q + lane;
       const int4 e = buf[wid][stage][32 * q + lane];
-      const float dx = __int_as_float(e.x) - fx, dy = __int_as_float(e.y) - fy, dz = __int_as_float(e.z) - fz;
-      const bool keep = k < dss && fmaf(dx, dx, fmaf(dy, dy, dz * dz)) <= c2;
+      const bool keep = k < dss && filter_keep(e, fx, fy, fz, c2);
       const unsigned m = __ballot_sync(0xffffffffu, keep);
       if (EMIT && keep) {
         const long long at = slot_index(outs, cols, cnt + __popc(m & ((1u << lane) - 1u)));
@@ -636,6 +648,77 @@ __global__ void __launch_bounds__(kFilterThreads) k_filter(const BuildReq* reqs)
         if (R.write_index) R.slot_i[slot_index(outs, cols, k)] = -1;
       }
     }
+  }
+}
+
+// Filter stage over the resident sweep list (refilter = 1): warp per old
+// tile, lane per source (its old column, read in candidate order two slots
+// per 1-KB unit row, so the warp's loads are contiguous). Same predicate and
+// entries as k_filter, in the same order -> the same list. COUNT writes
+// count[j] and the tile's max |T z_j - old_T z_j|^2 (the subset condition
+// k_tile_offsets checks against filter_limit_sq); EMIT copies the kept
+// entries into j's new column and pads it.
+template <bool EMIT>
+__global__ void __launch_bounds__(kFilterThreads) k_refilter(const BuildReq* reqs) {
+  const BuildReq& R = reqs[blockIdx.y];
+  const int lane = threadIdx.x & 31;
+  const int t = blockIdx.x * (kFilterThreads / 32) + (threadIdx.x >> 5);
+  if (!R.refilter || t >= R.n_tiles) return;
+  if (EMIT && R.tile_off[R.n_tiles] > R.capacity) return;  // host re-runs from the candidate list
+  const int p = 32 * t + lane;
+  const bool own = p < R.n_z;
+  const int j = own ? R.old_perm[p] : 0;
+  const int deg = own ? R.old_deg_s[p] : 0;
+  float ex = 0.f, ey = 0.f, ez = 0.f;
+  unsigned long long d2 = 0;
+  if (own) {
+    filter_shift(R, j, ex, ey, ez, d2);
+    if (!EMIT) {
+      double qx, qy, qz, ox, oy, oz;
+      apply_T(R.T, R.zx[j], R.zy[j], R.zz[j], qx, qy, qz);
+      apply_T(R.old_T, R.zx[j], R.zy[j], R.zz[j], ox, oy, oz);
+      const double dx = qx - ox, dy = qy - oy, dz = qz - oz;
+      d2 = (unsigned long long)__double_as_longlong(dx * dx + dy * dy + dz * dz);
+    }
+  }
+  if (!EMIT) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long v = __shfl_xor_sync(0xffffffffu, d2, o);
+      d2 = v > d2 ? v : d2;
+    }
+    if (lane == 0) R.disp_blk[t] = d2;
+  }
+  long long out = 0;
+  int col = 0, height = 0;
+  if (EMIT && own) {
+    const int pn = R.pos[j], tn = pn >> 5;
+    out = R.tile_off[tn];
+    col = pn & 31;
+    height = (R.unit_off[tn + 1] - R.unit_off[tn]) * kUnitSteps;
+  }
+  const long long base = R.old_tile_off[t];
+  const int h_old = (R.old_unit_off[t + 1] - R.old_unit_off[t]) * kUnitSteps;
+  const float c2 = (float)R.cutoff_sq;
+  int cnt = 0;
+  constexpr int kB = 8;  // slots per lane in flight (4 unit rows, 4 KB per warp)
+  for (int k0 = 0; k0 < h_old; k0 += kB) {
+    int4 e[kB];
+#pragma unroll
+    for (int q = 0; q < kB; ++q)
+      e[q] = k0 + q < h_old ? __ldcs(R.old_slots + slot_index(base, lane, k0 + q)) : make_int4(0, 0, 0, 0);
+#pragma unroll
+    for (int q = 0; q < kB; ++q) {
+      if (k0 + q < deg && filter_keep(e[q], ex, ey, ez, c2)) {
+        if (EMIT) R.slots[slot_index(out, col, cnt)] = e[q];
+        ++cnt;
+      }
+    }
+  }
+  if (!EMIT) {
+    if (own) R.count[j] = cnt;
+  } else {
+    for (int k = cnt; k < height; ++k) R.slots[slot_index(out, col, k)] = make_int4(0, 0, 0, __float_as_int(-INFINITY));
   }
 }
 
@@ -1342,12 +1425,18 @@ void build_pairs_batched(const BuildReq* h, const BuildReq* d, int n, cudaStream
     launches += 9;
   }
   const dim3 gt(max(1, (max_nz + kFilterBlock - 1) / kFilterBlock), n);
-  k_filter<false><<<gt, kFilterThreads, 0, st>>>(d);
+  int n_refilter = 0;
+  for (int r = 0; r < n; ++r) n_refilter += h[r].refilter ? 1 : 0;
+  const bool cand = n_refilter < n;
+  const dim3 gr(max(1, ((max_nz + 31) / 32 + kFilterThreads / 32 - 1) / (kFilterThreads / 32)), n);
+  if (cand) k_filter<false><<<gt, kFilterThreads, 0, st>>>(d);
+  if (n_refilter) k_refilter<false><<<gr, kFilterThreads, 0, st>>>(d);
   k_order<<<dim3(max(1, (max_nz + kOrderWindow - 1) / kOrderWindow), n), kOrderWindow, 0, st>>>(d);
   k_tile_offsets<false><<<n, 1024, 0, st>>>(d);
-  k_filter<true><<<gt, kFilterThreads, 0, st>>>(d);
+  if (cand) k_filter<true><<<gt, kFilterThreads, 0, st>>>(d);
+  if (n_refilter) k_refilter<true><<<gr, kFilterThreads, 0, st>>>(d);
   k_chunk_records<<<dim3(kMaxChunks / 8, n), 256, 0, st>>>(d);
-  count_launch(launches + 5);
+  count_launch(launches + 3 + (cand ? 2 : 0) + (n_refilter ? 2 : 0));
 }
 
 size_t sweep_ctl_bytes(int n) { return sizeof(SweepCtl) * ((n + kMaxSweepReqs - 1) / kMaxSweepReqs + 1); }

@@ -333,6 +333,31 @@ def test_deterministic_and_batch_independent(ctx):
     assert np.array_equal(res[0].transform.as12(), a.transform.as12())
 
 
+def test_sweep_list_refilter_matches_candidate_filter(ctx):
+    """Opt-in refilter (KREG_REFILTER=1): at annealing steps whose move since
+    the last build is below the cutoff shrink, the new list is filtered from
+    the resident sweep list. Same predicate on the same entries in the same
+    order, so the registrations are bit-identical to the default path."""
+    X, Z, Ts = synth.kitti_pair(7, 10000)  # converges in ~400 iterations, ~26 refilters
+    p, cfg = synth.kitti_params(), synth.kitti_subsequent_config()
+    init = synth.perturbed(Ts, 5)
+    a = api.register_clouds(X, Z, init, p, cfg)
+    os.environ["KREG_REFILTER"] = "1"
+    try:
+        c2 = api.Context()
+    finally:
+        del os.environ["KREG_REFILTER"]
+    try:
+        c2.reset_stats()
+        b = api.register_clouds(X, Z, init, p, cfg, ctx=c2)
+        assert c2.build_stats()["refilter_builds"] > 0
+        assert np.array_equal(a.objective_trace, b.objective_trace)
+        assert np.array_equal(a.pair_count_trace, b.pair_count_trace)
+        assert np.array_equal(a.transform.as12(), b.transform.as12())
+    finally:
+        c2.close()
+
+
 def test_host_buffer_batch_matches_device_batch(ctx):
     """register_batch_host (clouds staged on host threads, uploaded into the
     context arena) gives bitwise the results of register_batch."""
