@@ -734,12 +734,14 @@ void begin_round(kreg_ctx* ctx, RoundSlot& S, std::vector<BuildJob>&& builds_in,
   S.d_sweep.ensure(ne + 1);
   const size_t n_res = static_cast<size_t>(ne) * kreg_dev::kMaxCandidates * kreg_dev::kOut + kreg_dev::kBuildStatus * (nb + 1);
   S.n_res = n_res;
-  S.d_results.ensure(n_res);
+  // results land in pinned host memory straight from the kernels (UVA maps
+  // cudaMallocHost memory into the device address space): no D2H copy, the
+  // round's completion event is all the host waits for
   S.h_results.ensure(n_res);
 
   for (int b = 0; b < nb; ++b) {
     prepare_build(ctx, builds[b], S.h_build.ptr[b]);
-    S.h_build.ptr[b].status = S.d_results.ptr + static_cast<size_t>(ne) * kreg_dev::kMaxCandidates * kreg_dev::kOut +
+    S.h_build.ptr[b].status = S.h_results.ptr + static_cast<size_t>(ne) * kreg_dev::kMaxCandidates * kreg_dev::kOut +
                               kreg_dev::kBuildStatus * b;
   }
   assign_grid_arena(S, S.h_build.ptr, nb);
@@ -749,6 +751,14 @@ void begin_round(kreg_ctx* ctx, RoundSlot& S, std::vector<BuildJob>&& builds_in,
     builds[b].pairs->last_req = S.h_build.ptr[b];
     builds[b].pairs->last_req.refilter = 0;
     builds[b].pairs->index_valid = false;
+  }
+  // builds go to the device before the sweep requests are prepared
+  if (nb) {
+    KREG_CUDA(cudaMemcpyAsync(S.d_build.ptr, S.h_build.ptr, sizeof(kreg_dev::BuildReq) * nb, cudaMemcpyHostToDevice,
+                              ctx->stream));
+    if (ctx->profiling) KREG_CUDA(cudaEventRecord(S.evb0, ctx->stream));
+    kreg_dev::build_pairs_batched(S.h_build.ptr, S.d_build.ptr, nb, ctx->stream);
+    if (ctx->profiling) KREG_CUDA(cudaEventRecord(S.evb1, ctx->stream));
   }
   const auto tb = clk::now();
   ctx->t_build_prep += std::chrono::duration<double>(tb - t0).count();
@@ -768,28 +778,18 @@ void begin_round(kreg_ctx* ctx, RoundSlot& S, std::vector<BuildJob>&& builds_in,
   for (int e = 0; e < ne; ++e) {
     prepare_sweep(evals[e], S.h_sweep.ptr[e], S.part_arena.ptr + scratch[e].part_off,
                   S.disp_arena.ptr + static_cast<size_t>(e) * kreg_dev::kMaxCandidates);
-    S.h_sweep.ptr[e].out = S.d_results.ptr + static_cast<size_t>(e) * kreg_dev::kMaxCandidates * kreg_dev::kOut;
+    S.h_sweep.ptr[e].out = S.h_results.ptr + static_cast<size_t>(e) * kreg_dev::kMaxCandidates * kreg_dev::kOut;
   }
   const auto ts = clk::now();
   ctx->t_sweep_prep += std::chrono::duration<double>(ts - tb).count();
-  if (nb)
-    KREG_CUDA(cudaMemcpyAsync(S.d_build.ptr, S.h_build.ptr, sizeof(kreg_dev::BuildReq) * nb, cudaMemcpyHostToDevice,
-                              ctx->stream));
   if (ne)
     KREG_CUDA(cudaMemcpyAsync(S.d_sweep.ptr, S.h_sweep.ptr, sizeof(kreg_dev::SweepReq) * ne, cudaMemcpyHostToDevice,
                               ctx->stream));
-  if (nb) {
-    if (ctx->profiling) KREG_CUDA(cudaEventRecord(S.evb0, ctx->stream));
-    kreg_dev::build_pairs_batched(S.h_build.ptr, S.d_build.ptr, nb, ctx->stream);
-    if (ctx->profiling) KREG_CUDA(cudaEventRecord(S.evb1, ctx->stream));
-  }
   if (ne) {
     kreg_dev::sweep_batched(S.h_sweep.ptr, S.d_sweep.ptr, ne, ctx->sm_count, S.counter_arena.ptr, ctx->stream,
                             ctx->profiling ? S.ev0 : nullptr, ctx->profiling ? S.ev1 : nullptr);
   }
   KREG_CUDA(cudaGetLastError());
-  KREG_CUDA(cudaMemcpyAsync(S.h_results.ptr, S.d_results.ptr, sizeof(double) * n_res, cudaMemcpyDeviceToHost,
-                            ctx->stream));
   KREG_CUDA(cudaEventRecord(S.done, ctx->stream));
   S.in_flight = true;
   ctx->t_prepare += std::chrono::duration<double>(clk::now() - t0).count();

@@ -327,8 +327,7 @@ struct RoundSlot {
   PinnedBuf<kreg_dev::BuildReq> h_build;
   DevBuf<kreg_dev::SweepReq> d_sweep;
   PinnedBuf<kreg_dev::SweepReq> h_sweep;
-  DevBuf<double> d_results;
-  PinnedBuf<double> h_results;
+  PinnedBuf<double> h_results;             // written by the kernels (mapped pinned memory)
   DevBuf<double> part_arena;                // sweep chunk partials (one slice per request)
   DevBuf<unsigned int> counter_arena;       // sweep chunk counters, self-resetting
   DevBuf<unsigned long long> disp_arena;    // displacement maxima, self-resetting
