@@ -786,6 +786,7 @@ void begin_round(kreg_ctx* ctx, RoundSlot& S, std::vector<BuildJob>&& builds_in,
     KREG_CUDA(cudaMemcpyAsync(S.d_sweep.ptr, S.h_sweep.ptr, sizeof(kreg_dev::SweepReq) * ne, cudaMemcpyHostToDevice,
                               ctx->stream));
   if (ne) {
+    S.sweep_issue = ctx->sweep_issued++;
     kreg_dev::sweep_batched(S.h_sweep.ptr, S.d_sweep.ptr, ne, ctx->sm_count, S.counter_arena.ptr, ctx->stream,
                             ctx->profiling ? S.ev0 : nullptr, ctx->profiling ? S.ev1 : nullptr);
   }
@@ -888,8 +889,8 @@ void end_round(kreg_ctx* ctx, RoundSlot& S) {
   ctx->slots_streamed += round_slots;
   static const bool trace = std::getenv("KREG_TRACE_ROUNDS") != nullptr;
   if (trace && ne)  // diagnostic: match profiled sweep launches to their pair / slot counts
-    std::fprintf(stderr, "kreg-round sweeps=%lld requests=%d launches=%d pairs=%lld slots=%lld\n",
-                 ctx->sweep_launches, ne, (ne + kreg_dev::kMaxSweepReqs - 1) / kreg_dev::kMaxSweepReqs, round_pairs,
+    std::fprintf(stderr, "kreg-round sweeps=%lld launch=%lld requests=%d launches=%d pairs=%lld slots=%lld\n",
+                 ctx->sweep_launches, S.sweep_issue, ne, (ne + kreg_dev::kMaxSweepReqs - 1) / kreg_dev::kMaxSweepReqs, round_pairs,
                  round_slots);
   if (ne) {
     ctx->sweep_launches += 1;

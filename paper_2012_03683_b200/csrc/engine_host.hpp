@@ -139,6 +139,7 @@ struct kreg_ctx {
   bool profiling = false;
   double sweep_ms = 0.0;
   long long sweep_launches = 0;
+  long long sweep_issued = 0;  // sweep launches issued, re-runs included
   long long pair_evals = 0;
   long long pairs_streamed = 0;
   long long slots_streamed = 0;
@@ -342,6 +343,7 @@ struct RoundSlot {
   std::vector<BuildJob> builds;
   std::vector<EvalJob> evals;
   size_t n_res = 0;
+  long long sweep_issue = -1;  // index of this round's sweep launch in the context (traces)
   bool in_flight = false;
   ~RoundSlot();
 };

@@ -15,7 +15,7 @@ def summarise(path, top=20):
             continue
         name = r[ki].split('(')[0].replace('kreg_dev::', '').replace('(anonymous namespace)::', '').replace('void ', '').replace('<unnamed>::', '')
         v = float(r[vi].replace(',', ''))
-        v *= {'nsecond': 1e-3, 'usecond': 1.0, 'msecond': 1e3}.get(r[ui], 1.0)
+        v *= {'nsecond': 1e-3, 'usecond': 1.0, 'msecond': 1e3, 'ns': 1e-3, 'us': 1.0, 'ms': 1e3}.get(r[ui], 1.0)
         agg[name][0] += 1
         agg[name][1] += v
     tot = sum(a[1] for a in agg.values())
