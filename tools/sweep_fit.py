@@ -37,6 +37,10 @@ A = np.stack([np.ones_like(ms), slots * msum / np.maximum(req, 1) / 1e9], 1)
 coef, *_ = np.linalg.lstsq(A, ms, rcond=None)
 print(f"launches {len(ms)}  total {ms.sum():.1f} ms  mean {ms.mean() * 1e3:.1f} us")
 print(f"fit ms = {coef[0] * 1e3:.1f} us + {coef[1]:.3f} ms per 1e9 slot-candidates")
+A2 = np.stack([np.ones_like(ms), slots / 1e9, req, grad, builds], 1)
+c2, *_ = np.linalg.lstsq(A2, ms, rcond=None)
+print(f"fit ms = {c2[0] * 1e3:.1f} us + {c2[1]:.3f} ms/Gslot + {c2[2] * 1e3:.2f} us/request"
+      f" + {c2[3] * 1e3:.2f} us/grad request + {c2[4] * 1e3:.2f} us/build")
 for lo, hi in ((0, 16), (16, 64), (64, 129), (129, 10000)):
     s = (req >= lo) & (req < hi)
     if s.any():

@@ -29,3 +29,8 @@ pr = api.build_pairs(X, Z, Ts, p, 3.0, 1e-4)
 for _ in range(3):
     api.eval_transforms(pr, X, Z, [Ts, Ts], p)
 print("pairs", pr.size())
+ctx = api.default_context()
+ctx.set_profiling(True)
+ctx.reset_stats()
+api.eval_transforms(pr, X, Z, [Ts, Ts], p)
+print("pairs", pr.size(), "sweep_us", round(ctx.sweep_stats()["sweep_ms"] * 1e3, 1))
