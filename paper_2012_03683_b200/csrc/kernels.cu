@@ -1259,6 +1259,9 @@ __device__ __forceinline__ unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+constexpr unsigned kTlCap = 1u << 16;
+__device__ unsigned long long g_tl[kTlCap][4];  // {start, end, cta << 16 | warp, item << 1 | chunk}
+__device__ unsigned g_tl_n;
 #endif
 
 template <int NPG>
@@ -1340,6 +1343,9 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(const SweepReq* reqs
     const int C = cbase[r + 1] - cbase[r] - D;
     const int n_items = (C + kChunkGroup - 1) / kChunkGroup + D;
     const int c = g - cbase[r] - D;
+#ifdef KREG_TIMELINE
+    const unsigned long long ti0 = gtimer();
+#endif
     if (c < 0) displacement_item(w, R, r, c + D, n_items);
     else if (R.grad) chunk_body<NPG, true>(w, R, r, c, C, n_items);
     else chunk_body<4, false>(w, R, r, c, C, n_items);
@@ -1347,18 +1353,32 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(const SweepReq* reqs
     if (lane == 0) ++g_wq[wid].head;
     __syncwarp();
 #ifdef KREG_TIMELINE
-    if (lane == 0) {
+    if (lane == 0) {  // item record
+      const unsigned long long ti1 = gtimer();
       atomicAdd(&tl_items, 1u);
-      atomicMax(&tl_last, gtimer());
+      atomicMax(&tl_last, ti1);
+      const unsigned k = atomicAdd(&g_tl_n, 1u);
+      if (k < kTlCap) {
+        g_tl[k][0] = ti0;
+        g_tl[k][1] = ti1;
+        g_tl[k][2] = ((unsigned long long)blockIdx.x << 16) | wid;
+        g_tl[k][3] = ((unsigned long long)g << 1) | (c < 0 ? 0 : 1);
+      }
     }
 #endif
   }
   // the last CTA to exit resets the launch's item counter
   __syncthreads();
 #ifdef KREG_TIMELINE
-  if (threadIdx.x == 0)
-    printf("TL cta %d sm %d start %llu last_item %llu end %llu items %u\n", blockIdx.x, 0, tl0, tl_last, gtimer(),
-           tl_items);
+  if (threadIdx.x == 0) {  // CTA record: {start, end, cta << 16 | 0xffff, items}
+    const unsigned k = atomicAdd(&g_tl_n, 1u);
+    if (k < kTlCap) {
+      g_tl[k][0] = tl0;
+      g_tl[k][1] = gtimer();
+      g_tl[k][2] = ((unsigned long long)blockIdx.x << 16) | 0xffffu;
+      g_tl[k][3] = tl_items;
+    }
+  }
 #endif
   if (threadIdx.x == 0) {
     __threadfence();
@@ -1501,3 +1521,19 @@ void interleave_positions(const double* x, const double* y, const double* z, int
 long long kernel_launch_count() { return g_launches.load(); }
 
 }  // namespace kreg_dev
+
+#ifdef KREG_TIMELINE
+// Diagnostic export of the timeline variant: copies the recorded item / CTA
+// records (4 x u64 each) and clears them; returns the count.
+extern "C" int kreg_debug_timeline(unsigned long long* out, int cap) {
+  unsigned n = 0;
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(&n, kreg_dev::g_tl_n, sizeof(n));
+  if (n > kreg_dev::kTlCap) n = kreg_dev::kTlCap;
+  if ((int)n > cap) n = (unsigned)cap;
+  if (n) cudaMemcpyFromSymbol(out, kreg_dev::g_tl, sizeof(unsigned long long) * 4 * n);
+  const unsigned z = 0;
+  cudaMemcpyToSymbol(kreg_dev::g_tl_n, &z, sizeof(z));
+  return (int)n;
+}
+#endif
