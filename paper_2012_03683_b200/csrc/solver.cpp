@@ -548,6 +548,13 @@ void register_many(kreg_ctx* ctx, std::vector<RegJob>& jobs, const Collective* c
   for (int g = 0; g < n_groups; ++g) groups[g].slot = round_slot(ctx, g);
   const size_t per_group = (window + n_groups - 1) / n_groups;
 
+  // host phase trace (KREG_TRACE_HOST=1): per-round microseconds of
+  // end_round after the wait, consume, refill + plan, begin_round
+  static const bool trace_host = std::getenv("KREG_TRACE_HOST") != nullptr;
+  double ph[4] = {0, 0, 0, 0};
+  long long ph_rounds = 0;
+  const double wait0 = ctx ? ctx->t_wait : 0.0;
+  auto us = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
   // consume the finished round of group g, refill, plan and launch its next
   auto step = [&](Group& G) -> bool {
     const auto t0 = clk::now();
@@ -556,6 +563,7 @@ void register_many(kreg_ctx* ctx, std::vector<RegJob>& jobs, const Collective* c
       if (coll && coll->fn) reduce_round(*G.slot, *coll);
       G.pending = false;
       const auto t1 = clk::now();
+      if (trace_host) ph[0] += us(t0, t1);
       Reg* last = nullptr;
       for (Reg* r : G.owners) {  // each registration consumes once per round
         if (r == last) continue;
@@ -563,6 +571,7 @@ void register_many(kreg_ctx* ctx, std::vector<RegJob>& jobs, const Collective* c
         consume(*r);
       }
       if (ctx) ctx->t_total += std::chrono::duration<double>(clk::now() - t1).count();
+      if (trace_host) ph[1] += us(t1, clk::now());
     }
     const auto t2 = clk::now();
     for (;;) {
@@ -592,7 +601,13 @@ void register_many(kreg_ctx* ctx, std::vector<RegJob>& jobs, const Collective* c
       for (Reg* r : G.active) plan(*r, builds, evals, G.owners, k_first, fail_grad);
       if (!builds.empty() || !evals.empty()) {
         if (ctx) ctx->t_total += std::chrono::duration<double>(clk::now() - t2).count();
+        const auto t3 = clk::now();
         begin_round(ctx, *G.slot, std::move(builds), std::move(evals));
+        if (trace_host) {
+          ph[2] += us(t2, t3);
+          ph[3] += us(t3, clk::now());
+          ++ph_rounds;
+        }
         G.pending = true;
         (void)t0;
         return true;
@@ -605,6 +620,12 @@ void register_many(kreg_ctx* ctx, std::vector<RegJob>& jobs, const Collective* c
   while (live[0] || live[1]) {
     for (int g = 0; g < n_groups; ++g)
       if (live[g]) live[g] = step(groups[g]);
+  }
+  if (trace_host && ph_rounds) {
+    const double n = static_cast<double>(ph_rounds), wait = ctx ? (ctx->t_wait - wait0) * 1e6 : 0.0;
+    std::fprintf(stderr,
+                 "kreg-host rounds %lld  us/round: end_round %.1f (wait %.1f), consume %.1f, plan %.1f, begin_round %.1f\n",
+                 ph_rounds, ph[0] / n, wait / n, ph[1] / n, ph[2] / n, ph[3] / n);
   }
 }
 
