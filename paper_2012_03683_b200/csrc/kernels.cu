@@ -26,6 +26,25 @@ namespace {
 std::atomic<long long> g_launches{0};
 inline void count_launch(int n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
+// Debug-variant bounds checks (KREG_DEBUG_BOUNDS): count violations in a
+// device counter read back by kreg_debug_violations (no trap: the tests run
+// real workloads through the variant and require zero).
+#ifdef KREG_DEBUG_BOUNDS
+__device__ unsigned long long g_viol;
+__device__ int g_viol_site;
+#define KREG_CHECK(cond, site)            \
+  do {                                     \
+    if (!(cond)) {                         \
+      atomicAdd(&g_viol, 1ull);            \
+      atomicExch(&g_viol_site, (site));    \
+    }                                      \
+  } while (0)
+#else
+#define KREG_CHECK(cond, site) \
+  do {                         \
+  } while (0)
+#endif
+
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -273,9 +292,15 @@ __global__ void __launch_bounds__(256) k_pair_pass(const BuildReq* reqs) {
   const long long czl = (long long)floor((qz - R.origin[2]) * R.inv_h);
 
   long long out = 0;
+#ifdef KREG_DEBUG_BOUNDS
+  long long Hdbg = 0;
+#endif
   if (EMIT) {
     const long long t0 = R.sup_off[j >> 5], H = (R.sup_off[(j >> 5) + 1] - t0) >> 5;
     out = t0 + (j & 31) * H;
+#ifdef KREG_DEBUG_BOUNDS
+    Hdbg = H;
+#endif
   }
   int cnt = 0;
   const bool geo = !EMIT || R.cp.n_channels == 0;
@@ -311,6 +336,9 @@ __global__ void __launch_bounds__(256) k_pair_pass(const BuildReq* reqs) {
             // {x_i - Ts z_j (FP32), log2 c}: the filter tests and emits
             // x_i - T z_j = this - (T - Ts) z_j without gathering x_i
             const int pos = __popc(m & ((1u << lane) - 1u));
+#ifdef KREG_DEBUG_BOUNDS
+            KREG_CHECK(cnt + pos < Hdbg && out + cnt + pos < R.sup_capacity, 1);
+#endif
             R.sup[out + cnt + pos] = make_int4(__float_as_int((float)dx), __float_as_int((float)dy2),
                                                __float_as_int((float)dz2), __float_as_int(lc));
             R.sup_i[out + cnt + pos] = i;
@@ -423,6 +451,10 @@ __global__ void k_chunk_records(const BuildReq* reqs) {
     if (R.unit_off[mid] <= u0) lo = mid;
     else hi = mid - 1;
   }
+  KREG_CHECK(c < kMaxChunks, 8);
+#ifdef KREG_BOUNDS_SELFTEST
+  KREG_CHECK(c != 0 || lane != 0, 99);  // positive control: fires once per list
+#endif
   ChunkRec& rec = R.chunks[c];
   if (lane == 0) {
     rec.t0 = lo;
@@ -621,6 +653,7 @@ __global__ void __launch_bounds__(kFilterThreads) k_filter(const BuildReq* reqs)
       const unsigned m = __ballot_sync(0xffffffffu, keep);
       if (EMIT && keep) {
         const long long at = slot_index(outs, cols, cnt + __popc(m & ((1u << lane) - 1u)));
+        KREG_CHECK(at < R.capacity && rbs + k < R.sup_capacity, 2);
         // the candidate entry itself, x_i - Ts z_j: the sweep forms
         // d = x_i - T z_j as this minus (T - Ts) z_j, and a later filter of
         // this list reproduces a filter of the candidate list bit for bit
@@ -643,7 +676,9 @@ __global__ void __launch_bounds__(kFilterThreads) k_filter(const BuildReq* reqs)
       const int hs = __shfl_sync(0xffffffffu, height, s), cs = __shfl_sync(0xffffffffu, my_cnt, s);
       const long long outs = __shfl_sync(0xffffffffu, out, s);
       const int cols = __shfl_sync(0xffffffffu, col, s);
+      KREG_CHECK(cs <= hs || hs == 0, 3);  // kept <= column height
       for (int k = cs + lane; k < hs; k += 32) {
+        KREG_CHECK(slot_index(outs, cols, k) < R.capacity, 4);
         R.slots[slot_index(outs, cols, k)] = make_int4(0, 0, 0, __float_as_int(-INFINITY));
         if (R.write_index) R.slot_i[slot_index(outs, cols, k)] = -1;
       }
@@ -710,7 +745,10 @@ __global__ void __launch_bounds__(kFilterThreads) k_refilter(const BuildReq* req
 #pragma unroll
     for (int q = 0; q < kB; ++q) {
       if (k0 + q < deg && filter_keep(e[q], ex, ey, ez, c2)) {
-        if (EMIT) R.slots[slot_index(out, col, cnt)] = e[q];
+        if (EMIT) {
+          KREG_CHECK(cnt < height && slot_index(out, col, cnt) < R.capacity, 5);
+          R.slots[slot_index(out, col, cnt)] = e[q];
+        }
         ++cnt;
       }
     }
@@ -1024,6 +1062,7 @@ __device__ __forceinline__ bool produce(SweepWarp& w) {
   const int s = Q.issued % kSweepStages;
   const SweepReq& P = w.reqs[Q.pr];
   fence_proxy_async();
+  KREG_CHECK(((long long)Q.pu + nu) * kUnitSlots <= P.capacity && Q.pc < kMaxChunks && nu > 0, 6);
   mbar_expect_tx(&w.bars[s], nu * kUnitBytes + (Q.first ? (unsigned)sizeof(ChunkRec) : 0u));
   tma_load_1d(w.ring + s * kStageSlots, P.slots + (long long)Q.pu * kUnitSlots, nu * kUnitBytes, &w.bars[s]);
   if (Q.first) {
@@ -1217,6 +1256,7 @@ __device__ __forceinline__ void chunk_body(SweepWarp& w, const SweepReq& R, int 
 
   // chunk partial: FP32 warp sums (fixed butterfly order) widened to FP64;
   // lane v stores value v
+  KREG_CHECK(c < kMaxChunks && c / kChunkGroup < kMaxChunkGroups, 7);
   double* part = R.partials + (size_t)c * MV;
 #pragma unroll
   for (int p = 0; p < NP; ++p) {
@@ -1535,5 +1575,21 @@ extern "C" int kreg_debug_timeline(unsigned long long* out, int cap) {
   const unsigned z = 0;
   cudaMemcpyToSymbol(kreg_dev::g_tl_n, &z, sizeof(z));
   return (int)n;
+}
+#endif
+
+#ifdef KREG_DEBUG_BOUNDS
+// Diagnostic export of the bounds-check variant: violations since the last
+// call (and the site of the latest one), then clears them.
+extern "C" long long kreg_debug_violations(int* site) {
+  unsigned long long n = 0;
+  int st = 0;
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(&n, kreg_dev::g_viol, sizeof(n));
+  cudaMemcpyFromSymbol(&st, kreg_dev::g_viol_site, sizeof(st));
+  const unsigned long long z = 0;
+  cudaMemcpyToSymbol(kreg_dev::g_viol, &z, sizeof(z));
+  if (site) *site = st;
+  return (long long)n;
 }
 #endif
