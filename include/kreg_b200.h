@@ -271,6 +271,42 @@ enum { KREG_SWEEP_ROTATION = 0, KREG_SWEEP_TRANSLATION = 1 };
 kreg_status kreg_indicator_sweep(kreg_ctx* ctx, const kreg_cloud_view* cloud, const kreg_kernel_params* params,
                                  int32_t axis, double range, int32_t steps, double cutoff_multiplier,
                                  double c_min, double* magnitudes, double* indicators);
+/* ---- frame ingest (projection.hpp:12-39, selector.hpp:12-42) */
+typedef struct {             /* kreg::CameraIntrinsics (projection.hpp:12-19) */
+  double fx, fy, cx, cy;     /* pixels */
+  double depth_scale;        /* meters per stored depth unit */
+  double max_depth;          /* meters; points beyond are dropped */
+  int32_t skip_top_rows;     /* rows excluded from the top of the image */
+} kreg_camera_intrinsics;
+typedef struct {             /* kreg::SelectorConfig (selector.hpp:12-18) */
+  int32_t target_min, target_max;
+  double initial_threshold, adjust_factor;
+  int32_t max_adjust_rounds;
+} kreg_selector_config;
+typedef struct {             /* kreg::Selection minus the pixel list (selector.hpp:22-27) */
+  int64_t count;             /* selected pixels (rows of the outputs) */
+  double threshold;          /* accepted corner threshold */
+  int32_t in_band;           /* count landed in [target_min, target_max] */
+  int32_t fallback;          /* corner test could not supply target_min: every valid pixel */
+  int64_t valid_pixels;      /* pixels with valid depth (the fallback note) */
+} kreg_selection_info;
+/* select_points (selector.cpp:63-125): rgb w x h x channels (1 or 3),
+ * valid_depth w x h mask; writes info->count (u, v) pairs in raster order to
+ * pixels_uv when capacity >= info->count (else only info). */
+kreg_status kreg_select_points(kreg_ctx* ctx, const uint8_t* rgb, int32_t channels, int32_t width, int32_t height,
+                               const uint8_t* valid_depth, const kreg_selector_config* sel, int32_t* pixels_uv,
+                               int64_t capacity, kreg_selection_info* info);
+/* depth_rgb_to_cloud (projection.cpp:30-75): depth w x h (uint16), rgb w x h x
+ * channels, semantics w x h x semantic_channels (float, nullable); writes
+ * info->count rows of xyz (3 doubles) and features (3 + semantic_channels
+ * doubles: rgb / 255 then the class probabilities) when capacity >=
+ * info->count. The pixel test, threshold rounds and back-projection are the
+ * reference's, bit for bit. */
+kreg_status kreg_depth_rgb_to_cloud(kreg_ctx* ctx, const uint16_t* depth, const uint8_t* rgb, int32_t channels,
+                                    const float* semantics, int32_t semantic_channels, int32_t width, int32_t height,
+                                    const kreg_camera_intrinsics* intr, const kreg_selector_config* sel, double* xyz,
+                                    double* features, int64_t capacity, kreg_selection_info* info);
+
 kreg_status kreg_exact_cosine(kreg_ctx* ctx, const kreg_cloud_view* X, const kreg_cloud_view* Z,
                               const double T[12], const kreg_kernel_params* params, double* cosine,
                               double parts[3]);

@@ -712,3 +712,134 @@ int ko_register_clouds(const kreg_cloud_view* X, const kreg_cloud_view* Z, const
   res->rebuilds = 0;
   return 0;
 }
+
+
+/* ------------------------------------------------------------ frame ingest
+ * Plain restatement of image.cpp:144-155, selector.cpp:21-125 and
+ * projection.cpp:30-75 (the detector is re-run every threshold round, as the
+ * reference does). */
+void ko_to_gray(const uint8_t* rgb, int channels, int w, int h, uint8_t* gray) {
+  for (long i = 0; i < (long)w * h; ++i) {
+    if (channels == 1) {
+      gray[i] = rgb[i];
+    } else {
+      const uint8_t* p = rgb + i * channels;
+      gray[i] = (uint8_t)((299 * p[0] + 587 * p[1] + 114 * p[2]) / 1000);
+    }
+  }
+}
+
+static const int ko_circle[16][2] = {
+    {0, -3}, {1, -3}, {2, -2}, {3, -1}, {3, 0},  {3, 1},  {2, 2},  {1, 3},
+    {0, 3},  {-1, 3}, {-2, 2}, {-3, 1}, {-3, 0}, {-3, -1}, {-2, -2}, {-1, -3},
+};
+
+int ko_is_corner(const uint8_t* gray, int w, int u, int v, double t) {
+  const double center = gray[(long)v * w + u];
+  int state[16];
+  for (int s = 0; s < 16; ++s) {
+    const double p = gray[(long)(v + ko_circle[s][1]) * w + u + ko_circle[s][0]];
+    state[s] = p > center + t ? 1 : (p < center - t ? -1 : 0);
+  }
+  for (int want = 1; want >= -1; want -= 2) {
+    int run = 0;
+    for (int s = 0; s < 32; ++s) {
+      if (state[s & 15] == want) {
+        if (++run >= 9) return 1;
+      } else {
+        run = 0;
+      }
+    }
+  }
+  return 0;
+}
+
+long ko_select_points(const uint8_t* rgb, int channels, int w, int h, const uint8_t* valid,
+                      const kreg_selector_config* sel, int32_t* pixels, double* threshold, int* in_band,
+                      int* fallback) {
+  uint8_t* gray = (uint8_t*)malloc((size_t)w * h + 1);
+  int32_t* cur = (int32_t*)malloc(sizeof(int32_t) * 2 * ((size_t)w * h + 1));
+  ko_to_gray(rgb, channels, w, h, gray);
+  double t = sel->initial_threshold;
+  long best_gap = -1, best_n = 0;
+  *threshold = 0.0;
+  *in_band = 0;
+  *fallback = 0;
+  int done = 0;
+  for (int round = 0; round < sel->max_adjust_rounds && !done; ++round) {
+    long n = 0;
+    for (int v = 3; v < h - 3; ++v)
+      for (int u = 3; u < w - 3; ++u)
+        if (ko_is_corner(gray, w, u, v, t) && valid[(long)v * w + u]) {
+          cur[2 * n] = u;
+          cur[2 * n + 1] = v;
+          ++n;
+        }
+    const long gap = n < sel->target_min ? sel->target_min - n : n > sel->target_max ? n - sel->target_max : 0;
+    if (best_gap < 0 || gap < best_gap) {
+      best_gap = gap;
+      best_n = n;
+      *threshold = t;
+      memcpy(pixels, cur, sizeof(int32_t) * 2 * (size_t)n);
+    }
+    if (gap == 0) {
+      *in_band = 1;
+      done = 1;
+      break;
+    }
+    if (n > sel->target_max) {
+      t *= sel->adjust_factor;
+    } else {
+      if (t <= 0.5) break;
+      t = t / sel->adjust_factor > 0.5 ? t / sel->adjust_factor : 0.5;
+    }
+  }
+  if (!*in_band && best_n < sel->target_min) {
+    best_n = 0;
+    for (int v = 0; v < h; ++v)
+      for (int u = 0; u < w; ++u)
+        if (valid[(long)v * w + u]) {
+          pixels[2 * best_n] = u;
+          pixels[2 * best_n + 1] = v;
+          ++best_n;
+        }
+    *fallback = 1;
+  }
+  free(gray);
+  free(cur);
+  return best_n;
+}
+
+long ko_depth_rgb_to_cloud(const uint16_t* depth, const uint8_t* rgb, int channels, const float* sem, int sem_ch,
+                           int w, int h, const kreg_camera_intrinsics* in, const kreg_selector_config* sel,
+                           double* xyz, double* feat, int* fallback, int* in_band) {
+  uint8_t* valid = (uint8_t*)calloc((size_t)w * h + 1, 1);
+  int32_t* px = (int32_t*)malloc(sizeof(int32_t) * 2 * ((size_t)w * h + 1));
+  for (int v = in->skip_top_rows; v < h; ++v)
+    for (int u = 0; u < w; ++u) {
+      const uint16_t d = depth[(long)v * w + u];
+      if (d == 0) continue;
+      if (d * in->depth_scale > in->max_depth) continue;
+      valid[(long)v * w + u] = 1;
+    }
+  double thr;
+  const long n = ko_select_points(rgb, channels, w, h, valid, sel, px, &thr, in_band, fallback);
+  const int D = 3 + (sem ? sem_ch : 0);
+  for (long k = 0; k < n; ++k) {
+    const int u = px[2 * k], v = px[2 * k + 1];
+    const long i = (long)v * w + u;
+    const double dm = depth[i] * in->depth_scale;
+    xyz[3 * k] = dm * ((u - in->cx) / in->fx);
+    xyz[3 * k + 1] = dm * ((v - in->cy) / in->fy);
+    xyz[3 * k + 2] = dm * 1.0;
+    const long end = (long)w * h * channels;
+    for (int c = 0; c < 3; ++c) {
+      const long at = i * channels + c;
+      feat[D * k + c] = (at < end ? rgb[at] : 0) / 255.0;
+    }
+    for (int c = 0; sem && c < sem_ch; ++c) feat[D * k + 3 + c] = sem[i * sem_ch + c];
+  }
+  free(valid);
+  free(px);
+  return n;
+}

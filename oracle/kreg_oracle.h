@@ -62,6 +62,19 @@ int ko_check_config(const kreg_registration_config* config);
 int ko_register_clouds(const kreg_cloud_view* X, const kreg_cloud_view* Z,
                        const double initial[12], const kreg_kernel_params* params,
                        const kreg_registration_config* config, kreg_registration_result* result);
+/* image.cpp:144-155 integer rec601 luma (channels 1 or >= 3) */
+void ko_to_gray(const uint8_t* rgb, int channels, int w, int h, uint8_t* gray);
+/* selector.cpp:29-51 segment test (16-pixel circle, 9 contiguous, strict) */
+int ko_is_corner(const uint8_t* gray, int w, int u, int v, double t);
+/* selector.cpp:63-125: the budgeted selection; pixels (u, v) raster order,
+ * capacity w*h pairs; returns the count, fills threshold / in_band / fallback */
+long ko_select_points(const uint8_t* rgb, int channels, int w, int h, const uint8_t* valid,
+                      const kreg_selector_config* sel, int32_t* pixels, double* threshold, int* in_band,
+                      int* fallback);
+/* projection.cpp:30-75: rows xyz (3) and features (3 + sem_ch), capacity w*h */
+long ko_depth_rgb_to_cloud(const uint16_t* depth, const uint8_t* rgb, int channels, const float* sem, int sem_ch,
+                           int w, int h, const kreg_camera_intrinsics* intr, const kreg_selector_config* sel,
+                           double* xyz, double* feat, int* fallback, int* in_band);
 /* rng.hpp:11-46 SplitMix64 helpers for fixtures */
 uint64_t ko_splitmix_next(uint64_t* state);
 uint64_t ko_splitmix_derive(uint64_t seed, uint64_t index);

@@ -10,6 +10,7 @@
 
 #include <omp.h>
 
+#include <cstdio>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -17,6 +18,9 @@
 
 #include "kreg/errors.hpp"
 #include "kreg/eval.hpp"
+#include "kreg/image.hpp"
+#include "kreg/projection.hpp"
+#include "kreg/selector.hpp"
 #include "kreg/inner_product.hpp"
 #include "kreg/reference.hpp"
 #include "kreg/registration.hpp"
@@ -339,6 +343,72 @@ int kref_make_ring_cloud(uint64_t seed, int sectors, int per_sector, int with_co
     for (int i = 0; i < c.size(); ++i)
       for (int k = 0; k < 3; ++k) xyz[3 * i + k] = c.position(i)[k];
     if (with_color) std::memcpy(features, c.features().data(), c.features().size() * sizeof(double));
+  });
+}
+
+// Frame ingest (selector.cpp / projection.cpp): plain arrays in, the
+// reference's Selection / PointCloud out (rows copied when capacity suffices).
+namespace {
+SelectorConfig to_sel(const kreg_selector_config* s) {
+  SelectorConfig o;
+  o.target_min = s->target_min;
+  o.target_max = s->target_max;
+  o.initial_threshold = s->initial_threshold;
+  o.adjust_factor = s->adjust_factor;
+  o.max_adjust_rounds = s->max_adjust_rounds;
+  return o;
+}
+ImageU8 to_img(const uint8_t* p, int w, int h, int c) {
+  ImageU8 im(w, h, c);
+  std::memcpy(im.data.data(), p, static_cast<size_t>(w) * h * c);
+  return im;
+}
+}  // namespace
+
+int kref_select_points(const uint8_t* rgb, int channels, int w, int h, const uint8_t* valid,
+                       const kreg_selector_config* sel, int32_t* pixels, int64_t cap, kreg_selection_info* info,
+                       char* note, int note_cap) {
+  return guarded([&] {
+    const Selection s = select_points(to_img(rgb, w, h, channels),
+                                      std::vector<uint8_t>(valid, valid + static_cast<size_t>(w) * h), to_sel(sel));
+    info->count = static_cast<int64_t>(s.pixels.size());
+    info->threshold = s.threshold;
+    info->in_band = s.in_band ? 1 : 0;
+    info->fallback = s.note.find("fallback") != std::string::npos ? 1 : 0;
+    info->valid_pixels = 0;
+    if (cap >= info->count)
+      for (size_t k = 0; k < s.pixels.size(); ++k) {
+        pixels[2 * k] = s.pixels[k].first;
+        pixels[2 * k + 1] = s.pixels[k].second;
+      }
+    if (note && note_cap > 0) std::snprintf(note, note_cap, "%s", s.note.c_str());
+  });
+}
+
+int kref_depth_rgb_to_cloud(const uint16_t* depth, const uint8_t* rgb, int channels, const float* sem, int sem_ch,
+                            int w, int h, const kreg_camera_intrinsics* in, const kreg_selector_config* sel,
+                            double* xyz, double* feat, int64_t cap, int64_t* n, char* note, int note_cap) {
+  return guarded([&] {
+    ImageU16 d(w, h, 1);
+    std::memcpy(d.data.data(), depth, static_cast<size_t>(w) * h * sizeof(uint16_t));
+    ImageF s;
+    if (sem) {
+      s = ImageF(w, h, sem_ch);
+      std::memcpy(s.data.data(), sem, static_cast<size_t>(w) * h * sem_ch * sizeof(float));
+    }
+    CameraIntrinsics ci;
+    ci.fx = in->fx; ci.fy = in->fy; ci.cx = in->cx; ci.cy = in->cy;
+    ci.depth_scale = in->depth_scale; ci.max_depth = in->max_depth; ci.skip_top_rows = in->skip_top_rows;
+    std::vector<std::string> warnings;
+    const PointCloud c = depth_rgb_to_cloud(d, to_img(rgb, w, h, channels), sem ? &s : nullptr, ci, to_sel(sel),
+                                            &warnings);
+    *n = c.size();
+    if (cap >= *n) {
+      for (int i = 0; i < c.size(); ++i)
+        for (int k = 0; k < 3; ++k) xyz[3 * i + k] = c.position(i)[k];
+      std::memcpy(feat, c.features().data(), c.features().size() * sizeof(double));
+    }
+    if (note && note_cap > 0) std::snprintf(note, note_cap, "%s", warnings.empty() ? "" : warnings[0].c_str());
   });
 }
 

@@ -103,6 +103,21 @@ class kreg_sequence_result(C.Structure):
     ]
 
 
+class kreg_camera_intrinsics(C.Structure):
+    _fields_ = [("fx", C.c_double), ("fy", C.c_double), ("cx", C.c_double), ("cy", C.c_double),
+                ("depth_scale", C.c_double), ("max_depth", C.c_double), ("skip_top_rows", C.c_int32)]
+
+
+class kreg_selector_config(C.Structure):
+    _fields_ = [("target_min", C.c_int32), ("target_max", C.c_int32), ("initial_threshold", C.c_double),
+                ("adjust_factor", C.c_double), ("max_adjust_rounds", C.c_int32)]
+
+
+class kreg_selection_info(C.Structure):
+    _fields_ = [("count", C.c_int64), ("threshold", C.c_double), ("in_band", C.c_int32), ("fallback", C.c_int32),
+                ("valid_pixels", C.c_int64)]
+
+
 def as_ptr(a: np.ndarray, ctype=C.c_double):
     return a.ctypes.data_as(C.POINTER(ctype))
 

@@ -17,8 +17,9 @@ import threading
 import numpy as np
 
 from . import _abi
-from .types import (Isometry, KernelParams, PointCloud, RegistrationConfig, RegistrationResult,
-                    SequenceBuffers, SequenceResult, raise_for)
+from .types import (CameraIntrinsics, Channel, ChannelKind, FeatureSchema, Isometry, KernelParams, PointCloud,
+                    RegistrationConfig, RegistrationResult, Selection, SelectorConfig, SequenceBuffers, SequenceResult,
+                    raise_for)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("KREG_LIB") or os.path.join(_HERE, "libkreg_b200.so")
@@ -97,6 +98,13 @@ def lib():
         L.kreg_register_clouds_rows.argtypes = [P, P, P, C.c_int64, _abi.dptr, KP, CP, RP]
         L.kreg_ctx_set_collective.argtypes = [P, COLLECTIVE_FN, VP_]
         L.kreg_exact_cosine.argtypes = [P, VP, VP, _abi.dptr, KP, _abi.dptr, _abi.dptr]
+        L.kreg_select_points.argtypes = [P, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
+                                         C.POINTER(_abi.kreg_selector_config), C.c_void_p, C.c_int64,
+                                         C.POINTER(_abi.kreg_selection_info)]
+        L.kreg_depth_rgb_to_cloud.argtypes = [P, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_int32,
+                                              C.c_int32, C.POINTER(_abi.kreg_camera_intrinsics),
+                                              C.POINTER(_abi.kreg_selector_config), _abi.dptr, _abi.dptr, C.c_int64,
+                                              C.POINTER(_abi.kreg_selection_info)]
         L.kreg_indicator_sweep.argtypes = [P, VP, KP, C.c_int32, D, C.c_int32, D, D, _abi.dptr, _abi.dptr]
         L.kreg_se3_exp.argtypes = [_abi.dptr, _abi.dptr]
         L.kreg_se3_compose.argtypes = [_abi.dptr, _abi.dptr, _abi.dptr]
@@ -527,6 +535,91 @@ def exact_cosine(X: PointCloud, Z: PointCloud, T, params: KernelParams, ctx=None
     pr = np.zeros(3)
     _check(lib().kreg_exact_cosine(ctx.h, X.view(), Z.view(), tp, params.cstruct(), _abi.as_ptr(out), _abi.as_ptr(pr)))
     return (float(out[0]), tuple(pr)) if parts else float(out[0])
+
+
+def _selection_note(info, sel) -> str:
+    # selector.cpp:112-123 (the reference's warning strings)
+    if info.fallback:
+        return (f"selector fallback: {info.valid_pixels} valid-depth pixels returned without corner filtering")
+    if not info.in_band:
+        return f"selector accepted out-of-band count {info.count} after {sel.max_adjust_rounds} rounds"
+    return ""
+
+
+def _image_u8(rgb):
+    a = np.ascontiguousarray(rgb, dtype=np.uint8)
+    if a.ndim == 2:
+        a = a[:, :, None]
+    if a.ndim != 3 or a.shape[2] not in (1, 3):
+        raise ValueError("image: expected h x w (x 1 or 3) uint8")
+    return a
+
+
+def select_points(rgb, valid_depth, sel: SelectorConfig | None = None, ctx=None) -> Selection:
+    """reference selector.cpp:63-125 (budgeted FAST corners over valid-depth
+    pixels): FAST scores and their histogram on the device, the reference's
+    threshold rounds replayed from the histogram, ordered compaction."""
+    ctx = ctx or default_context()
+    sel = sel or SelectorConfig()
+    img = _image_u8(rgb)
+    h, w, ch = img.shape
+    mask = np.ascontiguousarray(valid_depth, dtype=np.uint8)
+    if mask.size != w * h:
+        raise ValueError("select_points: mask size does not match image")
+    info = _abi.kreg_selection_info()
+    cs = sel.cstruct()
+    _check(lib().kreg_select_points(ctx.h, img.ctypes.data_as(C.c_void_p), ch, w, h, mask.ctypes.data_as(C.c_void_p),
+                                    C.byref(cs), None, 0, C.byref(info)))
+    px = np.zeros((max(info.count, 1), 2), dtype=np.int32)
+    if info.count:
+        _check(lib().kreg_select_points(ctx.h, img.ctypes.data_as(C.c_void_p), ch, w, h,
+                                        mask.ctypes.data_as(C.c_void_p), C.byref(cs), px.ctypes.data_as(C.c_void_p),
+                                        info.count, C.byref(info)))
+    return Selection(pixels=[(int(u), int(v)) for u, v in px[:info.count]], threshold=float(info.threshold),
+                     in_band=bool(info.in_band), note=_selection_note(info, sel))
+
+
+def depth_rgb_to_cloud(depth, rgb, semantics, intr: CameraIntrinsics, sel: SelectorConfig | None = None, ctx=None,
+                       warnings: list | None = None) -> PointCloud:
+    """reference projection.cpp:30-75: valid-depth pixels (row >= skip_top_rows,
+    d != 0, d * scale <= max_depth) -> budgeted FAST selection -> back-projected
+    cloud with colour (rgb / 255) and optional class-probability channels,
+    bit-identical to the reference, on the device."""
+    ctx = ctx or default_context()
+    sel = sel or SelectorConfig()
+    d = np.ascontiguousarray(depth, dtype=np.uint16)
+    img = _image_u8(rgb)
+    if d.shape != img.shape[:2]:
+        raise ValueError("depth_rgb_to_cloud: depth and rgb resolutions differ")
+    h, w, ch = img.shape
+    sem = None
+    n_sem = 0
+    if semantics is not None:
+        sem = np.ascontiguousarray(semantics, dtype=np.float32)
+        if sem.ndim == 2:
+            sem = sem[:, :, None]
+        if sem.shape[:2] != d.shape:
+            raise ValueError("depth_rgb_to_cloud: semantics resolution differs")
+        n_sem = sem.shape[2]
+    info = _abi.kreg_selection_info()
+    ci, cs = intr.cstruct(), sel.cstruct()
+    sem_p = sem.ctypes.data_as(C.c_void_p) if sem is not None else None
+    _check(lib().kreg_depth_rgb_to_cloud(ctx.h, d.ctypes.data_as(C.c_void_p), img.ctypes.data_as(C.c_void_p), ch,
+                                         sem_p, n_sem, w, h, C.byref(ci), C.byref(cs), None, None, 0, C.byref(info)))
+    n = int(info.count)
+    xyz = np.zeros((max(n, 1), 3))
+    feat = np.zeros((max(n, 1), 3 + n_sem))
+    if n:
+        _check(lib().kreg_depth_rgb_to_cloud(ctx.h, d.ctypes.data_as(C.c_void_p), img.ctypes.data_as(C.c_void_p), ch,
+                                             sem_p, n_sem, w, h, C.byref(ci), C.byref(cs), _abi.as_ptr(xyz),
+                                             _abi.as_ptr(feat), n, C.byref(info)))
+    note = _selection_note(info, sel)
+    if warnings is not None and note:
+        warnings.append(note)
+    chans = [Channel("color", 3, ChannelKind.color)]
+    if n_sem:
+        chans.append(Channel("semantic", n_sem, ChannelKind.semantic))
+    return PointCloud(xyz[:n], FeatureSchema(chans), feat[:n])
 
 
 def se3_exp(xi) -> Isometry:

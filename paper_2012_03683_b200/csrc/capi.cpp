@@ -770,6 +770,171 @@ kreg_status kreg_indicator_sweep(kreg_ctx* ctx, const kreg_cloud_view* cloud, co
   });
 }
 
+// ---------------------------------------------------------------- ingest
+}  // extern "C"
+namespace {
+
+void check_selector(const kreg_selector_config* sel) {  // selector.cpp:8-19
+  require(sel != nullptr, "NULL argument");
+  if (!(sel->target_min > 0 && sel->target_min < sel->target_max))
+    throw Error(KREG_INVALID_ARGUMENT, "selector: need 0 < target_min < target_max");
+  if (!(sel->initial_threshold > 0.0)) throw Error(KREG_INVALID_ARGUMENT, "selector: initial_threshold must be > 0");
+  if (!(sel->adjust_factor > 1.0)) throw Error(KREG_INVALID_ARGUMENT, "selector: adjust_factor must be > 1");
+}
+
+void check_intr(const kreg_camera_intrinsics* in) {  // projection.cpp:7-20
+  require(in != nullptr, "NULL argument");
+  if (!(in->fx > 0.0 && in->fy > 0.0)) throw Error(KREG_INVALID_ARGUMENT, "intrinsics: fx and fy must be > 0");
+  if (!(in->max_depth > 0.0)) throw Error(KREG_INVALID_ARGUMENT, "intrinsics: max_depth must be > 0");
+  if (!(in->depth_scale > 0.0)) throw Error(KREG_INVALID_ARGUMENT, "intrinsics: depth_scale must be > 0");
+  if (in->skip_top_rows < 0) throw Error(KREG_INVALID_ARGUMENT, "intrinsics: skip_top_rows must be >= 0");
+}
+
+// One frame: score + histogram on the device, the reference's threshold
+// rounds on the host (selector.cpp:81-124) from the histogram, then the
+// ordered compaction / back-projection when the caller's capacity suffices.
+void run_ingest(kreg_ctx* ctx, const uint16_t* depth, const uint8_t* rgb, int channels, const float* sem, int sem_ch,
+                const uint8_t* valid_mask, int w, int h, const kreg_camera_intrinsics* intr,
+                const kreg_selector_config* sel, int32_t* pixels, double* xyz, double* feat, int64_t cap,
+                kreg_selection_info* info) {
+  require(rgb && info && w >= 0 && h >= 0 && (channels == 1 || channels >= 3) && sem_ch >= 0,
+          "invalid ingest arguments");
+  KREG_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->stream;
+  const size_t npx = static_cast<size_t>(w) * h;
+  kreg_dev::IngestReq R{};
+  R.w = w; R.h = h; R.channels = channels; R.sem_channels = sem ? sem_ch : 0;
+  ctx->ing_rgb.ensure(npx * channels + 1);
+  ctx->ing_score.ensure(npx + 1);
+  ctx->ing_valid.ensure(npx + 1);
+  ctx->ing_hist.ensure(256);
+  if (npx) KREG_CUDA(cudaMemcpyAsync(ctx->ing_rgb.ptr, rgb, npx * channels, cudaMemcpyHostToDevice, st));
+  R.rgb = ctx->ing_rgb.ptr;
+  if (valid_mask) {
+    ctx->ing_valid_in.ensure(npx + 1);
+    if (npx) KREG_CUDA(cudaMemcpyAsync(ctx->ing_valid_in.ptr, valid_mask, npx, cudaMemcpyHostToDevice, st));
+    R.valid_in = ctx->ing_valid_in.ptr;
+  } else {
+    ctx->ing_depth.ensure(npx + 1);
+    if (npx) KREG_CUDA(cudaMemcpyAsync(ctx->ing_depth.ptr, depth, npx * sizeof(uint16_t), cudaMemcpyHostToDevice, st));
+    R.depth = ctx->ing_depth.ptr;
+    R.skip_top_rows = intr->skip_top_rows;
+    R.depth_scale = intr->depth_scale; R.max_depth = intr->max_depth;
+    R.fx = intr->fx; R.fy = intr->fy; R.cx = intr->cx; R.cy = intr->cy;
+    if (sem && sem_ch > 0) {
+      ctx->ing_sem.ensure(npx * sem_ch + 1);
+      if (npx) KREG_CUDA(cudaMemcpyAsync(ctx->ing_sem.ptr, sem, npx * sem_ch * sizeof(float), cudaMemcpyHostToDevice, st));
+      R.sem = ctx->ing_sem.ptr;
+    }
+  }
+  R.score = ctx->ing_score.ptr;
+  R.valid = ctx->ing_valid.ptr;
+  R.hist = ctx->ing_hist.ptr;
+  KREG_CUDA(cudaMemsetAsync(R.hist, 0, 256 * sizeof(unsigned long long), st));
+  unsigned long long hist[256] = {};
+  if (npx) {
+    kreg_dev::ingest_score(R, st);
+    KREG_CUDA(cudaMemcpyAsync(hist, R.hist, sizeof(hist), cudaMemcpyDeviceToHost, st));
+    KREG_CUDA(cudaStreamSynchronize(st));
+  }
+  long long total_valid = 0;
+  for (unsigned long long v : hist) total_valid += static_cast<long long>(v);
+  // corner count at threshold t: valid interior pixels with score > t (the
+  // reference's strict segment test at t; scores <= 0 never pass t >= 0.5)
+  auto count = [&](double t) {
+    long long c = 0;
+    for (int s = 1; s < 256; ++s)
+      if (static_cast<double>(s) > t) c += static_cast<long long>(hist[s]);
+    return c;
+  };
+  constexpr double kMinThreshold = 0.5;  // selector.cpp:81
+  double t = sel->initial_threshold, best_t = 0.0;
+  long best_gap = -1;
+  long long best_count = 0;
+  bool in_band = false;
+  for (int round = 0; round < sel->max_adjust_rounds; ++round) {
+    const long long cnt = count(t);
+    const long gap = cnt < sel->target_min ? sel->target_min - cnt : cnt > sel->target_max ? cnt - sel->target_max : 0;
+    if (best_gap < 0 || gap < best_gap) {
+      best_gap = gap;
+      best_t = t;
+      best_count = cnt;
+    }
+    if (gap == 0) {
+      in_band = true;
+      break;
+    }
+    if (cnt > sel->target_max) {
+      t *= sel->adjust_factor;
+    } else {
+      if (t <= kMinThreshold) break;
+      t = std::max(t / sel->adjust_factor, kMinThreshold);
+    }
+  }
+  const bool fallback = !in_band && best_count < sel->target_min;
+  info->count = fallback ? total_valid : best_count;
+  info->threshold = best_t;
+  info->in_band = in_band ? 1 : 0;
+  info->fallback = fallback ? 1 : 0;
+  info->valid_pixels = total_valid;
+  const long long n = info->count;
+  if (n == 0 || cap < n || !pixels) return;
+  R.threshold = best_t;
+  R.fallback = fallback ? 1 : 0;
+  const int nb = kreg_dev::ingest_blocks(static_cast<long long>(npx));
+  ctx->ing_block_count.ensure(nb + 1);
+  ctx->ing_block_off.ensure(nb + 2);
+  ctx->ing_pixels.ensure(2 * static_cast<size_t>(n));
+  R.block_count = ctx->ing_block_count.ptr;
+  R.block_off = ctx->ing_block_off.ptr;
+  R.pixels = ctx->ing_pixels.ptr;
+  R.cap = n;
+  const int D = 3 + R.sem_channels;
+  if (xyz && feat && !valid_mask) {
+    ctx->ing_xyz.ensure(3 * static_cast<size_t>(n));
+    ctx->ing_feat.ensure(static_cast<size_t>(D) * n);
+    R.xyz = ctx->ing_xyz.ptr;
+    R.feat = ctx->ing_feat.ptr;
+  }
+  kreg_dev::ingest_emit(R, true, st);
+  kreg_dev::ingest_emit(R, false, st);
+  KREG_CUDA(cudaMemcpyAsync(pixels, R.pixels, 2 * sizeof(int) * n, cudaMemcpyDeviceToHost, st));
+  if (R.xyz) {
+    KREG_CUDA(cudaMemcpyAsync(xyz, R.xyz, 3 * sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    KREG_CUDA(cudaMemcpyAsync(feat, R.feat, sizeof(double) * D * n, cudaMemcpyDeviceToHost, st));
+  }
+  KREG_CUDA(cudaStreamSynchronize(st));
+}
+
+}  // namespace
+extern "C" {
+
+kreg_status kreg_select_points(kreg_ctx* ctx, const uint8_t* rgb, int32_t channels, int32_t width, int32_t height,
+                               const uint8_t* valid_depth, const kreg_selector_config* sel, int32_t* pixels_uv,
+                               int64_t capacity, kreg_selection_info* info) {
+  return guarded([&] {
+    require(ctx && valid_depth, "NULL argument");
+    check_selector(sel);
+    run_ingest(ctx, nullptr, rgb, channels, nullptr, 0, valid_depth, width, height, nullptr, sel, pixels_uv, nullptr,
+               nullptr, capacity, info);
+  });
+}
+
+kreg_status kreg_depth_rgb_to_cloud(kreg_ctx* ctx, const uint16_t* depth, const uint8_t* rgb, int32_t channels,
+                                    const float* semantics, int32_t semantic_channels, int32_t width, int32_t height,
+                                    const kreg_camera_intrinsics* intr, const kreg_selector_config* sel, double* xyz,
+                                    double* features, int64_t capacity, kreg_selection_info* info) {
+  return guarded([&] {
+    require(ctx && depth, "NULL argument");
+    check_intr(intr);
+    check_selector(sel);
+    // the pixel list is device scratch here; positions and features are the output
+    std::vector<int32_t> px(capacity > 0 ? static_cast<size_t>(2 * capacity) : 0);
+    run_ingest(ctx, depth, rgb, channels, semantics, semantic_channels, nullptr, width, height, intr, sel,
+               px.empty() ? nullptr : px.data(), xyz, features, capacity, info);
+  });
+}
+
 kreg_status kreg_exact_cosine(kreg_ctx* ctx, const kreg_cloud_view* X, const kreg_cloud_view* Z, const double T[12],
                               const kreg_kernel_params* params, double* cosine, double parts[3]) {
   return guarded([&] {
@@ -879,3 +1044,4 @@ void kreg_se3_inverse(const double T[12], double out[12]) { kreg_se3::inverse(T,
 double kreg_cloud_diameter(const kreg_cloud_view* view) { return diameter_host(view->xyz, view->n); }
 
 }  // extern "C"
+

@@ -209,6 +209,31 @@ void sweep_batched(const SweepReq* h_reqs, const SweepReq* d_reqs, int n, int sm
 void displacement(const double* zx, const double* zy, const double* zz, int n, const double* d_T2,
                   unsigned long long* d_out, cudaStream_t stream);
 
+// Frame ingest (ingest.cu): depth + RGB -> FAST-selected pixels -> cloud rows.
+struct IngestReq {
+  int w, h, channels, sem_channels;
+  const uint16_t* depth;     // w x h (null for select_points)
+  const uint8_t* rgb;        // w x h x channels
+  const float* sem;          // w x h x sem_channels or null
+  const uint8_t* valid_in;   // w x h mask (select_points) or null: derived from depth
+  int skip_top_rows;
+  double depth_scale, max_depth, fx, fy, cx, cy;
+  uint8_t* score;            // w x h: FAST score clamped at 0
+  uint8_t* valid;            // w x h
+  unsigned long long* hist;  // 256 bins of the score over valid pixels
+  double threshold;          // selection: score > threshold (or every valid pixel)
+  int fallback;
+  int* block_count;          // per 1024-pixel block
+  long long* block_off;      // exclusive prefix (+ total)
+  long long cap;             // output rows
+  int* pixels;               // cap x (u, v)
+  double* xyz;               // cap x 3 or null
+  double* feat;              // cap x (3 + sem_channels)
+};
+void ingest_score(const IngestReq& R, cudaStream_t stream);
+int ingest_blocks(long long pixels);
+void ingest_emit(const IngestReq& R, bool count_only, cudaStream_t stream);
+
 // K4 dense double sum over all pairs (a, b) of two clouds (dense.cu).
 constexpr int kMaxDenseDim = 32;
 struct DenseChannel {

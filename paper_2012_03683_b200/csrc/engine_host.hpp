@@ -156,6 +156,14 @@ struct kreg_ctx {
   kreg_host::DevBuf<double> arena_d;
   kreg_host::DevBuf<float> arena_f;
   kreg_host::DevBuf<double4> arena_w;
+  // frame ingest (kreg_depth_rgb_to_cloud / kreg_select_points)
+  kreg_host::DevBuf<uint8_t> ing_rgb, ing_valid_in, ing_score, ing_valid;
+  kreg_host::DevBuf<uint16_t> ing_depth;
+  kreg_host::DevBuf<float> ing_sem;
+  kreg_host::DevBuf<unsigned long long> ing_hist;
+  kreg_host::DevBuf<int> ing_block_count, ing_pixels;
+  kreg_host::DevBuf<long long> ing_block_off;
+  kreg_host::DevBuf<double> ing_xyz, ing_feat;
   // pair-list workspaces kept across registrations (device buffers keep capacity)
   std::vector<kreg_pairs*> pool;
   int max_active = 0;  // lockstep window of kreg_register_batch (0 = all at once)

@@ -1,0 +1,221 @@
+// Frame ingest ahead of the registration path: depth +
+// RGB (+ class probabilities) -> semi-dense cloud through the budgeted FAST
+// corner selector, as the reference's depth_rgb_to_cloud / select_points
+// (projection.cpp:30-75, selector.cpp:32-125, image.cpp:144-155).
+//
+// B200 formulation (byte / integer work, HBM-bound, no tensor cores):
+//  * k_fast_score: one thread per pixel over 32x8 tiles with a 3-pixel halo
+//    of luma in shared memory (luma computed from the interleaved RGB as the
+//    reference's integer rec601 formula). Per valid interior pixel the
+//    segment-test SCORE S = max over the 16 nine-sample arcs of the Bresenham
+//    circle of min(p - c) (brighter arc) or min(c - p) (darker arc), found as
+//    the smallest integer threshold at which the 16-bit brighter / darker
+//    masks lose their circular run of 9 (binary search, 8 mask tests). The
+//    reference's test "9 contiguous samples all > c + t or all < c - t" holds
+//    exactly when S > t (monotone in t), so one pass yields every threshold
+//    round: a 256-bin histogram of S over valid interior pixels.
+//  * the host replays the reference's threshold rounds on the histogram
+//    (counts for any t in O(256)), giving the same threshold, band flag and
+//    fallback decision without re-running the detector per round;
+//  * k_flag_count / k_block_scan / k_emit: order-preserving compaction of
+//    the selected pixels (raster order, as detect_corners' loops) fused with
+//    the FP64 back-projection p = d s ((u - cx)/fx, (v - cy)/fy, 1) and the
+//    feature rows (rgb / 255, class probabilities), in the reference's
+//    operation order (IEEE intrinsics: no contraction) -> bitwise identical.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "engine.cuh"
+
+namespace kreg_dev {
+
+namespace {
+
+constexpr int kTileW = 32, kTileH = 8, kHalo = 3;
+
+__device__ __forceinline__ int luma(const uint8_t* rgb, int channels, long long i) {
+  if (channels == 1) return rgb[i];
+  const uint8_t* p = rgb + i * channels;  // image.cpp:149-150 (integer division)
+  return (299 * p[0] + 587 * p[1] + 114 * p[2]) / 1000;
+}
+
+__global__ void __launch_bounds__(kTileW* kTileH) k_fast_score(IngestReq R) {
+  __shared__ int g[kTileH + 2 * kHalo][kTileW + 2 * kHalo];
+  __shared__ unsigned hist[256];
+  const int tx = threadIdx.x % kTileW, ty = threadIdx.x / kTileW;
+  const int u0 = blockIdx.x * kTileW, v0 = blockIdx.y * kTileH;
+  for (int k = threadIdx.x; k < 256; k += blockDim.x) hist[k] = 0;
+  for (int k = threadIdx.x; k < (kTileH + 2 * kHalo) * (kTileW + 2 * kHalo); k += blockDim.x) {
+    const int yy = k / (kTileW + 2 * kHalo), xx = k % (kTileW + 2 * kHalo);
+    const int u = u0 + xx - kHalo, v = v0 + yy - kHalo;
+    g[yy][xx] = (u >= 0 && u < R.w && v >= 0 && v < R.h) ? luma(R.rgb, R.channels, (long long)v * R.w + u) : 0;
+  }
+  __syncthreads();
+  const int u = u0 + tx, v = v0 + ty;
+  int score = 0;
+  bool valid = false;
+  if (u < R.w && v < R.h) {
+    const long long i = (long long)v * R.w + u;
+    if (R.valid_in) {
+      valid = R.valid_in[i] != 0;
+    } else {  // projection.cpp:42-49: row >= skip_top_rows, d != 0, d * scale <= max_depth
+      const uint16_t d = R.depth[i];
+      valid = v >= R.skip_top_rows && d != 0 && !((double)d * R.depth_scale > R.max_depth);
+    }
+    if (valid && u >= 3 && u < R.w - 3 && v >= 3 && v < R.h - 3) {  // detect_corners' loop bounds
+      // Bresenham circle of radius 3, clockwise from 12 o'clock
+      // (selector.cpp:24-27); unrolled, the offsets are immediates
+      const int cdx[16] = {0, 1, 2, 3, 3, 3, 2, 1, 0, -1, -2, -3, -3, -3, -2, -1};
+      const int cdy[16] = {-3, -3, -2, -1, 0, 1, 2, 3, 3, 3, 2, 1, 0, -1, -2, -3};
+      const int c = g[ty + kHalo][tx + kHalo];
+      int p[16];
+#pragma unroll
+      for (int s = 0; s < 16; ++s) p[s] = g[ty + kHalo + cdy[s]][tx + kHalo + cdx[s]];
+      // corner at integer threshold t: a circular run of 9 set bits in the
+      // 16-bit mask of samples brighter than c + t or of those darker than
+      // c - t (selector.cpp:33-50); monotone in t, so the score max(S, 0) is
+      // the smallest t >= 0 at which the pixel stops being a corner
+      int dd[16];
+#pragma unroll
+      for (int s = 0; s < 16; ++s) dd[s] = p[s] - c;
+      auto run9 = [](unsigned m) {
+        const unsigned x = m | (m << 16);
+        unsigned y = x;
+#pragma unroll
+        for (int k = 1; k < 9; ++k) y &= x >> k;
+        return (y & 0xFFFFu) != 0u;
+      };
+      auto corner_at = [&](int t) {
+        unsigned bright = 0u, dark = 0u;
+#pragma unroll
+        for (int s = 0; s < 16; ++s) {
+          bright |= (dd[s] > t ? 1u : 0u) << s;
+          dark |= (dd[s] < -t ? 1u : 0u) << s;
+        }
+        return run9(bright) || run9(dark);
+      };
+      int lo = 0, hi = 255;  // corner_at(255) is false (|p - c| <= 255)
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (corner_at(mid)) lo = mid + 1;
+        else hi = mid;
+      }
+      const int best = lo;
+      score = best;
+    }
+    R.score[i] = (uint8_t)(score > 0 ? score : 0);
+    R.valid[i] = valid ? 1 : 0;
+  }
+  if (valid) {
+    atomicAdd(&hist[score > 0 ? score : 0], 1u);
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < 256; k += blockDim.x)
+    if (hist[k]) atomicAdd(&R.hist[k], (unsigned long long)hist[k]);
+}
+
+constexpr int kScanBlock = 1024;
+
+__device__ __forceinline__ bool selected(const IngestReq& R, long long i) {
+  return R.valid[i] && (R.fallback || (double)R.score[i] > R.threshold);
+}
+
+// Selected pixels per block of kScanBlock raster-order pixels.
+__global__ void __launch_bounds__(kScanBlock) k_flag_count(IngestReq R) {
+  const long long i = (long long)blockIdx.x * kScanBlock + threadIdx.x;
+  const bool f = i < (long long)R.w * R.h && selected(R, i);
+  const int n = __syncthreads_count(f);
+  if (threadIdx.x == 0) R.block_count[blockIdx.x] = n;
+}
+
+// Exclusive scan of the block counts (one block; loops over chunks).
+__global__ void __launch_bounds__(kScanBlock) k_block_scan(IngestReq R, int n_blocks) {
+  __shared__ long long warp_tot[32];
+  long long carry = 0;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int b0 = 0; b0 < n_blocks; b0 += kScanBlock) {
+    const int b = b0 + threadIdx.x;
+    const long long v = b < n_blocks ? R.block_count[b] : 0;
+    long long inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    if (lane == 31) warp_tot[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+      long long t = warp_tot[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long s = __shfl_up_sync(0xffffffffu, t, o);
+        if (lane >= o) t += s;
+      }
+      warp_tot[lane] = t;
+    }
+    __syncthreads();
+    const long long ex = carry + (wid ? warp_tot[wid - 1] : 0) + inc - v;
+    if (b < n_blocks) R.block_off[b] = ex;
+    carry += warp_tot[31];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) R.block_off[n_blocks] = carry;
+}
+
+// Selected pixels in raster order: pixel list, FP64 positions and feature rows.
+__global__ void __launch_bounds__(kScanBlock) k_emit(IngestReq R) {
+  __shared__ int warp_n[kScanBlock / 32];
+  const long long i = (long long)blockIdx.x * kScanBlock + threadIdx.x;
+  const bool f = i < (long long)R.w * R.h && selected(R, i);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const unsigned m = __ballot_sync(0xffffffffu, f);
+  if (lane == 0) warp_n[wid] = __popc(m);
+  __syncthreads();
+  int before = 0;
+  for (int k = 0; k < wid; ++k) before += warp_n[k];
+  if (!f) return;
+  const long long k = R.block_off[blockIdx.x] + before + __popc(m & ((1u << lane) - 1u));
+  if (k >= R.cap) return;  // the host re-runs with the exact size
+  const int u = (int)(i % R.w), v = (int)(i / R.w);
+  R.pixels[2 * k] = u;
+  R.pixels[2 * k + 1] = v;
+  if (R.xyz) {
+    // projection.cpp:23-25 / :66: depth_m * ((u - cx)/fx, (v - cy)/fy, 1)
+    const double dm = __dmul_rn((double)R.depth[i], R.depth_scale);
+    R.xyz[3 * k] = __dmul_rn(dm, __ddiv_rn(__dsub_rn((double)u, R.cx), R.fx));
+    R.xyz[3 * k + 1] = __dmul_rn(dm, __ddiv_rn(__dsub_rn((double)v, R.cy), R.fy));
+    R.xyz[3 * k + 2] = __dmul_rn(dm, 1.0);
+    double* f = R.feat + k * (3 + R.sem_channels);
+    // projection.cpp:67-69: rgb.at(u, v, c) = data[(v w + u) channels + c]
+    // (a 1-channel image reads the next pixels, as the reference does)
+    const long long end = (long long)R.w * R.h * R.channels;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const long long at = i * R.channels + c;
+      f[c] = __ddiv_rn((double)(at < end ? R.rgb[at] : 0), 255.0);
+    }
+    for (int c = 0; c < R.sem_channels; ++c) f[3 + c] = (double)R.sem[i * R.sem_channels + c];
+  }
+}
+
+}  // namespace
+
+void ingest_score(const IngestReq& R, cudaStream_t st) {
+  const dim3 grid((R.w + kTileW - 1) / kTileW, (R.h + kTileH - 1) / kTileH);
+  k_fast_score<<<grid, kTileW * kTileH, 0, st>>>(R);
+}
+
+int ingest_blocks(long long pixels) { return (int)((pixels + kScanBlock - 1) / kScanBlock); }
+
+void ingest_emit(const IngestReq& R, bool count_only, cudaStream_t st) {
+  const int nb = ingest_blocks((long long)R.w * R.h);
+  if (count_only) {
+    k_flag_count<<<nb, kScanBlock, 0, st>>>(R);
+    k_block_scan<<<1, kScanBlock, 0, st>>>(R, nb);
+  } else {
+    k_emit<<<nb, kScanBlock, 0, st>>>(R);
+  }
+}
+
+}  // namespace kreg_dev

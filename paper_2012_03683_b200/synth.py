@@ -453,3 +453,25 @@ def perturbed(T: Isometry, seed: int, angle: float = math.radians(0.5), trans: f
     rng = SplitMix64(seed)
     from .types import compose
     return compose(random_isometry(rng, angle, trans), T)
+
+
+def kitti_frame(seed: int, width: int = 1241, height: int = 376, classes: int = 19, block: int = 4):
+    """Synthetic KITTI-sized stereo frame for the ingest path (SURVEY §8f rank
+    3): blocky random texture (FAST corners at block corners), a depth image in
+    KITTI's 1/256 m units with holes and far pixels, and per-pixel class
+    probabilities (normalised). Returns (depth u16 h x w, rgb u8 h x w x 3,
+    semantics f32 h x w x classes, intrinsics)."""
+    from .types import CameraIntrinsics
+    rng = np.random.default_rng(seed)
+    bh, bw = (height + block - 1) // block, (width + block - 1) // block
+    tex = rng.integers(0, 256, size=(bh, bw, 3), dtype=np.uint8)
+    rgb = np.repeat(np.repeat(tex, block, axis=0), block, axis=1)[:height, :width].copy()
+    v = np.arange(height)[:, None].astype(np.float64)
+    z = 4.0 + 60.0 * np.clip((height - v) / height, 0.02, 1.0) ** 2 + rng.normal(0.0, 0.05, size=(height, width))
+    depth = np.clip(z * 256.0, 0, 65535).astype(np.uint16)
+    depth[rng.random((height, width)) < 0.1] = 0  # holes
+    sem = rng.random((height, width, classes)).astype(np.float32)
+    sem /= sem.sum(axis=2, keepdims=True)
+    intr = CameraIntrinsics(fx=718.856, fy=718.856, cx=607.1928, cy=185.2157, depth_scale=1.0 / 256.0,
+                            max_depth=55.0, skip_top_rows=100)
+    return depth, rgb, sem, intr

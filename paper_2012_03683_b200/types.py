@@ -309,3 +309,42 @@ def raise_for(code: int, message: str):
     if code in (_abi.KREG_CUDA_ERROR, _abi.KREG_OUT_OF_MEMORY, _abi.KREG_NO_DEVICE):
         raise CudaError(message)
     raise RuntimeError(message)
+
+
+@dataclasses.dataclass
+class CameraIntrinsics:
+    """kreg::CameraIntrinsics (projection.hpp:12-19)."""
+    fx: float = 0.0
+    fy: float = 0.0
+    cx: float = 0.0
+    cy: float = 0.0
+    depth_scale: float = 1.0
+    max_depth: float = 55.0
+    skip_top_rows: int = 100
+
+    def cstruct(self):
+        return _abi.kreg_camera_intrinsics(self.fx, self.fy, self.cx, self.cy, self.depth_scale, self.max_depth,
+                                           self.skip_top_rows)
+
+
+@dataclasses.dataclass
+class SelectorConfig:
+    """kreg::SelectorConfig (selector.hpp:12-18)."""
+    target_min: int = 3000
+    target_max: int = 15000
+    initial_threshold: float = 20.0
+    adjust_factor: float = 1.5
+    max_adjust_rounds: int = 20
+
+    def cstruct(self):
+        return _abi.kreg_selector_config(self.target_min, self.target_max, self.initial_threshold, self.adjust_factor,
+                                         self.max_adjust_rounds)
+
+
+@dataclasses.dataclass
+class Selection:
+    """kreg::Selection (selector.hpp:22-27): (u, v) pixels in raster order."""
+    pixels: list
+    threshold: float = 0.0
+    in_band: bool = False
+    note: str = ""

@@ -31,6 +31,11 @@ CP = C.POINTER(_abi.kreg_registration_config)
 RP = C.POINTER(_abi.kreg_registration_result)
 
 
+def _img(rgb):
+    a = np.ascontiguousarray(rgb, dtype=np.uint8)
+    return a[:, :, None] if a.ndim == 2 else a
+
+
 def _d12(T):
     a = (T.as12() if isinstance(T, Isometry) else np.ascontiguousarray(T, dtype=np.float64).reshape(12))
     return a, _abi.as_ptr(a)
@@ -69,6 +74,37 @@ class Oracle:
 
     def _err(self, rc):
         raise_for(rc, self.lib.ko_last_error().decode())
+
+    # frame ingest (selector.cpp / projection.cpp restated in C)
+    def select_points(self, rgb, valid, sel):
+        img = _img(rgb)
+        h, w, ch = img.shape
+        m = np.ascontiguousarray(valid, dtype=np.uint8)
+        px = np.zeros((w * h + 1, 2), dtype=np.int32)
+        thr, ib, fb = C.c_double(), C.c_int(), C.c_int()
+        cs = sel.cstruct()
+        L = self.lib
+        L.ko_select_points.restype = C.c_long
+        n = L.ko_select_points(img.ctypes.data_as(C.c_void_p), ch, w, h, m.ctypes.data_as(C.c_void_p), C.byref(cs),
+                               px.ctypes.data_as(C.c_void_p), C.byref(thr), C.byref(ib), C.byref(fb))
+        return [tuple(map(int, p)) for p in px[:n]], thr.value, bool(ib.value), bool(fb.value)
+
+    def depth_rgb_to_cloud(self, depth, rgb, sem, intr, sel):
+        d = np.ascontiguousarray(depth, dtype=np.uint16)
+        img = _img(rgb)
+        h, w, ch = img.shape
+        s = None if sem is None else np.ascontiguousarray(sem, dtype=np.float32)
+        sc = 0 if s is None else (1 if s.ndim == 2 else s.shape[2])
+        xyz = np.zeros((w * h + 1, 3))
+        feat = np.zeros((w * h + 1, 3 + sc))
+        ib, fb = C.c_int(), C.c_int()
+        ci, cs = intr.cstruct(), sel.cstruct()
+        L = self.lib
+        L.ko_depth_rgb_to_cloud.restype = C.c_long
+        n = L.ko_depth_rgb_to_cloud(d.ctypes.data_as(C.c_void_p), img.ctypes.data_as(C.c_void_p), ch,
+                                    None if s is None else s.ctypes.data_as(C.c_void_p), sc, w, h, C.byref(ci),
+                                    C.byref(cs), _abi.as_ptr(xyz), _abi.as_ptr(feat), C.byref(fb), C.byref(ib))
+        return xyz[:n], feat[:n], bool(fb.value)
 
     def build_pairs(self, X, Z, T, params: KernelParams, cutoff=3.0, c_min=1e-4, dense=False):
         h = P()
@@ -177,6 +213,38 @@ class Reference:
 
     def _err(self, rc):
         raise_for(rc, self.lib.kref_last_error().decode())
+
+    # frame ingest: the reference's select_points / depth_rgb_to_cloud
+    def select_points(self, rgb, valid, sel):
+        img = _img(rgb)
+        h, w, ch = img.shape
+        m = np.ascontiguousarray(valid, dtype=np.uint8)
+        px = np.zeros((w * h + 1, 2), dtype=np.int32)
+        info = _abi.kreg_selection_info()
+        note = C.create_string_buffer(256)
+        cs = sel.cstruct()
+        self._err(self.lib.kref_select_points(img.ctypes.data_as(C.c_void_p), ch, w, h, m.ctypes.data_as(C.c_void_p),
+                                              C.byref(cs), px.ctypes.data_as(C.c_void_p), C.c_int64(w * h + 1),
+                                              C.byref(info), note, 256))
+        return ([tuple(map(int, p)) for p in px[:info.count]], info.threshold, bool(info.in_band),
+                note.value.decode())
+
+    def depth_rgb_to_cloud(self, depth, rgb, sem, intr, sel):
+        d = np.ascontiguousarray(depth, dtype=np.uint16)
+        img = _img(rgb)
+        h, w, ch = img.shape
+        s = None if sem is None else np.ascontiguousarray(sem, dtype=np.float32)
+        sc = 0 if s is None else (1 if s.ndim == 2 else s.shape[2])
+        xyz = np.zeros((w * h + 1, 3))
+        feat = np.zeros((w * h + 1, 3 + sc))
+        n = C.c_int64()
+        note = C.create_string_buffer(256)
+        ci, cs = intr.cstruct(), sel.cstruct()
+        self._err(self.lib.kref_depth_rgb_to_cloud(
+            d.ctypes.data_as(C.c_void_p), img.ctypes.data_as(C.c_void_p), ch,
+            None if s is None else s.ctypes.data_as(C.c_void_p), sc, w, h, C.byref(ci), C.byref(cs),
+            _abi.as_ptr(xyz), _abi.as_ptr(feat), C.c_int64(w * h + 1), C.byref(n), note, 256))
+        return xyz[:n.value], feat[:n.value], note.value.decode()
 
     def set_threads(self, n):
         self.lib.kref_set_threads(int(n))
