@@ -604,15 +604,20 @@ def depth_rgb_to_cloud(depth, rgb, semantics, intr: CameraIntrinsics, sel: Selec
     info = _abi.kreg_selection_info()
     ci, cs = intr.cstruct(), sel.cstruct()
     sem_p = sem.ctypes.data_as(C.c_void_p) if sem is not None else None
-    _check(lib().kreg_depth_rgb_to_cloud(ctx.h, d.ctypes.data_as(C.c_void_p), img.ctypes.data_as(C.c_void_p), ch,
-                                         sem_p, n_sem, w, h, C.byref(ci), C.byref(cs), None, None, 0, C.byref(info)))
-    n = int(info.count)
-    xyz = np.zeros((max(n, 1), 3))
-    feat = np.zeros((max(n, 1), 3 + n_sem))
-    if n:
+    # one call when the selection fits the guess (the band's upper end, or the
+    # previous frame's count); otherwise a second call with the exact size
+    cap = max(int(sel.target_max), getattr(ctx, "_ingest_cap", 0))
+    for _ in range(2):
+        xyz = np.zeros((cap, 3))
+        feat = np.zeros((cap, 3 + n_sem))
         _check(lib().kreg_depth_rgb_to_cloud(ctx.h, d.ctypes.data_as(C.c_void_p), img.ctypes.data_as(C.c_void_p), ch,
                                              sem_p, n_sem, w, h, C.byref(ci), C.byref(cs), _abi.as_ptr(xyz),
-                                             _abi.as_ptr(feat), n, C.byref(info)))
+                                             _abi.as_ptr(feat), cap, C.byref(info)))
+        n = int(info.count)
+        if n <= cap:
+            break
+        cap = n
+    ctx._ingest_cap = max(getattr(ctx, "_ingest_cap", 0), n)
     note = _selection_note(info, sel)
     if warnings is not None and note:
         warnings.append(note)
