@@ -96,6 +96,7 @@ void dense_sums(const DenseReq* h, const DenseReq* d, int n, int b_chunks, cudaS
   if (max_d == 0) k_dense<0><<<grid, kDenseThreads, 0, st>>>(d);
   else if (max_d <= 8) k_dense<8><<<grid, kDenseThreads, 0, st>>>(d);
   else k_dense<kMaxDenseDim><<<grid, kDenseThreads, 0, st>>>(d);
+  note_launches(1);
 }
 
 int dense_blocks_a(int n_a) { return (n_a + kDenseThreads - 1) / kDenseThreads; }

@@ -260,5 +260,6 @@ void filter_emit_index(const BuildReq* d_req, int n_z, cudaStream_t stream);
 void interleave_positions(const double* x, const double* y, const double* z, int n, double4* out, cudaStream_t stream);
 
 long long kernel_launch_count();
+void note_launches(int n);  // launches issued from other translation units
 
 }  // namespace kreg_dev

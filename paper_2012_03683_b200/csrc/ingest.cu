@@ -204,6 +204,7 @@ __global__ void __launch_bounds__(kScanBlock) k_emit(IngestReq R) {
 void ingest_score(const IngestReq& R, cudaStream_t st) {
   const dim3 grid((R.w + kTileW - 1) / kTileW, (R.h + kTileH - 1) / kTileH);
   k_fast_score<<<grid, kTileW * kTileH, 0, st>>>(R);
+  note_launches(1);
 }
 
 int ingest_blocks(long long pixels) { return (int)((pixels + kScanBlock - 1) / kScanBlock); }
@@ -213,8 +214,10 @@ void ingest_emit(const IngestReq& R, bool count_only, cudaStream_t st) {
   if (count_only) {
     k_flag_count<<<nb, kScanBlock, 0, st>>>(R);
     k_block_scan<<<1, kScanBlock, 0, st>>>(R, nb);
+    note_launches(2);
   } else {
     k_emit<<<nb, kScanBlock, 0, st>>>(R);
+    note_launches(1);
   }
 }
 

@@ -1559,6 +1559,7 @@ void interleave_positions(const double* x, const double* y, const double* z, int
 }
 
 long long kernel_launch_count() { return g_launches.load(); }
+void note_launches(int n) { count_launch(n); }
 
 }  // namespace kreg_dev
 
