@@ -378,7 +378,10 @@ std::unique_ptr<AsyncUpload> cloud_upload_async(kreg_ctx* ctx, const kreg_cloud_
   up->ready = std::vector<std::atomic<int>>(static_cast<size_t>(n_jobs));
   for (auto& r : up->ready) r.store(0);
   const unsigned hw = std::max(2u, std::thread::hardware_concurrency());
-  const int workers = static_cast<int>(std::min<unsigned>(std::min<unsigned>(hw - 1, 31u), static_cast<unsigned>(n_jobs)));
+  // staging threads (the solver thread keeps a core); KREG_STAGE_WORKERS overrides
+  unsigned cap = std::min(hw - 1, 31u);
+  if (const char* e = std::getenv("KREG_STAGE_WORKERS")) cap = std::max(1, std::atoi(e));
+  const int workers = static_cast<int>(std::min<unsigned>(cap, static_cast<unsigned>(n_jobs)));
   auto next = std::make_shared<std::atomic<int>>(0);
   AsyncUpload* U = up.get();
   const int device = ctx->device;
