@@ -5,19 +5,22 @@
 //   index locality == spatial locality):
 //     x/y/z        FP64 SoA positions            (build test, q = T z)
 //     feat         FP32 rows, stride fstride=4k  (c_ij in the pair build)
-//   Grid (per lengthscale level, over target X): dense cell index over the
-//     bbox of X, cell = cutoff*(1+1e-7) so the 27-cell stencil is a superset
-//     of the FP64 cutoff ball; counting sort with a deterministic order
+//   Grid (per candidate-list build, over target X): dense cell index over
+//     the bbox of X, cell = R_s (1 + 1e-7) so the 27-cell stencil is a
+//     superset of the FP64 R_s ball; counting sort with a deterministic order
 //     inside a cell (ascending point index) -> cell_start[] / cell_items[]
-//     plus cell-ordered FP64 copies cx/cy/cz for coalesced candidate tests.
-//   Pair list (per build): sliced ELL over tiles of 32 consecutive sources:
-//     tile t holds 32 columns (one per source j = 32 t + l) of tile_deg[t]
-//     slots (a multiple of kUnitSteps); slot (t, k, l) = tile_off[t] + 32 k
-//     + l; a slot is int4 {x_i in fixed point (2^-k m around the X bbox
-//     centre), float_as_int(log2 c)} = 16 B, so the sweep streams slots with
-//     TMA and never gathers; padding {0,0,0,-inf}. slot_i[] keeps the target
-//     index (export only); CSR offsets (int64[n_z+1]) record true degrees.
-//   Sweep scratch: per-work-block FP64 partials; per-request counters.
+//     plus cell-ordered FP64 positions and FP32 feature rows.
+//   Candidate list (reused across levels): per tile of 32 Morton-consecutive
+//     sources, 32 rows of H_t entries {x_i - Ts z_j (FP32 x3), log2 c} (16 B)
+//     + target index; R_s = cutoff (1 + skin).
+//   Sweep list (per build): sources degree-sorted inside windows of 1024,
+//     tiles of 32 sorted sources, column height rounded to units of
+//     kUnitSteps steps; slot = the candidate entry it was filtered from
+//     (16 B, the sweep subtracts (T - Ts) z_j); source-major XOR-swizzled
+//     units (slot_index); padding {0,0,0,-inf}; chunk records carry the
+//     first tile's sources so the TMA stream has no dependent loads.
+//   Sweep scratch: per-chunk and per-group FP64 partials; self-resetting
+//     launch control blocks.
 #pragma once
 
 #include <cstdint>
@@ -106,7 +109,7 @@ struct alignas(16) ChunkRec {
 // One pair-list build for one registration, in two stages:
 //  candidate stage (full = 1 only): grid over X + 27-cell search at the
 //    enlarged radius R_s = cutoff (1 + skin) around Ts z_j, c_ij and the
-//    c > c_min test -> candidate list {i, log2 c} (sliced ELL, 8 B entries);
+//    c > c_min test -> candidate list {x_i - Ts z_j, log2 c} (+ i), 16 B entries;
 //  filter stage (always): the reference predicate |x_i - T z_j|^2 <= cutoff^2
 //    (inner_product.cpp:69) over the candidate list -> sweep list.
 // The filter is exact while max_j |T z_j - Ts z_j| <= R_s - cutoff (triangle

@@ -246,7 +246,7 @@ struct kreg_pairs {
   kreg_host::DevBuf<int> count;            // degree per source (Morton order)
   kreg_host::DevBuf<int> perm, pos, deg_s; // degree-sorted sweep order of the sources
   kreg_host::DevBuf<long long> tile_off;
-  kreg_host::DevBuf<int4> slot_buf;        // sliced-ELL slots {x fixed point, log2 c}
+  kreg_host::DevBuf<int4> slot_buf;        // sweep-list slots {x_i - Ts z_j (FP32 x3), log2 c}
   kreg_host::DevBuf<int> slot_i;           // target index per slot (export only)
   kreg_host::DevBuf<int> unit_off;
   kreg_host::DevBuf<float4> zs;                 // sources in sweep order (FP32)

@@ -1,12 +1,14 @@
 // sm_100a kernels of the CVO registration hot path.
 //
 //  K1  grid build      : k_cell_assign, batched exclusive scan, k_scatter, k_rank
-//  K2  pair build      : k_pair_pass<EMIT=false> (count), scan, k_pair_pass<EMIT=true>
-//                        (emit (i, log2 c) + chunk table)
-//  K3  fused sweep     : k_transform_sources (q = T z in FP64 -> fixed point,
-//                        fused max displacement), k_sweep<MAXM> (F + SE(3)
-//                        gradient for up to 8 candidate transforms per pass,
-//                        MUFU ex2, deterministic FP64 block/grid reduction)
+//  K2  pair build      : candidate stage k_pair_pass<COUNT/EMIT> (grid search
+//                        at R_s, c_ij) + k_tile_offsets<SUP>; filter stage
+//                        k_filter<COUNT/EMIT> (or k_refilter), k_order,
+//                        k_tile_offsets, k_chunk_records
+//  K3  fused sweep     : k_sweep<NPG> (persistent, TMA-fed; F + SE(3) gradient
+//                        for up to 8 candidate transforms per pass, MUFU ex2,
+//                        FP64 displacement items, deterministic fixed-order
+//                        chunk / group / request reductions)
 //
 // Reference semantics (file:line under /root/reference/proj):
 //   k_geo          kernels.hpp:37-47          c_ij      kernels.cpp:18-53
@@ -816,11 +818,12 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 //    - delta = x_i - T_m z_j, r^2, w = ex2(r^2 kappa + log2 c) on MUFU, W += w,
 //    S += w d; candidates in pairs on FFMA2/FADD2/FMUL2. Per tile: torque +=
 //    a_j x S_j (sum_j q_j x S_j = sum_j (q_j - a) x S_j + a x sum S).
-//  * Each chunk's sums are one partial (FP32 warp sums widened to FP64);
-//    k_sweep_reduce adds a request's partials in a fixed order: bitwise
-//    reproducible, independent of scheduling and batch composition.
-//  * max_j |T_m z_j - T_b z_j| (inner_product.cpp:238-246) comes from
-//    k_displacement_batched in FP64 over the original coordinates.
+//  * Each chunk's sums are one partial (FP32 warp sums widened to FP64); the
+//    warp finishing a chunk group, then the one finishing the request, add
+//    the partials in a fixed shuffle-tree order: bitwise reproducible,
+//    independent of scheduling and batch composition.
+//  * max_j |T_m z_j - T_b z_j| (inner_product.cpp:238-246) comes from the
+//    launch's displacement work items in FP64 over the original coordinates.
 __device__ __forceinline__ long long request_units(const SweepReq& R) {
   // an overflowed build is skipped (its result is discarded by the host); the
   // unit count is passed by the host when the pair list was built earlier
