@@ -217,10 +217,10 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=25.0)
     args = ap.parse_args()
 
-    world, rank, local = dist_setup()
-    if args.impl == "reference":
-        run_reference_arm(args, world, rank)
+    if args.impl == "reference":  # CPU only: no process group, ranks > 0 exit at once
+        run_reference_arm(args, int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")))
         return
+    world, rank, local = dist_setup()
 
     from paper_2012_03683_b200 import api
     ctx = api.Context(local)
