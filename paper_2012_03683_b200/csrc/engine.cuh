@@ -33,7 +33,7 @@ constexpr int kSweepThreads = 256;  // threads per persistent sweep CTA (2 CTAs 
 #define KREG_UNIT_STEPS 2
 #endif
 #ifndef KREG_SWEEP_STAGES
-#define KREG_SWEEP_STAGES 3
+#define KREG_SWEEP_STAGES 2
 #endif
 constexpr int kUnitSteps = KREG_UNIT_STEPS;      // degree steps per sweep unit (x 32 lanes x 16 B)
 #ifndef KREG_STAGE_UNITS
