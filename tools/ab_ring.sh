@@ -1,5 +1,5 @@
 mkdir -p gpurun_out
-for lib in paper_2012_03683_b200/libkreg_b200.so paper_2012_03683_b200/_variants/ring_*.so paper_2012_03683_b200/libkreg_b200.so; do
+for lib in paper_2012_03683_b200/libkreg_b200.so paper_2012_03683_b200/_variants/${AB_GLOB:-ring_*}.so paper_2012_03683_b200/libkreg_b200.so; do
   n=$(basename $lib .so)
   KREG_LIB=$PWD/$lib timeout 300 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "golden or deterministic" > gpurun_out/ab_$n.test 2>&1
   echo "$n test rc=$?" >> gpurun_out/ab_summary.txt
