@@ -29,6 +29,10 @@
 namespace kreg_dev {
 
 constexpr int kSweepThreads = 256;  // threads per persistent sweep CTA (2 CTAs per SM)
+#ifndef KREG_SWEEP_CTAS_PER_SM
+#define KREG_SWEEP_CTAS_PER_SM 2
+#endif
+constexpr int kSweepCtasPerSm = KREG_SWEEP_CTAS_PER_SM;  // persistent grid: CTAs per SM
 #ifndef KREG_UNIT_STEPS
 #define KREG_UNIT_STEPS 2
 #endif

@@ -1308,7 +1308,7 @@ __device__ unsigned g_tl_n;
 #endif
 
 template <int NPG>
-__global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(const SweepReq* reqs, int n_req, SweepCtl* ctl) {
+__global__ void __launch_bounds__(kSweepThreads, kSweepCtasPerSm) k_sweep(const SweepReq* reqs, int n_req, SweepCtl* ctl) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #ifdef KREG_TIMELINE
   const unsigned long long tl0 = gtimer();
@@ -1524,7 +1524,7 @@ void sweep_batched(const SweepReq* h, const SweepReq* d, int n, int sm_count, un
   for (int r0 = 0; r0 < n; r0 += kMaxSweepReqs) {
     const int r1 = min(n, r0 + kMaxSweepReqs);
     int max_mg = 1;
-    // persistent grid of 2 CTAs per SM, fewer when the work items of the
+    // persistent grid of kSweepCtasPerSm CTAs per SM, fewer when the work items of the
     // launch are known on the host (lists built in earlier rounds): every
     // warp then has at least one item and idle CTAs are not launched
     long long items = 0;
@@ -1533,7 +1533,7 @@ void sweep_batched(const SweepReq* h, const SweepReq* d, int n, int sm_count, un
       items += h[r].units >= 0 ? chunk_count(h[r].units, h[r].chunk_pref) + (h[r].n_z + kDispItem - 1) / kDispItem
                                : (1LL << 40);
     }
-    const int grid = (int)max(1LL, min((long long)2 * sm_count, (items + kSweepWarps - 1) / kSweepWarps));
+    const int grid = (int)max(1LL, min((long long)kSweepCtasPerSm * sm_count, (items + kSweepWarps - 1) / kSweepWarps));
     const SweepReq* dr = d + r0;
     SweepCtl* ctl = reinterpret_cast<SweepCtl*>(d_ctl) + launches;
     if (max_mg <= 2) k_sweep<1><<<grid, kSweepThreads, kSweepSmem, st>>>(dr, r1 - r0, ctl);
