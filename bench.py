@@ -247,6 +247,7 @@ def main():
     iters = []
     for _ in range(args.steps):
         res, st = api.register_batch(dev_X, dev_Z, inits, params, cfg, ctx=ctx)
+        assert (np.asarray(st) == 0).all(), f"failed registrations in a timed step: {list(st)}"
         iters += [r.iterations for r in res if r is not None]
     ctx.synchronize()
     dt = time.perf_counter() - t0
@@ -268,6 +269,7 @@ def main():
     t0 = time.perf_counter()
     for _ in range(args.steps):
         res_h, st_h = api.register_batch_host(Xs, Zs, inits, params, cfg, ctx=ctx)
+        assert (np.asarray(st_h) == 0).all(), f"failed registrations in a timed step: {list(st_h)}"
     ctx.synchronize()
     dt_e2e = max_over_ranks(time.perf_counter() - t0, world)
     host_e2e = ctx.host_stats()

@@ -453,6 +453,8 @@ double ko_inner_product(const ko_pairs* p, const kreg_cloud_view* X, const kreg_
                         const double T[12], const kreg_kernel_params* params) {
   if (p->n == 0) return 0.0;
   double* partial = (double*)calloc((size_t)p->n_z, sizeof(double));
+  /* per-j partials, fixed-shape reduction: thread-count independent (reduce.hpp:8-11) */
+#pragma omp parallel for schedule(dynamic, 64)
   for (int j = 0; j < p->n_z; ++j) {
     double q[3];
     apply(T, Z->xyz + 3 * j, q);
@@ -477,6 +479,7 @@ void ko_objective_and_gradient(const ko_pairs* p, const kreg_cloud_view* X,
   if (p->n == 0) return;
   const double inv_l2 = 1.0 / (params->lengthscale * params->lengthscale);
   double* partial = (double*)calloc((size_t)p->n_z * 7, sizeof(double));
+#pragma omp parallel for schedule(dynamic, 64)
   for (int j = 0; j < p->n_z; ++j) {
     double q[3];
     apply(T, Z->xyz + 3 * j, q);
@@ -592,6 +595,20 @@ static void push_trace(kreg_registration_result* r, int it, double f, double ind
   if (r->rebuild_trace) r->rebuild_trace[it] = (uint8_t)rebuilt;
 }
 
+/* Replay log (parity tests): per iteration, the transform T the iteration
+ * evaluates and the build transform / lengthscale of the pair list it uses
+ * (after the rebuild rule, registration.cpp:123-130). */
+static double* g_log_T = NULL;
+static double* g_log_Tb = NULL;
+static double* g_log_l = NULL;
+static int g_log_cap = 0;
+void ko_set_iteration_log(double* T, double* Tb, double* l, int cap) {
+  g_log_T = T;
+  g_log_Tb = Tb;
+  g_log_l = l;
+  g_log_cap = cap;
+}
+
 /* registration.cpp:100-189 register_clouds */
 int ko_register_clouds(const kreg_cloud_view* X, const kreg_cloud_view* Z, const double initial[12],
                        const kreg_kernel_params* params, const kreg_registration_config* cfg,
@@ -639,6 +656,11 @@ int ko_register_clouds(const kreg_cloud_view* X, const kreg_cloud_view* Z, const
       if (np == 0) break;
     }
 
+    if (iter < g_log_cap) {
+      if (g_log_T) memcpy(g_log_T + 12 * (size_t)iter, T, sizeof(double) * 12);
+      if (g_log_Tb) memcpy(g_log_Tb + 12 * (size_t)iter, pairs->build_transform, sizeof(double) * 12);
+      if (g_log_l) g_log_l[iter] = lengthscale;
+    }
     double ev[7];
     ko_objective_and_gradient(pairs, X, Z, T, &wp, ev);
     const double gnorm = sqrt((ev[1] * ev[1] + ev[2] * ev[2] + ev[3] * ev[3]) + (ev[4] * ev[4] + ev[5] * ev[5] + ev[6] * ev[6]));

@@ -62,6 +62,10 @@ int ko_check_config(const kreg_registration_config* config);
 int ko_register_clouds(const kreg_cloud_view* X, const kreg_cloud_view* Z,
                        const double initial[12], const kreg_kernel_params* params,
                        const kreg_registration_config* config, kreg_registration_result* result);
+/* Replay log for the next ko_register_clouds calls on this process (NULL /
+ * cap 0 disables): per iteration T (12), the pair list's build transform (12)
+ * and the lengthscale. */
+void ko_set_iteration_log(double* T, double* Tb, double* l, int cap);
 /* image.cpp:144-155 integer rec601 luma (channels 1 or >= 3) */
 void ko_to_gray(const uint8_t* rgb, int channels, int w, int h, uint8_t* gray);
 /* selector.cpp:29-51 segment test (16-pixel circle, 9 contiguous, strict) */

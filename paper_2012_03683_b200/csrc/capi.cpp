@@ -51,7 +51,7 @@ void check_build_args(const kreg_cloud* X, const kreg_cloud* Z, const Params& p,
 }
 
 // Evaluate K transforms (any K) against a built pair list; out K x 8.
-void eval_many(kreg_ctx* ctx, kreg_pairs* p, const double* T, int K, double lengthscale, double* out) {
+void eval_many(kreg_ctx* ctx, kreg_pairs* p, const double* T, int K, double lengthscale, double sigma, double* out) {
   std::vector<BuildJob> none;
   std::vector<EvalJob> evals;
   for (int b = 0; b < K; b += kreg_dev::kMaxCandidates) {
@@ -60,6 +60,7 @@ void eval_many(kreg_ctx* ctx, kreg_pairs* p, const double* T, int K, double leng
     e.M = std::min(kreg_dev::kMaxCandidates, K - b);
     for (int m = 0; m < e.M; ++m) std::memcpy(e.T[m], T + 12 * (b + m), sizeof(double) * 12);
     e.lengthscale = lengthscale;
+    e.sigma = sigma;
     e.out = out + static_cast<size_t>(b) * kreg_dev::kOut;
     evals.push_back(e);
   }
@@ -205,6 +206,7 @@ kreg_status kreg_ctx_create(int32_t device, kreg_ctx** out) {
     auto ctx = std::make_unique<kreg_ctx>();
     ctx->device = device;
     KREG_CUDA(cudaSetDevice(device));
+    KREG_CUDA(kreg_dev::init_device());
     KREG_CUDA(cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device));
     KREG_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
     ctx->launches_base = kreg_dev::kernel_launch_count();
@@ -434,7 +436,7 @@ kreg_status kreg_eval_transforms(kreg_ctx* ctx, const kreg_pairs* pairs, const k
       }
       return;
     }
-    eval_many(ctx, const_cast<kreg_pairs*>(pairs), T, K, params->lengthscale, out);
+    eval_many(ctx, const_cast<kreg_pairs*>(pairs), T, K, params->lengthscale, params->sigma, out);
   });
 }
 
@@ -477,7 +479,7 @@ kreg_status kreg_indicator(kreg_ctx* ctx, const kreg_cloud* X, const kreg_cloud*
     if (X->n == 0 || Z->n == 0) throw Error(KREG_INVALID_ARGUMENT, "indicator: clouds must be non-empty");
     std::unique_ptr<kreg_pairs> p(build(ctx, X, Z, T, to_params(params), cutoff_multiplier, c_min));
     double o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    if (p->P > 0) eval_many(ctx, p.get(), T, 1, params->lengthscale, o);
+    if (p->P > 0) eval_many(ctx, p.get(), T, 1, params->lengthscale, params->sigma, o);
     const double denom = std::sqrt(static_cast<double>(X->n) * static_cast<double>(Z->n));
     *value = denom > 0.0 ? o[0] / denom : 0.0;
   });
@@ -541,7 +543,7 @@ kreg_status kreg_line_search(kreg_ctx* ctx, const kreg_cloud* X, const kreg_clou
       eps[static_cast<size_t>(k)] = e;
       e *= config->step_shrink;
     }
-    if (pairs->P > 0) eval_many(ctx, const_cast<kreg_pairs*>(pairs), Ts.data(), K + 1, params->lengthscale, out.data());
+    if (pairs->P > 0) eval_many(ctx, const_cast<kreg_pairs*>(pairs), Ts.data(), K + 1, params->lengthscale, params->sigma, out.data());
     *step = 0.0;
     for (int k = 0; k < K; ++k)
       if (out[8 * (k + 1)] > out[0]) {
@@ -758,6 +760,7 @@ kreg_status kreg_indicator_sweep(kreg_ctx* ctx, const kreg_cloud_view* cloud, co
       e.M = 1;
       std::memcpy(e.T[0], T, sizeof(double) * 12);
       e.lengthscale = p.lengthscale;
+      e.sigma = p.sigma;
       e.out = outs.data() + 8 * k;
       evals.push_back(e);
     }

@@ -206,6 +206,9 @@ struct alignas(16) SweepReq {
   double* out;           // M x kOut
 };
 
+// Once per device (kreg_ctx_create): kernel attributes of the current device.
+cudaError_t init_device();
+
 // All launches go to `stream`; d_reqs are device copies of h_reqs.
 void build_pairs_batched(const BuildReq* h_reqs, const BuildReq* d_reqs, int n, cudaStream_t stream);
 // d_ctl: sweep_ctl_bytes(n) bytes of launch control blocks, zero between

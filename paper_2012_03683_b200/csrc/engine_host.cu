@@ -653,7 +653,7 @@ static void prepare_sweep(EvalJob& job, kreg_dev::SweepReq& R, double* partials,
   }
   const double l = job.lengthscale;
   R.kappa = static_cast<float>(-1.4426950408889634 / (2.0 * l * l));
-  R.sigma2 = p->sigma * p->sigma;
+  R.sigma2 = job.sigma * job.sigma;  // the call's sigma, not the build's (inner_product.cpp:100,126)
   R.inv_l2 = 1.0 / (l * l);
   R.partials = partials;
   R.disp_bits = disp_bits;

@@ -326,6 +326,7 @@ struct EvalJob {
   int M;
   double T[kreg_dev::kMaxCandidates][12];
   double lengthscale;  // kernel lengthscale of the evaluation
+  double sigma = 1.0;  // kernel amplitude of the evaluation (params.sigma, inner_product.cpp:100,126)
   double* out;         // host, M x 8 {F, omega, v, disp}; filled after run_round
   bool grad = true;    // false: F + displacement only (gradient left zero)
 };

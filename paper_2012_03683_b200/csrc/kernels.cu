@@ -19,6 +19,8 @@
 
 #include <atomic>
 #include <cstdio>
+#include <mutex>
+#include <vector>
 
 #include "engine.cuh"
 
@@ -1502,18 +1504,33 @@ void build_pairs_batched(const BuildReq* h, const BuildReq* d, int n, cudaStream
   count_launch(launches + 3 + (cand ? 2 : 0) + (n_refilter ? 2 : 0));
 }
 
+// Per-device kernel attributes (the sweep's dynamic shared memory is above
+// the 48 KB default). cudaFuncSetAttribute applies to the current device
+// only, so every device a context is created on is initialised once.
+cudaError_t init_device() {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  static std::mutex mu;
+  static std::vector<char> done;
+  std::lock_guard<std::mutex> lk(mu);
+  if (dev < (int)done.size() && done[dev]) return cudaSuccess;
+  if ((e = cudaFuncSetAttribute(k_sweep<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepSmem)) != cudaSuccess)
+    return e;
+  if ((e = cudaFuncSetAttribute(k_sweep<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepSmem)) != cudaSuccess)
+    return e;
+  if ((e = cudaFuncSetAttribute(k_sweep<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepSmem)) != cudaSuccess)
+    return e;
+  if ((int)done.size() <= dev) done.resize(dev + 1, 0);
+  done[dev] = 1;
+  return cudaSuccess;
+}
+
 size_t sweep_ctl_bytes(int n) { return sizeof(SweepCtl) * ((n + kMaxSweepReqs - 1) / kMaxSweepReqs + 1); }
 
 void sweep_batched(const SweepReq* h, const SweepReq* d, int n, int sm_count, unsigned* d_ctl, cudaStream_t st,
                    cudaEvent_t ev0, cudaEvent_t ev1) {
   if (n == 0) return;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_sweep<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepSmem);
-    cudaFuncSetAttribute(k_sweep<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepSmem);
-    cudaFuncSetAttribute(k_sweep<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepSmem);
-    attr_set = true;
-  }
   if (ev0) cudaEventRecord(ev0, st);
   // requests arrive grouped: gradient requests first, then F-only ones; one
   // persistent launch per group (<= kMaxSweepReqs requests each), then one

@@ -253,6 +253,7 @@ void schedule_build_eval(Reg& r, std::vector<BuildJob>& builds, std::vector<Eval
   e.M = 1;
   std::memcpy(e.T[0], r.T, sizeof(r.T));
   e.lengthscale = r.lengthscale;
+  e.sigma = r.wp.sigma;
   e.out = r.ev;
   evals.push_back(e);
   eval_owner.push_back(&r);
@@ -305,6 +306,7 @@ void plan(Reg& r, std::vector<BuildJob>& builds, std::vector<EvalJob>& evals, st
           e.M = 1;
           std::memcpy(e.T[0], r.T, sizeof(r.T));
           e.lengthscale = r.lengthscale;
+          e.sigma = r.wp.sigma;
           e.out = r.ev;
           evals.push_back(e);
           owners.push_back(&r);
@@ -389,6 +391,7 @@ void plan(Reg& r, std::vector<BuildJob>& builds, std::vector<EvalJob>& evals, st
           e.M = std::min(kreg_dev::kMaxCandidates, n_new - b);
           for (int m = 0; m < e.M; ++m) std::memcpy(e.T[m], r.cand_T[b + m], sizeof(double) * 12);
           e.lengthscale = r.lengthscale;
+          e.sigma = r.wp.sigma;
           e.out = &r.cand_out[b][0];
           e.grad = r.cand_grad;
           evals.push_back(e);

@@ -71,6 +71,7 @@ class Oracle:
         L.ko_se3_inverse.argtypes = [_abi.dptr, _abi.dptr]
         L.ko_feature_coefficient.argtypes = [_abi.dptr, _abi.dptr, VP, KP]
         L.ko_feature_coefficient.restype = D
+        L.ko_set_iteration_log.argtypes = [P, P, P, C.c_int]
 
     def _err(self, rc):
         raise_for(rc, self.lib.ko_last_error().decode())
@@ -159,6 +160,22 @@ class Oracle:
         cfg = config.cstruct()
         self._err(self.lib.ko_register_clouds(X.view(), Z.view(), tp, params.cstruct(), C.byref(cfg), C.byref(buf.struct)))
         return RegistrationResult.from_buffers(buf)
+
+
+    def register_clouds_logged(self, X, Z, initial, params, config, capacity=None):
+        """register_clouds plus the replay log: per iteration the evaluated T,
+        the pair list's build transform and the lengthscale."""
+        cap = capacity or config.max_iterations
+        T = np.zeros((cap, 12))
+        Tb = np.zeros((cap, 12))
+        ls = np.zeros(cap)
+        self.lib.ko_set_iteration_log(T.ctypes.data, Tb.ctypes.data, ls.ctypes.data, cap)
+        try:
+            res = self.register_clouds(X, Z, initial, params, config, capacity)
+        finally:
+            self.lib.ko_set_iteration_log(None, None, None, 0)
+        n = res.iterations
+        return res, T[:n], Tb[:n], ls[:n]
 
 
 class _OraclePairs:
