@@ -8,10 +8,18 @@ error (constant-velocity prior). A step = one batch of B independent frame
 pairs registered to convergence on one GPU (lockstep batched host loop).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--impl ours|reference]
+                    [--mode throughput|latency] [--workload c3|first|c5] [--frames F] [--chains C]
 
 Prints ONE JSON line (rank 0). Multi-GPU: one process per GPU (torchrun),
 each rank registers its own B pairs (weak scaling, no data-path collective),
 time = max over ranks.
+
+Other measurements (not the driver's line; run by hand, results under profiles/):
+  --mode latency      one end-to-end kreg_register_clouds_host call per pair,
+                      pairs one after another (the CLI's `kreg register` path)
+  --workload first    the first-frame schedule (l 0.95 -> 0.0475) on B pairs
+  --workload c5       a KITTI-shaped sequence of F frames registered as C
+                      independent chains (kreg_register_sequence_chains)
 """
 from __future__ import annotations
 
@@ -141,10 +149,30 @@ def cloud_bytes(c) -> int:
     return c.positions.nbytes + c.features.nbytes
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def reference_env():
+    """OpenMP placement of the reference runs: one
+    thread per core, packed. Must be set before the runtime starts."""
+    os.environ.setdefault("OMP_PROC_BIND", "close")
+    os.environ.setdefault("OMP_PLACES", "cores")
+    return {"cpu": cpu_model(), "omp_proc_bind": os.environ["OMP_PROC_BIND"], "omp_places": os.environ["OMP_PLACES"]}
+
+
 def cpu_reference_sample(Xs, Zs, inits, params, cfg, seconds_budget: float = 30.0):
     """The compiled reference (oracle/_ref) on the box's host cores: latency
     mode (register_clouds with OpenMP over all threads, as the CLI runs it),
     pairs registered one after another until ~seconds_budget elapsed."""
+    env = reference_env()
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     from _checkers import Reference, ref_available, Oracle
     cores = os.cpu_count() or 1
@@ -167,15 +195,157 @@ def cpu_reference_sample(Xs, Zs, inits, params, cfg, seconds_budget: float = 30.
     dt = time.perf_counter() - t0
     return {"value": n / dt, "unit": UNIT, "cores": cores, "kind": kind,
             "sample": f"{n} KITTI-shaped 40k-point pair(s), register_clouds with OpenMP over {cores} threads, "
-                      f"{dt:.1f} s"}
+                      f"{dt:.1f} s", **env}
+
+
+# Per pair evaluation k_sweep issues 17 FP32 flops (3 sub, |d|^2 as 1 mul +
+# 2 FMA, the exponent FMA, W +=, 3 FMA into S) and one MUFU ex2. Nominal issue
+# rates on sm_100: 128 FP32 lanes (2 flops per FMA) and 16 MUFU lanes per SM
+# per clock.
+SWEEP_FLOPS_PER_PAIR = 17
+SM_COUNT = 148
+
+
+def issue_fractions(sweep, clk):
+    """FP32 and MUFU throughput of the sweep as fractions of nominal at the
+    measured SM clock: how close the pair loop is to its issue bound."""
+    if not sweep.get("sweep_ms"):
+        return {}
+    mhz = (clk or {}).get("sm_mhz") or 1965.0
+    pe = sweep["pair_evals"] / (sweep["sweep_ms"] * 1e-3)
+    fp32_peak = SM_COUNT * 128 * 2 * mhz * 1e6
+    mufu_peak = SM_COUNT * 16 * mhz * 1e6
+    return {"fp32_tflops": pe * SWEEP_FLOPS_PER_PAIR / 1e12,
+            "fp32_frac_of_nominal": pe * SWEEP_FLOPS_PER_PAIR / fp32_peak,
+            "mufu_frac_of_nominal": pe / mufu_peak,
+            "nominal_at_mhz": mhz}
+
+
+def run_other(args, world, rank, local):
+    """The hand-run measurements (module docstring). Prints one JSON line."""
+    from paper_2012_03683_b200 import api
+    ctx = api.Context(local)
+    params = synth.kitti_params()
+    clocks = ClockSampler(local)
+    if args.workload == "c5":
+        cfg = synth.kitti_subsequent_config()
+        t0 = time.perf_counter()
+        frames, _ = synth.kitti_sequence(1000 + rank, args.frames, args.points)
+        gen_s = time.perf_counter() - t0
+        for _ in range(args.warmup):
+            api.register_sequence(frames, params, cfg, ctx=ctx, chains=args.chains)
+        ctx.synchronize()
+        clocks.start()
+        barrier(world)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):  # frames resident on the device (uploaded by the warm-up)
+            seq = api.register_sequence(frames, params, cfg, ctx=ctx, chains=args.chains)
+        ctx.synchronize()
+        dt = max_over_ranks(time.perf_counter() - t0, world)
+        clk = clocks.stop()
+        # end to end: host frames in, every frame uploaded inside the timed call
+        ctx.reset_stats()
+        barrier(world)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            seq = api.register_sequence_host(frames, params, cfg, ctx=ctx, chains=args.chains)
+        ctx.synchronize()
+        dt_e2e = max_over_ranks(time.perf_counter() - t0, world)
+        io = ctx.io_stats()
+        n = sum_over_ranks((args.frames - 1) * args.steps, world)
+        line = {"metric": METRIC, "value": n / dt, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
+                "scaling": "weak", "dtype": "f32+f64", "data": "synthetic", "mode": "sequence",
+                "config": {"workload": f"C5 KITTI-shaped sequence, {args.frames} frames of {args.points} points, "
+                                       f"{args.chains} chains (kreg_register_sequence_chains)",
+                           "frame_generation_s": gen_s, "mean_iterations": float(np.mean(seq.iterations)),
+                           "fallbacks": int(np.sum(seq.fallback))},
+                "e2e": {"value": n / dt_e2e, "unit": UNIT, "h2d_bytes_per_step": io["h2d_bytes"] // args.steps,
+                        "d2h_bytes_per_step": io["d2h_bytes"] // args.steps},
+                "gpu_launches": ctx.kernel_launches(), "clocks": clk, "admission": ctx.admission_stats()}
+    else:
+        cfg = synth.kitti_first_config() if args.workload == "first" else synth.kitti_subsequent_config()
+        B = args.batch
+        Xs, Zs, inits = make_workload(rank, B, args.points)
+        if args.mode == "latency":
+            # one pair per call, host clouds in, results out: `kreg register`
+            n_pairs = max(1, args.steps)
+            for k in range(args.warmup):
+                api.register_clouds_host(Xs[k % B], Zs[k % B], inits[k % B], params, cfg, ctx=ctx)
+            ctx.synchronize()
+            ctx.reset_stats()
+            clocks.start()
+            barrier(world)
+            lat, its = [], []
+            for k in range(n_pairs):
+                t0 = time.perf_counter()
+                r = api.register_clouds_host(Xs[k % B], Zs[k % B], inits[k % B], params, cfg, ctx=ctx)
+                lat.append(time.perf_counter() - t0)
+                its.append(r.iterations)
+            clk = clocks.stop()
+            dt = max_over_ranks(sum(lat), world)
+            io = ctx.io_stats()
+            n = sum_over_ranks(n_pairs, world)
+            line = {"metric": METRIC, "value": n / dt, "unit": UNIT, "n_gpus": world, "steps": n_pairs,
+                    "warmup": args.warmup, "ms_per_step": dt / n_pairs * 1e3, "higher_is_better": True,
+                    "scaling": "weak", "dtype": "f32+f64", "data": "synthetic", "mode": "latency",
+                    "config": {"workload": f"{args.workload.upper()} KITTI-shaped {args.points}-point pairs, one "
+                                           "kreg_register_clouds_host call per pair",
+                               "mean_iterations": float(np.mean(its)),
+                               "latency_ms": {"p50": float(np.percentile(lat, 50) * 1e3),
+                                              "p90": float(np.percentile(lat, 90) * 1e3),
+                                              "max": float(np.max(lat) * 1e3)}},
+                    "e2e": {"value": n / dt, "unit": UNIT, "h2d_bytes_per_step": io["h2d_bytes"] // n_pairs,
+                            "d2h_bytes_per_step": io["d2h_bytes"] // n_pairs},
+                    "gpu_launches": ctx.kernel_launches(), "clocks": clk}
+        else:  # throughput, first-frame schedule
+            dev_X = [api.DeviceCloud(x, ctx) for x in Xs]
+            dev_Z = [api.DeviceCloud(z, ctx) for z in Zs]
+            for _ in range(args.warmup):
+                api.register_batch(dev_X, dev_Z, inits, params, cfg, ctx=ctx)
+            ctx.synchronize()
+            ctx.reset_stats()
+            ctx.set_profiling(True)
+            clocks.start()
+            barrier(world)
+            t0 = time.perf_counter()
+            its = []
+            for _ in range(args.steps):
+                res, st = api.register_batch(dev_X, dev_Z, inits, params, cfg, ctx=ctx)
+                assert (np.asarray(st) == 0).all(), f"failed registrations in a timed step: {list(st)}"
+                its += [r.iterations for r in res]
+            ctx.synchronize()
+            dt = max_over_ranks(time.perf_counter() - t0, world)
+            clk = clocks.stop()
+            ctx.set_profiling(False)
+            sweep, build = ctx.sweep_stats(), ctx.build_stats()
+            n = sum_over_ranks(B * args.steps, world)
+            line = {"metric": METRIC, "value": n / dt, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                    "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
+                    "scaling": "weak", "dtype": "f32+f64", "data": "synthetic", "mode": "throughput",
+                    "config": {"workload": f"first-frame schedule (l 0.95 -> 0.0475) on {B} KITTI-shaped "
+                                           f"{args.points}-point pairs", "mean_iterations": float(np.mean(its))},
+                    "gpu_launches": ctx.kernel_launches(), "clocks": clk,
+                    "sweep": {**sweep, **issue_fractions(sweep, clk)}, "build": build,
+                    "admission": ctx.admission_stats()}
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
 
 
 def run_reference_arm(args, world, rank):
-    """--impl reference: the reference CPU implementation on this box's cores."""
+    """--impl reference: the reference CPU implementation on this box's cores,
+    in both of its modes: latency (register_clouds with
+    OpenMP inside, one pair after another, as `kreg register` runs it: the
+    timed steps) and throughput (OpenMP over independent pairs, one thread each,
+    as synth_bench does, eval.cpp:323: one batch of `cores` pairs, reported
+    beside it). `value` is the better of the two."""
     if rank != 0:
         return
+    env = reference_env()
     params, cfg = synth.kitti_params(), synth.kitti_subsequent_config()
-    Xs, Zs, inits = make_workload(0, max(1, args.warmup + args.steps), args.points)
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     from _checkers import Reference, ref_available
     if not ref_available():
@@ -183,23 +353,42 @@ def run_reference_arm(args, world, rank):
         return
     r = Reference()
     cores = os.cpu_count() or 1
+    n_lat = max(1, args.warmup + args.steps)
+    Xs, Zs, inits = make_workload(0, n_lat + cores, args.points)
     r.set_threads(cores)
     for k in range(args.warmup):
         r.register_clouds(Xs[k], Zs[k], inits[k], params, cfg)
     t0 = time.perf_counter()
+    iters = []
     for k in range(args.warmup, args.warmup + args.steps):
-        r.register_clouds(Xs[k], Zs[k], inits[k], params, cfg)
+        iters.append(r.register_clouds(Xs[k], Zs[k], inits[k], params, cfg).iterations)
     dt = time.perf_counter() - t0
-    v = args.steps / dt
+    v_lat = args.steps / dt
+    # throughput mode: one thread per pair, `cores` pairs at once
+    res, st, secs = r.register_batch(Xs[n_lat:n_lat + cores], Zs[n_lat:n_lat + cores], inits[n_lat:n_lat + cores],
+                                     params, cfg)
+    v_thr = cores / secs if secs > 0 else 0.0
+    it_thr = [x.iterations for x in res if x is not None]
+    v = max(v_lat, v_thr)
+    mode = "latency" if v_lat >= v_thr else "throughput"
     print(json.dumps({
         "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "impl": "reference",
-        "config": {"workload": "C3 KITTI-shaped 40k-point semantic pairs, subsequent schedule", "points": args.points,
-                   "step": "one frame pair registered to convergence (latency mode)"},
+        "config": {"workload": "C3 KITTI-shaped 40k-point semantic pairs (colour + 19-class), subsequent schedule "
+                               "l 0.1 -> 0.0475", "points": args.points,
+                   "step": "one frame pair registered to convergence (latency mode)",
+                   "mean_iterations": float(np.mean(iters)),
+                   "pairs": "make_workload(rank 0): the first steps + warmup pairs of the GPU arm's batch"},
+        "cpu_modes": {"latency": {"value": v_lat, "pairs": args.steps, "threads_per_pair": cores,
+                                  "mean_iterations": float(np.mean(iters))},
+                      "throughput": {"value": v_thr, "pairs": cores, "threads_per_pair": 1, "seconds": secs,
+                                     "mean_iterations": float(np.mean(it_thr)) if it_thr else None},
+                      "reported": mode},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "reference",
-                         "sample": f"{args.steps} pairs, register_clouds with OpenMP over {cores} threads"},
+                         "sample": f"better of latency ({args.steps} pairs, OpenMP over {cores} threads) and "
+                                   f"throughput ({cores} pairs, one thread each)", **env},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
 
@@ -215,6 +404,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=25.0)
+    ap.add_argument("--mode", default="throughput", choices=["throughput", "latency"])
+    ap.add_argument("--workload", default="c3", choices=["c3", "first", "c5"])
+    ap.add_argument("--frames", type=int, default=257, help="c5: frames in the sequence")
+    ap.add_argument("--chains", type=int, default=16, help="c5: independent chains")
     args = ap.parse_args()
 
     if args.impl == "reference":  # CPU only: no process group, ranks > 0 exit at once
@@ -223,6 +416,8 @@ def main():
     world, rank, local = dist_setup()
 
     from paper_2012_03683_b200 import api
+    if args.mode != "throughput" or args.workload != "c3":
+        return run_other(args, world, rank, local)
     ctx = api.Context(local)
     ctx.set_max_active(args.window)
     params, cfg = synth.kitti_params(), synth.kitti_subsequent_config()
@@ -274,8 +469,9 @@ def main():
     dt_e2e = max_over_ranks(time.perf_counter() - t0, world)
     host_e2e = ctx.host_stats()
     e2e_value = sum_over_ranks(B * args.steps, world) / dt_e2e
-    h2d = sum(cloud_bytes(c) for c in Xs + Zs)
-    d2h = int(host_e2e["rounds"] / max(1, args.steps)) * 8 * 8 * 4  # per-round result block (<= 4 requests avg)
+    io = ctx.io_stats()  # bytes the engine copied host->device / read back, counted in the library
+    h2d = io["h2d_bytes"] // args.steps
+    d2h = io["d2h_bytes"] // args.steps
 
     # ---- roofline of the fused sweep kernel (dominant kernel)
     peaks = measured_peaks()
@@ -302,6 +498,7 @@ def main():
                 "algorithmic_bytes_per_pair": 8,
                 "pair_evals_per_s": sweep["pair_evals"] / (sweep["sweep_ms"] * 1e-3) if sweep["sweep_ms"] else 0.0,
                 "sweep_share_of_step": sweep["sweep_ms"] * 1e-3 / dt,
+                **issue_fractions(sweep, clk),
                 "peak_source": "MEASURED_PEAKS.json" if "hbm_gbs" in peaks else "fallback"}
 
     if rank == 0:

@@ -159,6 +159,14 @@ kreg_status kreg_ctx_set_profiling(kreg_ctx* ctx, int32_t enabled);
 /* Throughput mode: at most `n` registrations in flight at once (0 = all);
  * a finished registration is replaced by the next one immediately. */
 kreg_status kreg_ctx_set_max_active(kreg_ctx* ctx, int32_t n);
+/* Device-memory budget of the pair-list workspaces (bytes; 0 = admit against
+ * the device's free memory). kreg_register_batch / _sequence start a
+ * registration only when its workspace fits; the rest wait for a finished
+ * one. Results do not depend on the budget. Engine extension. */
+kreg_status kreg_ctx_set_memory_budget(kreg_ctx* ctx, int64_t bytes);
+/* Admission since the last reset: {most registrations in flight at once,
+ * admissions deferred for memory}. */
+kreg_status kreg_ctx_admission_stats(const kreg_ctx* ctx, int64_t out[2]);
 /* Host-side round accounting: {rounds, s preparing + launching, s waiting for
  * the device, s preparing builds, s preparing sweeps, s in the solver state
  * machines, device allocations so far (process), s spent in them (process)}. */
@@ -168,6 +176,11 @@ kreg_status kreg_ctx_host_stats(const kreg_ctx* ctx, double out[8]);
  * sliced-ELL slots streamed, rounds, s preparing, s waiting}. */
 kreg_status kreg_ctx_stats(const kreg_ctx* ctx, double out[8]);
 kreg_status kreg_ctx_reset_stats(kreg_ctx* ctx);
+/* Host <-> device traffic since the last reset: {bytes uploaded (cloud
+ * positions FP64 + padded FP32 feature rows), bytes of results the kernels
+ * wrote into mapped host memory (per request F, gradient, displacement; per
+ * build its status block)}. Engine extension, no reference counterpart. */
+kreg_status kreg_ctx_io_stats(const kreg_ctx* ctx, int64_t out[2]);
 /* Candidate-list skin: a full build searches the grid at R_s = cutoff (1 +
  * skin) and later builds filter that list while max_j |T z_j - T_s z_j| <=
  * R_s - cutoff (exact: same FP64 predicate); 0 = always search the grid.
@@ -378,6 +391,15 @@ kreg_status kreg_register_sequence_chains(kreg_ctx* ctx, const kreg_cloud* const
                                           const kreg_kernel_params* params,
                                           const kreg_registration_config* config,
                                           kreg_sequence_result* result);
+/* End-to-end form of kreg_register_sequence_chains (n_chains = 1: exactly
+ * kreg_register_sequence): host frames in; they are staged and uploaded on
+ * worker threads, in order, while the first pairs already run. The CLI's
+ * `kreg sequence` path (main.cpp) after the frames are read. */
+kreg_status kreg_register_sequence_host(kreg_ctx* ctx, const kreg_cloud_view* frames,
+                                        int32_t n_frames, int32_t n_chains,
+                                        const kreg_kernel_params* params,
+                                        const kreg_registration_config* config,
+                                        kreg_sequence_result* result);
 /* Chains with explicit pair spans [begins[s], ends[s]) (pair p registers frames
  * p -> p + 1; spans ordered and disjoint): a rank of a multi-GPU sequence runs
  * its share of the global chain partition. Pairs outside the spans are

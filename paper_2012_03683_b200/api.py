@@ -62,6 +62,9 @@ def lib():
         L.kreg_ctx_host_stats.argtypes = [P, _abi.dptr]
         L.kreg_ctx_stats.argtypes = [P, _abi.dptr]
         L.kreg_ctx_reset_stats.argtypes = [P]
+        L.kreg_ctx_io_stats.argtypes = [P, _abi.i64ptr]
+        L.kreg_ctx_set_memory_budget.argtypes = [P, C.c_int64]
+        L.kreg_ctx_admission_stats.argtypes = [P, _abi.i64ptr]
         L.kreg_ctx_set_candidate_skin.argtypes = [P, D]
         L.kreg_ctx_set_chunk_units.argtypes = [P, C.c_int32]
         L.kreg_ctx_build_stats.argtypes = [P, _abi.i64ptr]
@@ -93,6 +96,8 @@ def lib():
         L.kreg_register_sequence.argtypes = [P, C.POINTER(P), C.c_int32, KP, CP, C.POINTER(_abi.kreg_sequence_result)]
         L.kreg_register_sequence_chains.argtypes = [P, C.POINTER(P), C.c_int32, C.c_int32, KP, CP,
                                                     C.POINTER(_abi.kreg_sequence_result)]
+        L.kreg_register_sequence_host.argtypes = [P, C.POINTER(_abi.kreg_cloud_view), C.c_int32, C.c_int32, KP, CP,
+                                                  C.POINTER(_abi.kreg_sequence_result)]
         L.kreg_register_sequence_spans.argtypes = [P, C.POINTER(P), C.c_int32, _abi.i32ptr, _abi.i32ptr, C.c_int32, KP,
                                                    CP, C.POINTER(_abi.kreg_sequence_result)]
         L.kreg_register_clouds_rows.argtypes = [P, P, P, C.c_int64, _abi.dptr, KP, CP, RP]
@@ -186,6 +191,20 @@ class Context:
         return {"rounds": int(out[0]), "t_prepare_s": float(out[1]), "t_wait_s": float(out[2]),
                 "t_build_prep_s": float(out[3]), "t_sweep_prep_s": float(out[4]), "t_solver_s": float(out[5]),
                 "device_allocs": int(out[6]), "device_alloc_s": float(out[7])}
+
+    def set_memory_budget(self, nbytes: int):
+        """Workspace bytes registrations may hold at once (0 = free device memory)."""
+        _check(lib().kreg_ctx_set_memory_budget(self.h, int(nbytes)))
+
+    def admission_stats(self):
+        out = np.zeros(2, dtype=np.int64)
+        _check(lib().kreg_ctx_admission_stats(self.h, _abi.as_ptr(out, C.c_int64)))
+        return {"peak_in_flight": int(out[0]), "deferred": int(out[1])}
+
+    def io_stats(self):
+        out = np.zeros(2, dtype=np.int64)
+        _check(lib().kreg_ctx_io_stats(self.h, _abi.as_ptr(out, C.c_int64)))
+        return {"h2d_bytes": int(out[0]), "d2h_bytes": int(out[1])}
 
     def sweep_stats(self):
         o = np.zeros(8)
@@ -466,6 +485,20 @@ def register_sequence(frames, params: KernelParams, config: RegistrationConfig, 
     else:
         _check(lib().kreg_register_sequence_chains(ctx.h, fh, n, int(chains), params.cstruct(), C.byref(cfg),
                                                    C.byref(sb.struct)))
+    return sb.result()
+
+
+def register_sequence_host(frames, params: KernelParams, config: RegistrationConfig, ctx=None,
+                           chains: int = 1) -> SequenceResult:
+    """End-to-end sequence call: host frames in, uploaded inside the call
+    while the first pairs run (chains = 1: register_sequence's semantics)."""
+    ctx = ctx or default_context()
+    n = len(frames)
+    fv = (_abi.kreg_cloud_view * max(n, 1))(*[f.view() for f in frames])
+    sb = SequenceBuffers(max(n, 1))
+    cfg = config.cstruct()
+    _check(lib().kreg_register_sequence_host(ctx.h, fv, n, int(chains), params.cstruct(), C.byref(cfg),
+                                             C.byref(sb.struct)))
     return sb.result()
 
 

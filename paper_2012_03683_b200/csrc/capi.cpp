@@ -4,6 +4,7 @@
 // KREG_NO_DEVICE / KREG_CUDA_ERROR.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -121,10 +122,17 @@ void fill_sequence(const std::vector<double>& rel, const std::vector<uint8_t>& f
 
 // Registers the chains [begin_c, end_c] of `frames` concurrently. Inside a
 // chain, pair k starts from the previous relative motion at the subsequent
-// lengthscale (registration.cpp:191-230); NoOverlapError => fallback.
+// lengthscale (registration.cpp:191-230); NoOverlapError => fallback. Every
+// pair of every chain is one job of one lockstep batch; a chain's next pair
+// joins the batch the moment its predecessor finishes (no barrier across
+// chains). A chain's first pair starts from identity at init_lengthscale, as
+// register_sequence's first pair does: chains are independent sequences
+// (SURVEY.md 8(d) C5), so a span that starts mid-sequence does not inherit the
+// motion of the pair before it (the single-chain call is exactly the
+// reference's register_sequence).
 void run_chains(kreg_ctx* ctx, const kreg_cloud* const* frames, int n_frames, const std::vector<int>& begins,
                 const std::vector<int>& ends, const Params& params, const kreg_registration_config& config,
-                kreg_sequence_result* out) {
+                kreg_sequence_result* out, const std::atomic<int>* frame_ready = nullptr) {
   const int m = n_frames - 1;
   std::vector<double> rel(static_cast<size_t>(m) * 12);
   for (int k = 0; k < m; ++k) kreg_se3::identity(rel.data() + 12 * k);  // pairs outside the spans
@@ -132,55 +140,65 @@ void run_chains(kreg_ctx* ctx, const kreg_cloud* const* frames, int n_frames, co
   std::vector<double> fi(static_cast<size_t>(m));
   std::vector<int> it(static_cast<size_t>(m));
   const int nc = static_cast<int>(begins.size());
-  std::vector<int> cursor(begins);           // frame index k-1 of the next pair
-  std::vector<std::vector<double>> prev(static_cast<size_t>(nc), std::vector<double>(12));
-  for (auto& p : prev) kreg_se3::identity(p.data());
-  std::vector<kreg_registration_result> results(static_cast<size_t>(nc));
-  std::vector<long long> hint(static_cast<size_t>(nc), 0);
-  for (;;) {
-    std::vector<RegJob> jobs;
-    std::vector<int> chain_of;
+  // jobs ordered chain head first (all heads start at once), then by position
+  std::vector<int> pair_of;
+  std::vector<RegJob> jobs;
+  for (int pos = 0;; ++pos) {
+    bool any = false;
     for (int c = 0; c < nc; ++c) {
-      if (cursor[c] >= ends[c]) continue;
-      const int k = cursor[c] + 1;  // pair (k-1, k)
+      const int k = begins[c] + pos + 1;  // pair (k-1, k)
+      if (k > ends[c]) continue;
+      any = true;
       RegJob j;
       j.X = frames[k - 1];
       j.Z = frames[k];
-      std::memcpy(j.initial, prev[c].data(), sizeof(j.initial));
+      if (frame_ready) {  // end-to-end: the pair starts once both frames are on the device
+        j.ready = &frame_ready[k - 1];
+        j.ready2 = &frame_ready[k];
+      }
+      kreg_se3::identity(j.initial);
       j.params = params;
       j.cfg = config;
-      if (k - begins[c] > 1) j.cfg.init_lengthscale = config.subsequent_lengthscale;
+      if (pos > 0) j.cfg.init_lengthscale = config.subsequent_lengthscale;
       j.cfg.min_lengthscale = std::min(j.cfg.min_lengthscale, j.cfg.init_lengthscale);
-      std::memset(&results[c], 0, sizeof(kreg_registration_result));
-      j.out = &results[c];
-      j.expected_pairs = hint[c];
       jobs.push_back(j);
-      chain_of.push_back(c);
+      pair_of.push_back(k - 1);
     }
-    if (jobs.empty()) break;
-    register_many(ctx, jobs);
-    for (size_t q = 0; q < jobs.size(); ++q) {
-      const int c = chain_of[q];
-      const int k = cursor[c] + 1;
-      const int slot = k - 1;
-      const RegJob& j = jobs[q];
-      if (j.status == KREG_OK) {
-        std::memcpy(rel.data() + 12 * slot, results[c].transform, sizeof(double) * 12);
-        fb[slot] = 0;
-        cv[slot] = results[c].converged ? 1 : 0;
-        fi[slot] = results[c].final_indicator;
-        it[slot] = results[c].iterations;
-      } else if (j.status == KREG_NO_OVERLAP) {
-        std::memcpy(rel.data() + 12 * slot, prev[c].data(), sizeof(double) * 12);
-        fb[slot] = 1;
-        cv[slot] = 0;
-        fi[slot] = 0.0;
-        it[slot] = 0;
-      } else {
-        throw Error(j.status, j.error);
-      }
-      std::memcpy(prev[c].data(), rel.data() + 12 * slot, sizeof(double) * 12);
-      cursor[c] = k;
+    if (!any) break;
+  }
+  std::vector<int> job_of_pair(static_cast<size_t>(m), -1);
+  for (size_t q = 0; q < jobs.size(); ++q) job_of_pair[static_cast<size_t>(pair_of[q])] = static_cast<int>(q);
+  for (size_t q = 0; q < jobs.size(); ++q) {
+    const int p = pair_of[q];
+    const bool head = std::find(begins.begin(), begins.end(), p) != begins.end();
+    if (!head && p > 0 && job_of_pair[static_cast<size_t>(p - 1)] >= 0) {
+      jobs[q].pred = job_of_pair[static_cast<size_t>(p - 1)];
+      jobs[static_cast<size_t>(jobs[q].pred)].succ = static_cast<int>(q);
+    }
+  }
+  std::vector<kreg_registration_result> results(jobs.size());
+  for (size_t q = 0; q < jobs.size(); ++q) {
+    std::memset(&results[q], 0, sizeof(kreg_registration_result));
+    jobs[q].out = &results[q];
+  }
+  register_many(ctx, jobs);
+  for (size_t q = 0; q < jobs.size(); ++q) {
+    const int slot = pair_of[q];
+    const RegJob& j = jobs[q];
+    if (j.status == KREG_OK) {
+      std::memcpy(rel.data() + 12 * slot, results[q].transform, sizeof(double) * 12);
+      fb[slot] = 0;
+      cv[slot] = results[q].converged ? 1 : 0;
+      fi[slot] = results[q].final_indicator;
+      it[slot] = results[q].iterations;
+    } else if (j.status == KREG_NO_OVERLAP) {
+      std::memcpy(rel.data() + 12 * slot, j.initial, sizeof(double) * 12);  // the previous relative motion
+      fb[slot] = 1;
+      cv[slot] = 0;
+      fi[slot] = 0.0;
+      it[slot] = 0;
+    } else {
+      throw Error(j.status, j.error);
     }
   }
   fill_sequence(rel, fb, cv, fi, it, out);
@@ -305,10 +323,33 @@ kreg_status kreg_ctx_stats(const kreg_ctx* ctx, double out[8]) {
   });
 }
 
+kreg_status kreg_ctx_io_stats(const kreg_ctx* ctx, int64_t out[2]) {
+  return guarded([&] {
+    require(ctx != nullptr && out != nullptr, "NULL argument");
+    out[0] = ctx->h2d_bytes.load();
+    out[1] = ctx->d2h_bytes.load();
+  });
+}
+
 kreg_status kreg_ctx_set_max_active(kreg_ctx* ctx, int32_t n) {
   return guarded([&] {
     require(ctx != nullptr && n >= 0, "invalid argument");
     ctx->max_active = n;
+  });
+}
+
+kreg_status kreg_ctx_set_memory_budget(kreg_ctx* ctx, int64_t bytes) {
+  return guarded([&] {
+    require(ctx != nullptr && bytes >= 0, "invalid argument");
+    ctx->mem_budget = bytes;
+  });
+}
+
+kreg_status kreg_ctx_admission_stats(const kreg_ctx* ctx, int64_t out[2]) {
+  return guarded([&] {
+    require(ctx != nullptr && out != nullptr, "NULL argument");
+    out[0] = ctx->peak_in_flight;
+    out[1] = ctx->deferred_admissions;
   });
 }
 
@@ -327,6 +368,10 @@ kreg_status kreg_ctx_reset_stats(kreg_ctx* ctx) {
     ctx->t_prepare = ctx->t_wait = ctx->t_total = 0.0;
     ctx->t_build_prep = ctx->t_sweep_prep = 0.0;
     ctx->t_stage = ctx->t_upload_issue = 0.0;
+    ctx->h2d_bytes = 0;
+    ctx->d2h_bytes = 0;
+    ctx->peak_in_flight = 0;
+    ctx->deferred_admissions = 0;
     ctx->launches_base = kreg_dev::kernel_launch_count();
     ctx->full_builds = ctx->filter_builds = 0;
     ctx->build_ms = 0.0;
@@ -681,6 +726,36 @@ kreg_status kreg_register_sequence_chains(kreg_ctx* ctx, const kreg_cloud* const
       e.push_back(static_cast<int>(static_cast<long long>(m) * (c + 1) / nc));
     }
     run_chains(ctx, frames, n_frames, b, e, to_params(params), *config, result);
+  });
+}
+
+kreg_status kreg_register_sequence_host(kreg_ctx* ctx, const kreg_cloud_view* frames, int32_t n_frames,
+                                        int32_t n_chains, const kreg_kernel_params* params,
+                                        const kreg_registration_config* config, kreg_sequence_result* result) {
+  return guarded([&] {
+    if (n_frames < 2) throw Error(KREG_INVALID_ARGUMENT, "register_sequence: need at least 2 frames");
+    require(ctx && frames && params && config && result && n_chains >= 1, "invalid argument");
+    std::vector<const kreg_cloud_view*> views;
+    for (int k = 0; k < n_frames; ++k) views.push_back(&frames[k]);
+    // frames are staged and uploaded on worker threads in order while the
+    // first pairs already run
+    std::unique_ptr<AsyncUpload> up = cloud_upload_async(ctx, views.data(), n_frames, 1);
+    std::vector<const kreg_cloud*> fr;
+    for (auto& c : up->clouds) fr.push_back(c.get());
+    const int m = n_frames - 1;
+    const int nc = std::min(n_chains, m);
+    std::vector<int> b, e;
+    for (int c = 0; c < nc; ++c) {
+      b.push_back(static_cast<int>(static_cast<long long>(m) * c / nc));
+      e.push_back(static_cast<int>(static_cast<long long>(m) * (c + 1) / nc));
+    }
+    try {
+      run_chains(ctx, fr.data(), n_frames, b, e, to_params(params), *config, result, up->ready.data());
+    } catch (...) {
+      up.reset();  // join the workers before the clouds go away
+      throw;
+    }
+    up.reset();
   });
 }
 

@@ -268,6 +268,7 @@ void cloud_upload(kreg_ctx* ctx, kreg_cloud* c, const double* sx, const double* 
     c->xw.ensure(static_cast<size_t>(n) + 1, false, 1.0);
   }
   if (n) {
+    ctx->h2d_bytes += static_cast<long long>(sizeof(double) * 3 * n + sizeof(float) * static_cast<size_t>(n) * c->fstride);
     KREG_CUDA(cudaMemcpyAsync(c->x.ptr, sx, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
     KREG_CUDA(cudaMemcpyAsync(c->y.ptr, sy, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
     KREG_CUDA(cudaMemcpyAsync(c->z.ptr, sz, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
@@ -356,9 +357,10 @@ AsyncUpload::~AsyncUpload() {
     if (t.joinable()) t.join();
 }
 
-std::unique_ptr<AsyncUpload> cloud_upload_async(kreg_ctx* ctx, const kreg_cloud_view* const* views, int n_jobs) {
+std::unique_ptr<AsyncUpload> cloud_upload_async(kreg_ctx* ctx, const kreg_cloud_view* const* views, int n_jobs,
+                                                int per_unit) {
   auto up = std::make_unique<AsyncUpload>();
-  const int n = 2 * n_jobs;
+  const int n = per_unit * n_jobs;
   up->clouds.resize(static_cast<size_t>(n));
   for (int k = 0; k < n; ++k) up->clouds[k].reset(cloud_describe(ctx, views[k]));
   std::vector<size_t> doff(static_cast<size_t>(n) + 1, 0), foff(static_cast<size_t>(n) + 1, 0),
@@ -385,14 +387,14 @@ std::unique_ptr<AsyncUpload> cloud_upload_async(kreg_ctx* ctx, const kreg_cloud_
   auto next = std::make_shared<std::atomic<int>>(0);
   AsyncUpload* U = up.get();
   const int device = ctx->device;
-  auto work = [U, ctx, views, doff, foff, woff, next, n_jobs, device]() {
+  auto work = [U, ctx, views, doff, foff, woff, next, n_jobs, per_unit, device]() {
     cudaSetDevice(device);
     for (;;) {
       const int job = next->fetch_add(1);
       if (job >= n_jobs) return;
       try {
-        for (int h = 0; h < 2; ++h) {
-          const int k = 2 * job + h;
+        for (int h = 0; h < per_unit; ++h) {
+          const int k = per_unit * job + h;
           kreg_cloud* c = U->clouds[k].get();
           const int m = c->n;
           double* d = ctx->stage_d.ptr + doff[k];
@@ -829,6 +831,7 @@ void end_round(kreg_ctx* ctx, RoundSlot& S) {
         ok = false;
       } else {
         p->sup_valid = true;
+        ctx->hw_radius = std::max(ctx->hw_radius, p->sup_radius);
         p->sup_disp = 0.0;  // built at T: a re-run may filter it
         job.disp_hint = 0.0;
         p->expected_sup = std::max(p->expected_sup, p->sup_entries);
@@ -882,6 +885,9 @@ void end_round(kreg_ctx* ctx, RoundSlot& S) {
     }
   }
   long long round_pairs = 0, round_slots = 0;
+  long long d2h = static_cast<long long>(sizeof(double)) * kreg_dev::kBuildStatus * nb;  // build statuses
+  for (int e = 0; e < ne; ++e) d2h += static_cast<long long>(sizeof(double)) * kreg_dev::kOut * evals[e].M;
+  ctx->d2h_bytes += d2h;
   for (int e = 0; e < ne; ++e) {
     std::memcpy(evals[e].out, res + static_cast<size_t>(e) * kreg_dev::kMaxCandidates * kreg_dev::kOut,
                 sizeof(double) * kreg_dev::kOut * evals[e].M);

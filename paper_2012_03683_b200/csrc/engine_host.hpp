@@ -172,6 +172,12 @@ struct kreg_ctx {
   // capacity high-water marks over all workspaces: a pooled workspace that
   // must grow goes straight to the largest size any registration needed
   long long hw_slots = 0, hw_sup = 0;
+  // largest candidate radius R_s a grid build has completed at: a new
+  // registration at R_s <= hw_radius needs about workspace_estimate() bytes
+  // (kreg_register_batch admits registrations against free device memory)
+  double hw_radius = 0.0;
+  long long mem_budget = 0;  // workspace bytes (kreg_ctx_set_memory_budget; 0 = free device memory)
+  long long peak_in_flight = 0, deferred_admissions = 0;
   int chunk_pref = kreg_dev::kPrefChunkUnits;  // sweep chunk size of new lists (kreg_ctx_set_chunk_units)
   long long full_builds = 0, filter_builds = 0;
   // build-stage profile (profiling on): device ms of the build launches,
@@ -190,6 +196,9 @@ struct kreg_ctx {
   double t_prepare = 0.0, t_wait = 0.0, t_total = 0.0;
   double t_build_prep = 0.0, t_sweep_prep = 0.0;
   double t_stage = 0.0, t_upload_issue = 0.0;  // end-to-end calls: host staging, copy issue
+  // host <-> device traffic: cloud uploads, results the kernels write into
+  // mapped pinned memory (rounds) and explicit copies back
+  std::atomic<long long> h2d_bytes{0}, d2h_bytes{0};
   ~kreg_ctx();
 };
 
@@ -296,7 +305,10 @@ struct AsyncUpload {
   std::exception_ptr error;
   ~AsyncUpload();
 };
-std::unique_ptr<AsyncUpload> cloud_upload_async(kreg_ctx* ctx, const kreg_cloud_view* const* views, int n_jobs);
+// `per_unit` consecutive clouds form one unit with one ready flag (2: a
+// batch job's X and Z; 1: a sequence frame)
+std::unique_ptr<AsyncUpload> cloud_upload_async(kreg_ctx* ctx, const kreg_cloud_view* const* views, int n_units,
+                                                int per_unit = 2);
 
 // Many clouds: host staging on worker threads, device copies into a context
 // arena (valid until the next call of this function on the context).
@@ -373,6 +385,10 @@ void pairs_export(kreg_ctx* ctx, const kreg_pairs* p, int64_t* offsets, int32_t*
 
 // Workspace pool (ctx may be null: plain new/delete).
 kreg_pairs* acquire_workspace(kreg_ctx* ctx);
+// device bytes a workspace holds; bytes a workspace grown to the context's
+// high-water capacities holds
+long long workspace_bytes(const kreg_pairs* p);
+long long workspace_estimate(const kreg_ctx* ctx);
 void release_workspace(kreg_ctx* ctx, kreg_pairs* p);
 
 }  // namespace kreg_host

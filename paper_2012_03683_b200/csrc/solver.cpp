@@ -24,6 +24,8 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <deque>
+#include <functional>
 #include <memory>
 #include <thread>
 #include <vector>
@@ -73,6 +75,29 @@ void release_workspace(kreg_ctx* ctx, kreg_pairs* p) {
   } else {
     delete p;
   }
+}
+
+namespace {
+template <class T>
+long long held(const DevBuf<T>& b) {
+  return b.ptr && b.owned ? static_cast<long long>(b.cap * sizeof(T)) : 0;
+}
+}  // namespace
+
+long long workspace_bytes(const kreg_pairs* p) {
+  return held(p->sup) + held(p->sup_i) + held(p->sup_count) + held(p->sup_off) + held(p->count) + held(p->perm) +
+         held(p->pos) + held(p->deg_s) + held(p->tile_off) + held(p->slot_buf) + held(p->slot_i) +
+         held(p->unit_off) + held(p->zs) + held(p->chunks) + held(p->disp_blk) + held(p->alt_perm) +
+         held(p->alt_pos) + held(p->alt_deg_s) + held(p->alt_unit_off) + held(p->alt_tile_off) +
+         held(p->alt_slot_buf) + held(p->alt_zs) + held(p->alt_chunks);
+}
+
+long long workspace_estimate(const kreg_ctx* ctx) {
+  // candidate entries + indices, sweep slots + indices (+ the refilter's
+  // second slot buffer), plus the per-source arrays
+  const long long slot_bytes = static_cast<long long>(sizeof(int4) + sizeof(int)) * ctx->hw_slots;
+  return static_cast<long long>(sizeof(int4) + sizeof(int)) * ctx->hw_sup + slot_bytes +
+         (ctx->refilter ? slot_bytes : 0) + (16LL << 20);
 }
 
 namespace {
@@ -486,6 +511,7 @@ void register_many(kreg_ctx* ctx, std::vector<RegJob>& jobs, const Collective* c
   const int k_first = std::max(1, std::min(8, env_int("KREG_K_FIRST", 2)));
   const bool fail_grad = env_int("KREG_FAIL_GRAD", 0) != 0;
   std::vector<std::unique_ptr<Reg>> regs;
+  std::vector<Reg*> job_reg(jobs.size(), nullptr);
   for (RegJob& j : jobs) {
     j.status = KREG_OK;
     auto r = std::make_unique<Reg>();
@@ -527,7 +553,30 @@ void register_many(kreg_ctx* ctx, std::vector<RegJob>& jobs, const Collective* c
       j.error = msg;
       continue;
     }
+    job_reg[static_cast<size_t>(&j - jobs.data())] = r.get();
     regs.push_back(std::move(r));
+  }
+  // Ready queue: jobs without a predecessor in order; a chained job joins
+  // when its predecessor finishes (resolve), with the initial guess
+  // register_sequence gives it (registration.cpp:211-219).
+  std::deque<Reg*> ready;
+  std::function<void(int)> resolve = [&](int i) {
+    const int s = jobs[static_cast<size_t>(i)].succ;
+    if (s < 0) return;
+    RegJob& J = jobs[static_cast<size_t>(i)];
+    RegJob& S = jobs[static_cast<size_t>(s)];
+    std::memcpy(S.initial, J.status == KREG_OK ? J.out->transform : J.initial, sizeof(S.initial));
+    if (Reg* rs = job_reg[static_cast<size_t>(s)]) {
+      std::memcpy(rs->T, S.initial, sizeof(rs->T));
+      ready.push_back(rs);
+    } else {
+      resolve(s);  // failed before it could start (empty cloud): falls back at once
+    }
+  };
+  for (size_t i = 0; i < jobs.size(); ++i) {
+    if (jobs[i].pred >= 0) continue;
+    if (job_reg[i]) ready.push_back(job_reg[i]);
+    else resolve(static_cast<int>(i));
   }
 
   using clk = std::chrono::steady_clock;
@@ -550,6 +599,42 @@ void register_many(kreg_ctx* ctx, std::vector<RegJob>& jobs, const Collective* c
   Group groups[2];
   for (int g = 0; g < n_groups; ++g) groups[g].slot = round_slot(ctx, g);
   const size_t per_group = (window + n_groups - 1) / n_groups;
+
+  // Memory-aware admission: a registration starts only when the device has
+  // room for its workspace at the context's high-water capacities (every
+  // workspace grows to those). A registration whose first candidate radius
+  // exceeds any radius built so far (the first call on a context, or the
+  // first-frame schedule after subsequent pairs) starts alone and the rest
+  // wait one round for its build to size the estimate. One registration is
+  // always admitted when nothing is in flight.
+  auto in_flight = [&] {
+    size_t n = 0;
+    for (int g = 0; g < n_groups; ++g) n += groups[g].active.size();
+    return n;
+  };
+  // workspace bytes admitted in this refill pass but not allocated yet (the
+  // builds that grow them run after the pass)
+  long long admit_pending = 0;
+  auto admit = [&](const Reg* r) -> bool {
+    if (!ctx || in_flight() == 0) return true;
+    const double rs = r->cfg.cutoff_multiplier * r->cfg.init_lengthscale * (1.0 + std::max(0.0, ctx->skin));
+    if (rs > ctx->hw_radius * (1.0 + 1e-9)) return false;
+    if (ctx->mem_budget > 0)
+      return static_cast<long long>(in_flight() + 1) * workspace_estimate(ctx) <= ctx->mem_budget;
+    long long need = workspace_estimate(ctx);
+    if (!ctx->pool.empty()) need -= workspace_bytes(ctx->pool.back());
+    if (need <= 0) return true;
+    need += need / 4;
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+      cudaGetLastError();
+      return true;
+    }
+    const long long reserve = std::max<long long>(1LL << 30, static_cast<long long>(total_b / 50));
+    if (static_cast<long long>(free_b) < admit_pending + need + reserve) return false;
+    admit_pending += need;
+    return true;
+  };
 
   // host phase trace (KREG_TRACE_HOST=1): per-round microseconds of
   // end_round after the wait, consume, refill + plan, begin_round
@@ -578,25 +663,40 @@ void register_many(kreg_ctx* ctx, std::vector<RegJob>& jobs, const Collective* c
     }
     const auto t2 = clk::now();
     for (;;) {
+      for (Reg* r : G.active)  // finished chain links release their successors
+        if (r->phase == Phase::kDone) resolve(static_cast<int>(r->job - jobs.data()));
       G.active.erase(std::remove_if(G.active.begin(), G.active.end(), [](Reg* r) { return r->phase == Phase::kDone; }),
                      G.active.end());
-      while (G.active.size() < per_group && started < regs.size()) {
+      admit_pending = 0;
+      while (G.active.size() < per_group && !ready.empty()) {
         // end-to-end batches: start a job once its clouds' copies are enqueued
-        const std::atomic<int>* rd = regs[started]->job->ready;
-        if (rd) {
-          int v = rd->load(std::memory_order_acquire);
-          while (v == 0 && G.active.empty()) {  // nothing else to run: wait for the upload
+        const RegJob* fj = ready.front()->job;
+        if (fj->ready || fj->ready2) {
+          auto state = [fj] {
+            const int a = fj->ready ? fj->ready->load(std::memory_order_acquire) : 1;
+            const int b = fj->ready2 ? fj->ready2->load(std::memory_order_acquire) : 1;
+            return a < 0 || b < 0 ? -1 : std::min(a, b);
+          };
+          int v = state();
+          while (v == 0 && in_flight() == 0) {  // nothing else to run: wait for the upload
             std::this_thread::yield();
-            v = rd->load(std::memory_order_acquire);
+            v = state();
           }
           if (v < 0) throw Error(KREG_CUDA_ERROR, "cloud upload failed");
           if (v == 0) break;
         }
-        Reg* r = regs[started++].get();
+        if (!admit(ready.front())) {
+          if (ctx) ++ctx->deferred_admissions;
+          break;
+        }
+        Reg* r = ready.front();
+        ready.pop_front();
+        ++started;
         r->pairs.ctx = ctx;
         r->pairs.p = acquire_workspace(ctx);
         if (r->job->expected_pairs > 0) r->pairs->expected_pairs = r->job->expected_pairs;
         G.active.push_back(r);
+        if (ctx) ctx->peak_in_flight = std::max<long long>(ctx->peak_in_flight, static_cast<long long>(in_flight()));
       }
       std::vector<BuildJob> builds;
       std::vector<EvalJob> evals;
@@ -615,7 +715,8 @@ void register_many(kreg_ctx* ctx, std::vector<RegJob>& jobs, const Collective* c
         (void)t0;
         return true;
       }
-      if (started >= regs.size()) return false;  // group drained
+      if (ready.empty() && G.active.empty()) return false;  // group drained
+      if (G.active.empty()) return true;  // waiting for memory: the other group runs
       // every active registration finished without device work: refill
     }
   };

@@ -18,6 +18,12 @@ struct RegJob {
   long long expected_pairs = 0;   // optional capacity hint
   long long n_z_total = 0;        // row sharding: size of the whole source (0: Z->n)
   const std::atomic<int>* ready = nullptr;  // end-to-end: clouds enqueued (1), failed (-1); null = ready
+  const std::atomic<int>* ready2 = nullptr; // a second flag (sequences: X and Z are separate frames)
+  // sequence chains (register_sequence, registration.cpp:191-230): the job
+  // starts when job `pred` has finished, from pred's relative motion (pred's
+  // own initial guess when pred fell back on NoOverlapError); -1 = no link
+  int pred = -1;
+  int succ = -1;
   kreg_status status = KREG_OK;
   std::string error;
 };

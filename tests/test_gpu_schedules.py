@@ -20,6 +20,7 @@
 Tolerances are BASELINE.json:north_star's (1e-4 relative on F / grad,
 1e-3 rad / 1e-3 m on poses).
 """
+import dataclasses
 import math
 import os
 import socket
@@ -288,3 +289,60 @@ def test_row_sharded_two_ranks_on_device(ctx):
         assert np.allclose(g["obj"], want.objective_trace, rtol=1e-6, atol=0)
         ok, err = _pose_close(Isometry.from12(g["T"]), want.transform, 1e-5, 1e-5)
         assert ok, err
+
+
+def _same(a, b):
+    assert a.iterations == b.iterations
+    assert np.array_equal(a.transform.as12(), b.transform.as12())
+    assert np.array_equal(a.objective_trace, b.objective_trace)
+    assert np.array_equal(a.step_trace, b.step_trace)
+
+
+def test_memory_admission_same_results():
+    """Memory-aware admission (solver.cpp register_many): a fresh context
+    starts one registration, sizes the workspace estimate from its first
+    build, then admits the rest; a first-frame batch after subsequent ones
+    probes again (larger radius); a 1-byte budget runs the batch one
+    registration at a time. Every schedule gives bit-identical results."""
+    p = synth.kitti_params()
+    Xs, Zs, inits = [], [], []
+    for k in range(6):
+        X, Z, T = synth.kitti_pair(900 + k, 8000, start=float(k) * 9.0)
+        Xs.append(X)
+        Zs.append(Z)
+        inits.append(synth.perturbed(T, 900 + k))
+    sub = synth.kitti_subsequent_config()
+    first = dataclasses.replace(synth.kitti_first_config(), max_iterations=60)
+
+    a = api.Context(0)
+    ra, sa = api.register_batch(Xs, Zs, inits, p, sub, ctx=a)
+    st = a.admission_stats()
+    assert (sa == 0).all() and st["peak_in_flight"] == 6 and st["deferred"] >= 1, st
+    a.reset_stats()
+    fa, _ = api.register_batch(Xs[:3], Zs[:3], inits[:3], p, first, ctx=a)
+    st = a.admission_stats()
+    assert st["peak_in_flight"] == 3 and st["deferred"] >= 1, st
+
+    b = api.Context(0)
+    b.set_memory_budget(1)
+    rb, sb = api.register_batch(Xs, Zs, inits, p, sub, ctx=b)
+    st = b.admission_stats()
+    assert (sb == 0).all() and st["peak_in_flight"] == 1 and st["deferred"] >= 5, st
+    fb, _ = api.register_batch(Xs[:3], Zs[:3], inits[:3], p, first, ctx=b)
+    for x, y in zip(ra + fa, rb + fb):
+        _same(x, y)
+
+
+def test_sequence_host_matches_device_frames(ctx):
+    """kreg_register_sequence_host (frames uploaded inside the call, pairs
+    start as their two frames land) gives bit-identical results to the
+    device-frame entry points, for one chain and for several."""
+    frames, _ = synth.kitti_sequence(31, 7, 8000)
+    p, cfg = synth.kitti_params(), dataclasses.replace(synth.kitti_subsequent_config(), max_iterations=150)
+    for chains in (1, 3):
+        a = api.register_sequence(frames, p, cfg, ctx=ctx, chains=None if chains == 1 else chains)
+        b = api.register_sequence_host(frames, p, cfg, ctx=ctx, chains=chains)
+        assert np.array_equal(a.iterations, b.iterations)
+        assert np.array_equal(a.fallback, b.fallback)
+        for x, y in zip(a.relative, b.relative):
+            assert np.array_equal(x.as12(), y.as12())
