@@ -615,6 +615,7 @@ void register_many(kreg_ctx* ctx, std::vector<RegJob>& jobs, const Collective* c
   // workspace bytes admitted in this refill pass but not allocated yet (the
   // builds that grow them run after the pass)
   long long admit_pending = 0;
+  long long mem_free = -1;  // free device bytes minus a reserve, queried once per refill pass
   auto admit = [&](const Reg* r) -> bool {
     if (!ctx || in_flight() == 0) return true;
     const double rs = r->cfg.cutoff_multiplier * r->cfg.init_lengthscale * (1.0 + std::max(0.0, ctx->skin));
@@ -625,13 +626,15 @@ void register_many(kreg_ctx* ctx, std::vector<RegJob>& jobs, const Collective* c
     if (!ctx->pool.empty()) need -= workspace_bytes(ctx->pool.back());
     if (need <= 0) return true;
     need += need / 4;
-    size_t free_b = 0, total_b = 0;
-    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
-      cudaGetLastError();
-      return true;
+    if (mem_free < 0) {  // one query per refill pass (cudaMemGetInfo costs up to ~1 ms)
+      size_t free_b = 0, total_b = 0;
+      if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+        cudaGetLastError();
+        return true;
+      }
+      mem_free = static_cast<long long>(free_b) - std::max<long long>(1LL << 30, static_cast<long long>(total_b / 50));
     }
-    const long long reserve = std::max<long long>(1LL << 30, static_cast<long long>(total_b / 50));
-    if (static_cast<long long>(free_b) < admit_pending + need + reserve) return false;
+    if (mem_free < admit_pending + need) return false;
     admit_pending += need;
     return true;
   };
@@ -668,6 +671,7 @@ void register_many(kreg_ctx* ctx, std::vector<RegJob>& jobs, const Collective* c
       G.active.erase(std::remove_if(G.active.begin(), G.active.end(), [](Reg* r) { return r->phase == Phase::kDone; }),
                      G.active.end());
       admit_pending = 0;
+      mem_free = -1;
       while (G.active.size() < per_group && !ready.empty()) {
         // end-to-end batches: start a job once its clouds' copies are enqueued
         const RegJob* fj = ready.front()->job;
