@@ -41,7 +41,8 @@ typedef enum {
   KREG_CUDA_ERROR = 3,       /* device fault / launch failure                  */
   KREG_OUT_OF_MEMORY = 4,    /* device allocation failed                       */
   KREG_RUNTIME_ERROR = 5,    /* std::runtime_error                             */
-  KREG_NO_DEVICE = 6         /* no CUDA device: there is no CPU fallback       */
+  KREG_NO_DEVICE = 6,        /* no CUDA device: there is no CPU fallback       */
+  KREG_PARSE_ERROR = 7       /* kreg::ParseError (errors.hpp:9-22)             */
 } kreg_status;
 
 /* reference point_cloud.hpp:13 ChannelKind */
@@ -219,6 +220,24 @@ kreg_status kreg_ctx_set_collective(kreg_ctx* ctx, kreg_collective_fn fn, void* 
 kreg_status kreg_cloud_create(kreg_ctx* ctx, const kreg_cloud_view* view, kreg_cloud** out);
 kreg_status kreg_cloud_destroy(kreg_cloud* cloud);
 int32_t kreg_cloud_size(const kreg_cloud* cloud);
+
+/* PLY file straight into a device cloud (replaces read_ply / read_cloud for
+ * .ply, cloud_io.cpp:141-297 and cloud_io.hpp:18-26: ascii or
+ * binary_little_endian; schema from the properties present; 8/16-bit colour
+ * and intensity / 255 / 65535; ParseError -> KREG_PARSE_ERROR with the
+ * reference's "path:line: message"). The vertex block is read once into
+ * pinned memory, decoded, Morton-ordered and laid out on the device; the cloud
+ * is bitwise the one kreg_cloud_create makes from read_ply's PointCloud.
+ * `warnings` (may be NULL) receives "property 'name' skipped" lines. */
+kreg_status kreg_cloud_read_ply(kreg_ctx* ctx, const char* path, kreg_cloud** out, char* warnings,
+                                int32_t warnings_cap);
+/* Schema of a device cloud: feature dim and per-channel dims / kinds
+ * (arrays of `cap` entries; *n_channels is the full count). */
+kreg_status kreg_cloud_schema(const kreg_cloud* cloud, int32_t* dim, int32_t* n_channels, int32_t* dims,
+                              int32_t* kinds, int32_t cap);
+/* Positions (n x 3 FP64, exact) and features (n x dim, the device's FP32
+ * values) back in the original point order; either pointer may be NULL. */
+kreg_status kreg_cloud_download(const kreg_cloud* cloud, double* xyz, double* features);
 
 /* --------------------------------------------------- pair engine (L3) */
 /* reference inner_product.hpp:50-51 / inner_product.cpp:37-95 build_pairs. */

@@ -16,6 +16,7 @@
 #include <string>
 #include <vector>
 
+#include "kreg/cloud_io.hpp"
 #include "kreg/errors.hpp"
 #include "kreg/eval.hpp"
 #include "kreg/image.hpp"
@@ -44,6 +45,8 @@ int guarded(Fn&& fn) {
     return 0;
   } catch (const NoOverlapError& e) {
     return fail(KREG_NO_OVERLAP, e.what());
+  } catch (const ParseError& e) {
+    return fail(KREG_PARSE_ERROR, e.what());
   } catch (const std::invalid_argument& e) {
     return fail(KREG_INVALID_ARGUMENT, e.what());
   } catch (const std::exception& e) {
@@ -325,6 +328,45 @@ void kref_se3_compose(const double a[12], const double b[12], double out[12]) {
 }
 
 double kref_diameter(const kreg_cloud_view* v) { return diameter(to_cloud(v)); }
+
+// Cloud file I/O (cloud_io.cpp:141-297 read_ply, 456-529 write_ply).
+int kref_write_ply(const kreg_cloud_view* v, const char* path, int binary) {
+  return guarded([&] { write_ply(to_cloud(v), path, binary != 0); });
+}
+// read_ply into a heap PointCloud; *warnings gets the skipped-property lines
+int kref_read_ply(const char* path, void** out, int* n, int* dim, int* n_channels, char* warnings, int cap) {
+  return guarded([&] {
+    std::vector<std::string> w;
+    auto* c = new PointCloud(read_cloud(path, &w));
+    *out = c;
+    *n = c->size();
+    *dim = c->schema().total_dim();
+    *n_channels = c->schema().channel_count();
+    std::string all;
+    for (const auto& s : w) all += s + "\n";
+    if (warnings && cap > 0) {
+      const size_t k = std::min(all.size(), static_cast<size_t>(cap - 1));
+      std::memcpy(warnings, all.data(), k);
+      warnings[k] = '\0';
+    }
+  });
+}
+void kref_cloud_copy(const void* h, double* xyz, double* features, int* dims, int* kinds) {
+  const auto* c = static_cast<const PointCloud*>(h);
+  for (int i = 0; i < c->size(); ++i) {
+    const Eigen::Vector3d& p = c->position(i);
+    xyz[3 * i] = p.x();
+    xyz[3 * i + 1] = p.y();
+    xyz[3 * i + 2] = p.z();
+    const auto row = c->feature_row(i);
+    for (int d = 0; d < c->schema().total_dim(); ++d) features[static_cast<size_t>(i) * c->schema().total_dim() + d] = row[static_cast<size_t>(d)];
+  }
+  for (int k = 0; k < c->schema().channel_count(); ++k) {
+    dims[k] = c->schema().channel(k).dim;
+    kinds[k] = static_cast<int>(c->schema().channel(k).kind);
+  }
+}
+void kref_cloud_destroy(void* h) { delete static_cast<PointCloud*>(h); }
 
 // Generators (reference eval.cpp:248-300), for fixtures.
 int kref_make_box_cloud(uint64_t seed, int n, int with_color, double* xyz, double* features) {

@@ -16,6 +16,7 @@ KREG_CUDA_ERROR = 3
 KREG_OUT_OF_MEMORY = 4
 KREG_RUNTIME_ERROR = 5
 KREG_NO_DEVICE = 6
+KREG_PARSE_ERROR = 7
 
 KREG_EVAL_GRAD = 1
 KREG_EVAL_DISP = 2

@@ -73,6 +73,9 @@ def lib():
         L.kreg_cloud_create.argtypes = [P, VP, C.POINTER(P)]
         L.kreg_cloud_destroy.argtypes = [P]
         L.kreg_cloud_size.argtypes = [P]
+        L.kreg_cloud_read_ply.argtypes = [P, C.c_char_p, C.POINTER(P), C.c_char_p, C.c_int32]
+        L.kreg_cloud_schema.argtypes = [P, _abi.i32ptr, _abi.i32ptr, _abi.i32ptr, _abi.i32ptr, C.c_int32]
+        L.kreg_cloud_download.argtypes = [P, _abi.dptr, _abi.dptr]
         L.kreg_build_pairs.argtypes = [P, P, P, _abi.dptr, KP, D, D, C.POINTER(P), _abi.i64ptr]
         L.kreg_pairs_destroy.argtypes = [P]
         L.kreg_pairs_size.argtypes = [P]
@@ -226,12 +229,13 @@ def default_context() -> Context:
 class DeviceCloud:
     """Device-resident SoA copy of a PointCloud (kreg_cloud)."""
 
-    def __init__(self, cloud: PointCloud, ctx: Context | None = None):
+    def __init__(self, cloud: PointCloud, ctx: Context | None = None, handle=None):
         self.ctx = ctx or default_context()
         self.cloud = cloud
-        h = P()
-        _check(lib().kreg_cloud_create(self.ctx.h, cloud.view(), C.byref(h)))
-        self.h = h
+        if handle is None:
+            handle = P()
+            _check(lib().kreg_cloud_create(self.ctx.h, cloud.view(), C.byref(handle)))
+        self.h = handle
 
     def size(self):
         return self.cloud.size()
@@ -241,6 +245,34 @@ class DeviceCloud:
             lib().kreg_cloud_destroy(self.h)
         except Exception:
             pass
+
+
+_KIND_NAMES = {0: "color", 1: "intensity", 2: "semantic", 3: "custom"}
+
+
+def read_ply(path: str, ctx: Context | None = None, warnings: list | None = None) -> DeviceCloud:
+    """read_cloud for .ply (cloud_io.cpp:141-297) straight into a device cloud:
+    the vertex block is read once into pinned memory and decoded, ordered and
+    laid out on the device. `.cloud` is the host view (positions exact,
+    features the device's FP32 values). Raises ParseError like the reference."""
+    from .types import Channel, ChannelKind, FeatureSchema
+    ctx = ctx or default_context()
+    h = P()
+    wbuf = C.create_string_buffer(1 << 16)
+    _check(lib().kreg_cloud_read_ply(ctx.h, os.fsencode(path), C.byref(h), wbuf, len(wbuf)))
+    if warnings is not None:
+        warnings.extend(w for w in wbuf.value.decode().split("\n") if w)
+    n = lib().kreg_cloud_size(h)
+    dim, nch = np.zeros(1, np.int32), np.zeros(1, np.int32)
+    dims, kinds = np.zeros(8, np.int32), np.zeros(8, np.int32)
+    _check(lib().kreg_cloud_schema(h, _abi.as_ptr(dim, C.c_int32), _abi.as_ptr(nch, C.c_int32),
+                                   _abi.as_ptr(dims, C.c_int32), _abi.as_ptr(kinds, C.c_int32), 8))
+    xyz = np.zeros((n, 3))
+    feat = np.zeros((n, int(dim[0])))
+    _check(lib().kreg_cloud_download(h, _abi.as_ptr(xyz), _abi.as_ptr(feat) if dim[0] else None))
+    schema = FeatureSchema([Channel(_KIND_NAMES[int(kinds[k])], int(dims[k]), ChannelKind(int(kinds[k])))
+                            for k in range(int(nch[0]))])
+    return DeviceCloud(PointCloud(xyz, schema, feat), ctx, handle=h)
 
 
 def device_cloud(c, ctx: Context | None = None) -> DeviceCloud:

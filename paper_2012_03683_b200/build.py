@@ -15,7 +15,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libkreg_b200.so")
 OBJ_DIR = os.path.join(HERE, "_build")
 
-SOURCES = ["kernels.cu", "dense.cu", "ingest.cu", "engine_host.cu", "solver.cpp", "capi.cpp"]
+SOURCES = ["kernels.cu", "dense.cu", "ingest.cu", "ply.cu", "engine_host.cu", "solver.cpp", "capi.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O3", "-Xptxas", "-v",
               "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include")]

@@ -394,6 +394,40 @@ kreg_status kreg_cloud_destroy(kreg_cloud* cloud) {
 
 int32_t kreg_cloud_size(const kreg_cloud* cloud) { return cloud ? cloud->n : 0; }
 
+kreg_status kreg_cloud_read_ply(kreg_ctx* ctx, const char* path, kreg_cloud** out, char* warnings,
+                                int32_t warnings_cap) {
+  return guarded([&] {
+    require(ctx && path && out, "NULL argument");
+    std::string w;
+    *out = cloud_read_ply(ctx, path, &w);
+    if (warnings && warnings_cap > 0) {
+      const size_t k = std::min(w.size(), static_cast<size_t>(warnings_cap - 1));
+      std::memcpy(warnings, w.data(), k);
+      warnings[k] = '\0';
+    }
+  });
+}
+
+kreg_status kreg_cloud_schema(const kreg_cloud* cloud, int32_t* dim, int32_t* n_channels, int32_t* dims,
+                              int32_t* kinds, int32_t cap) {
+  return guarded([&] {
+    require(cloud != nullptr, "NULL argument");
+    if (dim) *dim = cloud->dim;
+    if (n_channels) *n_channels = static_cast<int32_t>(cloud->schema.size());
+    for (size_t k = 0; k < cloud->schema.size() && static_cast<int32_t>(k) < cap; ++k) {
+      if (dims) dims[k] = cloud->schema[k].dim;
+      if (kinds) kinds[k] = cloud->schema[k].kind;
+    }
+  });
+}
+
+kreg_status kreg_cloud_download(const kreg_cloud* cloud, double* xyz, double* features) {
+  return guarded([&] {
+    require(cloud != nullptr, "NULL argument");
+    cloud_download(cloud, xyz, features);
+  });
+}
+
 kreg_status kreg_build_pairs(kreg_ctx* ctx, const kreg_cloud* X, const kreg_cloud* Z, const double T[12],
                              const kreg_kernel_params* params, double cutoff_multiplier, double c_min,
                              kreg_pairs** out, int64_t* n_pairs) {

@@ -293,6 +293,10 @@ std::string describe_schema(const kreg_cloud* c);
 void check_config(const kreg_registration_config& c);
 
 kreg_cloud* cloud_create(kreg_ctx* ctx, const kreg_cloud_view* v);
+size_t cloud_stage_floats(const kreg_cloud* c);
+// PLY file -> device cloud (ply.cu); "property ... skipped" lines appended to warnings
+kreg_cloud* cloud_read_ply(kreg_ctx* ctx, const std::string& path, std::string* warnings);
+void cloud_download(const kreg_cloud* c, double* xyz, double* features);
 // Validation + metadata only (no device copies).
 kreg_cloud* cloud_describe(kreg_ctx* ctx, const kreg_cloud_view* v);
 // End-to-end batch: clouds (2k, 2k + 1) of job k staged and uploaded by

@@ -295,6 +295,16 @@ class NoOverlapError(RuntimeError):
         self.cutoff_radius = cutoff_radius
 
 
+class ParseError(RuntimeError):
+    """kreg::ParseError (errors.hpp:9-22): "path:line: message"."""
+
+    @property
+    def line(self) -> int:
+        import re
+        m = re.search(r":(\d+): ", str(self))
+        return int(m.group(1)) if m else 0
+
+
 class CudaError(RuntimeError):
     pass
 
@@ -308,6 +318,8 @@ def raise_for(code: int, message: str):
         raise NoOverlapError(message)
     if code in (_abi.KREG_CUDA_ERROR, _abi.KREG_OUT_OF_MEMORY, _abi.KREG_NO_DEVICE):
         raise CudaError(message)
+    if code == _abi.KREG_PARSE_ERROR:
+        raise ParseError(message)
     raise RuntimeError(message)
 
 

@@ -227,9 +227,40 @@ class Reference:
         L.kref_make_box_cloud.argtypes = [C.c_uint64, C.c_int, C.c_int, _abi.dptr, _abi.dptr]
         L.kref_make_ring_cloud.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_int, _abi.dptr, _abi.dptr]
         L.kref_max_threads.restype = C.c_int
+        L.kref_write_ply.argtypes = [VP, C.c_char_p, C.c_int]
+        L.kref_read_ply.argtypes = [C.c_char_p, C.POINTER(P), C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                    C.POINTER(C.c_int), C.c_char_p, C.c_int]
+        L.kref_cloud_copy.argtypes = [P, _abi.dptr, _abi.dptr, _abi.i32ptr, _abi.i32ptr]
+        L.kref_cloud_destroy.argtypes = [P]
 
     def _err(self, rc):
         raise_for(rc, self.lib.kref_last_error().decode())
+
+    # cloud file I/O: the reference's write_ply / read_cloud (cloud_io.cpp)
+    def write_ply(self, cloud, path, binary=True):
+        self._err(self.lib.kref_write_ply(cloud.view(), os.fsencode(path), int(binary)))
+
+    def read_ply(self, path):
+        """Returns (PointCloud with FP64 features, warnings list)."""
+        from paper_2012_03683_b200.types import Channel, ChannelKind, FeatureSchema
+        h, n, dim, nch = P(), C.c_int(), C.c_int(), C.c_int()
+        w = C.create_string_buffer(1 << 16)
+        self._err(self.lib.kref_read_ply(os.fsencode(path), C.byref(h), C.byref(n), C.byref(dim), C.byref(nch),
+                                         w, len(w)))
+        xyz = np.zeros((n.value, 3))
+        feat = np.zeros((n.value, max(dim.value, 1)))
+        dims = np.zeros(8, np.int32)
+        kinds = np.zeros(8, np.int32)
+        self.lib.kref_cloud_copy(h, _abi.as_ptr(xyz), _abi.as_ptr(feat), _abi.as_ptr(dims, C.c_int32),
+                                 _abi.as_ptr(kinds, C.c_int32))
+        self.lib.kref_cloud_destroy(h)
+        warns = [x for x in w.value.decode().split("\n") if x]
+        if nch.value == 0:
+            return PointCloud(xyz), warns
+        names = {0: "color", 1: "intensity", 2: "semantic", 3: "custom"}
+        schema = FeatureSchema([Channel(names[int(kinds[k])], int(dims[k]), ChannelKind(int(kinds[k])))
+                                for k in range(nch.value)])
+        return PointCloud(xyz, schema, feat[:, :dim.value]), warns
 
     # frame ingest: the reference's select_points / depth_rgb_to_cloud
     def select_points(self, rgb, valid, sel):
