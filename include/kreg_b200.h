@@ -272,6 +272,17 @@ kreg_status kreg_objective_and_gradient(kreg_ctx* ctx, const kreg_pairs* pairs,
                                         const kreg_cloud* X, const kreg_cloud* Z,
                                         const double T[12], const kreg_kernel_params* params,
                                         double out[7]);
+/* Second-order step-size terms along a search direction (north_star item
+ * (4); diagnostic only: the reference has no second-order step, SURVEY.md
+ * §8 A15, and the engine never uses them for a step decision). For
+ * F(eps) = inner_product(pairs, X, Z, exp(eps xi) T) with the pair list held
+ * fixed (left perturbation, the reference's candidate form
+ * registration.cpp:69), out = {F, dF/d eps, d2F/d eps2} at eps = 0, from one
+ * fused device pass (extra per-pair and per-tile reductions of the sweep).
+ * The Newton step along xi is -out[1] / out[2] where out[2] < 0. */
+kreg_status kreg_directional_terms(kreg_ctx* ctx, const kreg_pairs* pairs, const kreg_cloud* X,
+                                   const kreg_cloud* Z, const double T[12], const double xi[6],
+                                   const kreg_kernel_params* params, double out[3]);
 /* Batched candidate evaluation (the line-search candidates of
  * registration.cpp:63-75 in one device pass): K transforms, out K x 8 =
  * {F, omega[3], v[3], max displacement vs the pair list's build transform}. */

@@ -510,6 +510,45 @@ void ko_objective_and_gradient(const ko_pairs* p, const kreg_cloud_view* X,
   }
 }
 
+/* Second-order step-size terms along xi (north_star item (4); diagnostic
+ * only, the reference has no second-order step: SURVEY.md §8 A15).
+ * F(eps) = sum c k(|x_i - q_j(eps)|^2) with q_j(eps) = exp(eps xi) T z_j
+ * (left perturbation, registration.cpp:69), so q' = u = omega x q + v and
+ * q'' = omega x u at eps = 0; with d = x - q:
+ *   F'  = sum w (d.u) / l^2
+ *   F'' = sum w [ (d.u)^2 / l^4 - (|u|^2 - d.(omega x u)) / l^2 ]
+ * out = {F, F'(0), F''(0)}. */
+void ko_directional_terms(const ko_pairs* p, const kreg_cloud_view* X, const kreg_cloud_view* Z,
+                          const double T[12], const double xi[6], const kreg_kernel_params* params, double out[3]) {
+  out[0] = out[1] = out[2] = 0.0;
+  if (p->n == 0) return;
+  const double inv_l2 = 1.0 / (params->lengthscale * params->lengthscale);
+  double* partial = (double*)calloc((size_t)p->n_z * 3, sizeof(double));
+#pragma omp parallel for schedule(dynamic, 64)
+  for (int j = 0; j < p->n_z; ++j) {
+    double q[3];
+    apply(T, Z->xyz + 3 * j, q);
+    const double* w_ = xi;
+    const double u[3] = {w_[1] * q[2] - w_[2] * q[1] + xi[3], w_[2] * q[0] - w_[0] * q[2] + xi[4],
+                         w_[0] * q[1] - w_[1] * q[0] + xi[5]};
+    const double ou[3] = {w_[1] * u[2] - w_[2] * u[1], w_[2] * u[0] - w_[0] * u[2], w_[0] * u[1] - w_[1] * u[0]};
+    const double uu = u[0] * u[0] + u[1] * u[1] + u[2] * u[2];
+    double* a = partial + 3 * (size_t)j;
+    for (int64_t e = p->offsets[j]; e < p->offsets[j + 1]; ++e) {
+      const double* x = X->xyz + 3 * p->x_index[e];
+      const double w = p->coeff[e] * kernel_sq(sqdist(x, q), params->sigma, params->lengthscale);
+      const double d[3] = {x[0] - q[0], x[1] - q[1], x[2] - q[2]};
+      const double du = d[0] * u[0] + d[1] * u[1] + d[2] * u[2];
+      const double dou = d[0] * ou[0] + d[1] * ou[1] + d[2] * ou[2];
+      a[0] += w;
+      a[1] += w * du * inv_l2;
+      a[2] += w * (du * du * inv_l2 * inv_l2 - (uu - dou) * inv_l2);
+    }
+  }
+  pairwise_sum(partial, (size_t)p->n_z, 3, out);
+  free(partial);
+}
+
 /* inner_product.cpp:238-246 */
 double ko_max_point_displacement(const kreg_cloud_view* Z, const double built[12], const double now[12]) {
   double worst = 0.0;

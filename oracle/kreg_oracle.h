@@ -49,6 +49,8 @@ void ko_objective_and_gradient(const ko_pairs* p, const kreg_cloud_view* X,
                                const kreg_cloud_view* Z, const double T[12],
                                const kreg_kernel_params* params, double out[7]);
 /* inner_product.cpp:238-246 */
+void ko_directional_terms(const ko_pairs* p, const kreg_cloud_view* X, const kreg_cloud_view* Z,
+                          const double T[12], const double xi[6], const kreg_kernel_params* params, double out[3]);
 double ko_max_point_displacement(const kreg_cloud_view* Z, const double built[12],
                                  const double now[12]);
 /* point_cloud.cpp:69-87 */

@@ -85,6 +85,7 @@ def lib():
         L.kreg_inner_product.argtypes = [P, P, P, P, _abi.dptr, KP, _abi.dptr]
         L.kreg_objective_and_gradient.argtypes = [P, P, P, P, _abi.dptr, KP, _abi.dptr]
         L.kreg_eval_transforms.argtypes = [P, P, P, P, _abi.dptr, C.c_int32, KP, C.c_uint32, _abi.dptr]
+        L.kreg_directional_terms.argtypes = [P, P, P, P, _abi.dptr, _abi.dptr, KP, _abi.dptr]
         L.kreg_evaluate_alignment.argtypes = [P, P, P, P, _abi.dptr, KP, _abi.dptr, _abi.dptr, _abi.i64ptr]
         L.kreg_indicator.argtypes = [P, P, P, _abi.dptr, KP, D, D, _abi.dptr]
         L.kreg_max_point_displacement.argtypes = [P, P, _abi.dptr, _abi.dptr, _abi.dptr]
@@ -384,6 +385,18 @@ def inner_product(pairs: PairList, X, Z, T, params: KernelParams) -> float:
 def objective_and_gradient(pairs: PairList, X, Z, T, params: KernelParams) -> Evaluation:
     o = eval_transforms(pairs, X, Z, [T], params)[0]
     return Evaluation(float(o[0]), o[1:7].copy())
+
+
+def directional_terms(pairs: PairList, X, Z, T, xi, params: KernelParams) -> np.ndarray:
+    """{F, dF/d eps, d2F/d eps2} at eps = 0 for F(eps) = inner_product at
+    exp(eps xi) T, pair list fixed: the second-order step-size terms (a
+    diagnostic; no reference counterpart)."""
+    t, tp = _t12(T)
+    x = np.ascontiguousarray(np.asarray(xi, dtype=np.float64).reshape(6))
+    out = np.zeros(3)
+    _check(lib().kreg_directional_terms(pairs.X.ctx.h, pairs.h, pairs.X.h, pairs.Z.h, tp, _abi.as_ptr(x),
+                                        params.cstruct(), _abi.as_ptr(out)))
+    return out
 
 
 def gradient(pairs, X, Z, T, params) -> np.ndarray:

@@ -519,6 +519,35 @@ kreg_status kreg_eval_transforms(kreg_ctx* ctx, const kreg_pairs* pairs, const k
   });
 }
 
+kreg_status kreg_directional_terms(kreg_ctx* ctx, const kreg_pairs* pairs, const kreg_cloud* X, const kreg_cloud* Z,
+                                   const double T[12], const double xi[6], const kreg_kernel_params* params,
+                                   double out[3]) {
+  return guarded([&] {
+    require(ctx && pairs && T && xi && params && out, "invalid argument");
+    check_pairs_match(pairs, X, Z);
+    if (pairs->P == 0) {  // empty list: F and its derivatives vanish
+      out[0] = out[1] = out[2] = 0.0;
+      return;
+    }
+    double o[kreg_dev::kOut + 2];
+    std::vector<BuildJob> none;
+    std::vector<EvalJob> evals(1);
+    EvalJob& e = evals[0];
+    e.pairs = const_cast<kreg_pairs*>(pairs);
+    e.M = 1;
+    std::memcpy(e.T[0], T, sizeof(double) * 12);
+    e.lengthscale = params->lengthscale;
+    e.sigma = params->sigma;
+    e.out = o;
+    e.second = true;
+    std::memcpy(e.dir, xi, sizeof(e.dir));
+    run_round(ctx, none, evals);
+    out[0] = o[0];
+    out[1] = o[kreg_dev::kOut];
+    out[2] = o[kreg_dev::kOut + 1];
+  });
+}
+
 kreg_status kreg_inner_product(kreg_ctx* ctx, const kreg_pairs* pairs, const kreg_cloud* X, const kreg_cloud* Z,
                                const double T[12], const kreg_kernel_params* params, double* value) {
   double o[8];

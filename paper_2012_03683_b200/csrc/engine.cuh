@@ -83,6 +83,7 @@ __host__ __device__ __forceinline__ long long slot_index(long long tile_off, int
 constexpr int kMaxChannels = 8;
 constexpr int kMaxCandidates = 8;   // candidate transforms per sweep request
 constexpr int kOut = 8;             // {F, omega[3], v[3], max displacement}
+constexpr int kNvSecond = 11;       // partial values of a second-order request: 7 + {sum w (d.u)^2, u.S, |u|^2 W, (w x u).S}
 constexpr int kScanTile = 2048;     // elements per scan tile
 
 struct ChannelDev {
@@ -189,6 +190,8 @@ struct alignas(16) SweepReq {
   const int4* slots;
   long long capacity;    // slot capacity (an overflowed build is skipped)
   int grad;              // 0: F (+ displacement) only, 1: F + gradient
+  int second;            // 1 (M = 1, grad): also dF/d eps, d2F/d eps2 along exp(eps xi) T -> out[kOut .. kOut + 1]
+  float dir[6];          // xi = {omega, omega x anchor + v} (second-order requests)
   int chunk_pref;        // the list's sweep chunking (chunk_units)
   const double* zx; const double* zy; const double* zz;  // source, sorted
   int n_z;

@@ -621,7 +621,8 @@ static long long sweep_units(const kreg_pairs* p) {
 
 // chunk partials of one request: at most kMaxChunks x M x (7 | 1) doubles
 static size_t sweep_partials(const EvalJob& job) {
-  return static_cast<size_t>(kreg_dev::kMaxChunks + kreg_dev::kMaxChunkGroups) * job.M * (job.grad ? 7 : 1);
+  return static_cast<size_t>(kreg_dev::kMaxChunks + kreg_dev::kMaxChunkGroups) * job.M *
+         (job.second ? kreg_dev::kNvSecond : job.grad ? 7 : 1);
 }
 
 static void prepare_sweep(EvalJob& job, kreg_dev::SweepReq& R, double* partials, unsigned long long* disp_bits) {
@@ -637,7 +638,18 @@ static void prepare_sweep(EvalJob& job, kreg_dev::SweepReq& R, double* partials,
   R.n_tiles = p->n_tiles;
   R.slots = p->slot_buf.ptr;
   R.capacity = static_cast<long long>(p->slot_buf.cap);
-  R.grad = job.grad ? 1 : 0;
+  R.grad = job.grad || job.second ? 1 : 0;
+  R.second = job.second ? 1 : 0;
+  if (job.second) {  // u_j = omega x T z_j + v = omega x (arm_j) + (omega x anchor + v)
+    const double* w = job.dir;
+    const double* a = p->anchor;
+    const double v2[3] = {w[1] * a[2] - w[2] * a[1] + w[3], w[2] * a[0] - w[0] * a[2] + w[4],
+                          w[0] * a[1] - w[1] * a[0] + w[5]};
+    for (int k = 0; k < 3; ++k) {
+      R.dir[k] = static_cast<float>(w[k]);
+      R.dir[3 + k] = static_cast<float>(v2[k]);
+    }
+  }
   R.chunk_pref = p->chunk_pref;
   R.zx = p->Z->x.ptr; R.zy = p->Z->y.ptr; R.zz = p->Z->z.ptr;
   R.n_z = nz;
@@ -890,7 +902,7 @@ void end_round(kreg_ctx* ctx, RoundSlot& S) {
   ctx->d2h_bytes += d2h;
   for (int e = 0; e < ne; ++e) {
     std::memcpy(evals[e].out, res + static_cast<size_t>(e) * kreg_dev::kMaxCandidates * kreg_dev::kOut,
-                sizeof(double) * kreg_dev::kOut * evals[e].M);
+                sizeof(double) * (kreg_dev::kOut * evals[e].M + (evals[e].second ? 2 : 0)));
     ctx->pair_evals += evals[e].pairs->P * evals[e].M;
     round_pairs += evals[e].pairs->P;
     round_slots += evals[e].pairs->slots;

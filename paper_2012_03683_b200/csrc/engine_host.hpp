@@ -345,6 +345,8 @@ struct EvalJob {
   double sigma = 1.0;  // kernel amplitude of the evaluation (params.sigma, inner_product.cpp:100,126)
   double* out;         // host, M x 8 {F, omega, v, disp}; filled after run_round
   bool grad = true;    // false: F + displacement only (gradient left zero)
+  bool second = false; // M = 1: also {dF/d eps, d2F/d eps2} along exp(eps dir) T in out[8..9]
+  double dir[6] = {0, 0, 0, 0, 0, 0};
 };
 
 // Device resources of one in-flight round.

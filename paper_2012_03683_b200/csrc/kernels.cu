@@ -875,10 +875,11 @@ constexpr size_t kSweepSmem = (size_t)kSweepWarps * kSweepStages * kStageSlots *
 // `units` sweep units (2 steps each) of one tile column (lane = source) for M
 // candidates: d = (x - T_b z) - delta, w = ex2(r^2 kappa + log2 c), W += w
 // and (GRAD) S += w d on FFMA2/FADD2/FMUL2 + 2 MUFU.EX2 per candidate pair.
-template <int NP, bool GRAD>
+template <int NP, bool GRAD, bool SO>
 __device__ __forceinline__ void sweep_steps(const int4* __restrict__ unit, int lane, int units, const f2_t (&ndx)[NP],
                                             const f2_t (&ndy)[NP], const f2_t (&ndz)[NP], f2_t kap2, f2_t (&W)[NP],
-                                            f2_t (&Sx)[NP], f2_t (&Sy)[NP], f2_t (&Sz)[NP]) {
+                                            f2_t (&Sx)[NP], f2_t (&Sy)[NP], f2_t (&Sz)[NP], f2_t ux, f2_t uy,
+                                            f2_t uz, f2_t& Q2) {
   // slot s of unit u sits at 2 lane + (s ^ sw) (slot_index): two swizzled bases
   const int sw = (lane >> 2) & 1;
   const int4* p0 = unit + 2 * lane + sw;
@@ -901,6 +902,10 @@ __device__ __forceinline__ void sweep_steps(const int4* __restrict__ unit, int l
         fma2_acc(Sx[p], w, dx);
         fma2_acc(Sy[p], w, dy);
         fma2_acc(Sz[p], w, dz);
+      }
+      if (SO) {  // second-order term: w (d . u)^2, u = dq/d eps of the source
+        const f2_t du = fma2(dz, uz, fma2(dy, uy, mul2(dx, ux)));
+        fma2_acc(Q2, w, mul2(du, du));
       }
     }
   };
@@ -954,16 +959,16 @@ __device__ __noinline__ void item_done(const SweepReq& R, SweepCtl* ctl, int r, 
   old = __shfl_sync(0xffffffffu, old, 0);
   __syncwarp();
   if ((int)old != n_items - 1) return;
-  const int M = R.M, NV = R.grad ? 7 : 1, MV = M * NV;
+  const int M = R.M, NV = R.second ? kNvSecond : (R.grad ? 7 : 1), MV = M * NV;
   const int C = chunk_count(request_units(R), R.chunk_pref);
   const int NG = (C + kChunkGroup - 1) / kChunkGroup;
   const double* gpart = R.partials + (size_t)kMaxChunks * MV;
   // group partials: lane l holds groups l and l + 32 (NG <= 64), fixed-order
   // shuffle tree per value
-  double t[7];
+  double t[kNvSecond];
   for (int m = 0; m < M; ++m) {
 #pragma unroll
-    for (int k = 0; k < 7; ++k) {
+    for (int k = 0; k < kNvSecond; ++k) {
       double v = 0.0;
       if (k < NV) {
         if (lane < NG) v = __ldcg(gpart + (size_t)lane * MV + m * NV + k);
@@ -992,6 +997,10 @@ __device__ __noinline__ void item_done(const SweepReq& R, SweepCtl* ctl, int r, 
     const unsigned long long db = __ldcg(&R.disp_bits[lane]);
     o[7] = sqrt(__longlong_as_double((long long)db));
     R.disp_bits[lane] = 0ull;
+    if (R.second) {  // dF/d eps and d2F/d eps2 along exp(eps xi) T, in the next candidate's row (M = 1)
+      o[kOut] = g * t[8];
+      o[kOut + 1] = R.sigma2 * (t[7] * R.inv_l2 * R.inv_l2 - (t[9] - t[10]) * R.inv_l2);
+    }
   }
   if (lane == 0) ctl->req_done[r] = 0u;
 }
@@ -1114,12 +1123,14 @@ __device__ __noinline__ void displacement_item(SweepWarp& w, const SweepReq& R, 
 // One chunk (units [u0, u1) of request r) for M <= 2 NP candidates: stream the
 // stages, accumulate per tile, write the chunk partial, then the group /
 // request completion steps.
-template <int NP, bool GRAD>
+template <int NP, bool GRAD, bool SO = false>
 __device__ __forceinline__ void chunk_body(SweepWarp& w, const SweepReq& R, int r, int c, int C, int n_items) {
   constexpr int MAXM = 2 * NP;
+  constexpr int NV = SO ? kNvSecond : (GRAD ? 7 : 1);  // values per candidate in a partial
+  static_assert(!SO || (NP == 1 && GRAD), "second-order terms: one candidate with its gradient");
   const int lane = w.lane;
   const int M = R.M;
-  const int MV = M * (GRAD ? 7 : 1);
+  const int MV = M * NV;
   const long long U = w.units[r], cu = chunk_units(U, R.chunk_pref);
   const long long u0 = (long long)c * cu, u1 = min(U, u0 + cu);
   const f2_t kap2 = pk2(R.kappa, R.kappa);
@@ -1137,14 +1148,15 @@ __device__ __forceinline__ void chunk_body(SweepWarp& w, const SweepReq& R, int 
     __syncwarp();
   }
 
-  f2_t acc[NP][7];
+  f2_t acc[NP][SO ? kNvSecond : 7];
   f2_t ndx[NP], ndy[NP], ndz[NP];  // -delta per candidate pair
   float ax[MAXM], ay[MAXM], az[MAXM];  // torque arm T_m z_j - anchor
   f2_t W[NP], Sx[NP], Sy[NP], Sz[NP];
+  f2_t ux = 0ull, uy = 0ull, uz = 0ull, Q2 = 0ull;  // SO: u_j = omega x T z_j + v, sum w (d.u)^2
 #pragma unroll
   for (int p = 0; p < NP; ++p)
 #pragma unroll
-    for (int v = 0; v < 7; ++v) acc[p][v] = 0ull;
+    for (int v = 0; v < (SO ? kNvSecond : 7); ++v) acc[p][v] = 0ull;
 #pragma unroll
   for (int p = 0; p < NP; ++p) W[p] = Sx[p] = Sy[p] = Sz[p] = 0ull;
 
@@ -1169,6 +1181,15 @@ __device__ __forceinline__ void chunk_body(SweepWarp& w, const SweepReq& R, int 
         az[m] = fmaf(A[8], zx, fmaf(A[9], zy, fmaf(A[10], zz, A[11])));
       }
     }
+    if (SO) {  // u = omega x (arm + anchor) + v = omega x arm + v' (v' = omega x anchor + v)
+      const float* d = R.dir;
+      const float vx = fmaf(d[1], az[0], fmaf(-d[2], ay[0], d[3]));
+      const float vy = fmaf(d[2], ax[0], fmaf(-d[0], az[0], d[4]));
+      const float vz = fmaf(d[0], ay[0], fmaf(-d[1], ax[0], d[5]));
+      ux = pk2(vx, vx);
+      uy = pk2(vy, vy);
+      uz = pk2(vz, vz);
+    }
   };
   bool active = false;
   auto flush_tile = [&]() {
@@ -1188,10 +1209,25 @@ __device__ __forceinline__ void chunk_body(SweepWarp& w, const SweepReq& R, int 
           acc[p][5] = add2(acc[p][5], fma2(mul2(neg, fqx), Sz[p], mul2(fqz, Sx[p])));
           acc[p][6] = add2(acc[p][6], fma2(mul2(neg, fqy), Sx[p], mul2(fqx, Sy[p])));
         }
+        if (SO) {  // {sum w (d.u)^2, u . S, |u|^2 W, (omega x u) . S} of the tile
+          const float* d = R.dir;
+          float u0, u1, v0, v1, w0, w1;
+          upk2(ux, u0, u1);
+          upk2(uy, v0, v1);
+          upk2(uz, w0, w1);
+          const f2_t ou_x = pk2(d[1] * w0 - d[2] * v0, d[1] * w0 - d[2] * v0);
+          const f2_t ou_y = pk2(d[2] * u0 - d[0] * w0, d[2] * u0 - d[0] * w0);
+          const f2_t ou_z = pk2(d[0] * v0 - d[1] * u0, d[0] * v0 - d[1] * u0);
+          acc[p][7] = add2(acc[p][7], Q2);
+          acc[p][8] = add2(acc[p][8], fma2(uz, Sz[p], fma2(uy, Sy[p], mul2(ux, Sx[p]))));
+          acc[p][9] = add2(acc[p][9], mul2(W[p], fma2(uz, uz, fma2(uy, uy, mul2(ux, ux)))));
+          acc[p][10] = add2(acc[p][10], fma2(ou_z, Sz[p], fma2(ou_y, Sy[p], mul2(ou_x, Sx[p]))));
+        }
       }
     }
 #pragma unroll
     for (int p = 0; p < NP; ++p) W[p] = Sx[p] = Sy[p] = Sz[p] = 0ull;
+    Q2 = 0ull;
   };
 
   if (u1 > u0) {
@@ -1223,7 +1259,7 @@ __device__ __forceinline__ void chunk_body(SweepWarp& w, const SweepReq& R, int 
       if (u != u0) mbar_wait(&w.bars[s], (w.consumed / kSweepStages) & 1);
       const int4* stage = w.ring + s * kStageSlots;
       if (u + nu <= t_end) {  // whole stage inside the current tile
-        if (active) sweep_steps<NP, GRAD>(stage, lane, nu, ndx, ndy, ndz, kap2, W, Sx, Sy, Sz);
+        if (active) sweep_steps<NP, GRAD, SO>(stage, lane, nu, ndx, ndy, ndz, kap2, W, Sx, Sy, Sz, ux, uy, uz, Q2);
       } else {
         long long v = u;
         while (v < u + nu) {
@@ -1246,8 +1282,8 @@ __device__ __forceinline__ void chunk_body(SweepWarp& w, const SweepReq& R, int 
           }
           const long long w_end = min(u + nu, t_end);
           if (active)
-            sweep_steps<NP, GRAD>(stage + (v - u) * kUnitSlots, lane, (int)(w_end - v), ndx, ndy, ndz, kap2, W, Sx, Sy,
-                                  Sz);
+            sweep_steps<NP, GRAD, SO>(stage + (v - u) * kUnitSlots, lane, (int)(w_end - v), ndx, ndy, ndz, kap2, W, Sx,
+                                      Sy, Sz, ux, uy, uz, Q2);
           v = w_end;
         }
       }
@@ -1266,10 +1302,10 @@ __device__ __forceinline__ void chunk_body(SweepWarp& w, const SweepReq& R, int 
 #pragma unroll
   for (int p = 0; p < NP; ++p) {
 #pragma unroll
-    for (int v = 0; v < (GRAD ? 7 : 1); ++v) {
+    for (int v = 0; v < NV; ++v) {
       float a0, a1;
       upk2(warp_sum_f2(acc[p][v]), a0, a1);
-      const int i0 = (2 * p) * (GRAD ? 7 : 1) + v, i1 = (2 * p + 1) * (GRAD ? 7 : 1) + v;
+      const int i0 = (2 * p) * NV + v, i1 = (2 * p + 1) * NV + v;
       if (2 * p < M && lane == (i0 & 31)) part[i0] = (double)a0;
       if (2 * p + 1 < M && lane == (i1 & 31)) part[i1] = (double)a1;
     }
@@ -1392,7 +1428,11 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepCtasPerSm) k_sweep(const 
     const unsigned long long ti0 = gtimer();
 #endif
     if (c < 0) displacement_item(w, R, r, c + D, n_items);
-    else if (R.grad) chunk_body<NPG, true>(w, R, r, c, C, n_items);
+    else if (R.grad && R.second) {
+      // second-order requests go to the NPG = 2 instantiation (sweep_batched),
+      // keeping their extra registers out of the main M <= 2 kernel
+      if constexpr (NPG == 2) chunk_body<1, true, true>(w, R, r, c, C, n_items);
+    } else if (R.grad) chunk_body<NPG, true>(w, R, r, c, C, n_items);
     else chunk_body<4, false>(w, R, r, c, C, n_items);
     __syncwarp();
     if (lane == 0) ++g_wq[wid].head;
@@ -1547,6 +1587,7 @@ void sweep_batched(const SweepReq* h, const SweepReq* d, int n, int sm_count, un
     long long items = 0;
     for (int r = r0; r < r1; ++r) {
       if (h[r].grad) max_mg = max(max_mg, h[r].M);
+      if (h[r].second) max_mg = max(max_mg, 3);  // NPG = 2 instantiation
       items += h[r].units >= 0 ? chunk_count(h[r].units, h[r].chunk_pref) + (h[r].n_z + kDispItem - 1) / kDispItem
                                : (1LL << 40);
     }

@@ -60,6 +60,7 @@ class Oracle:
         L.ko_inner_product.restype = D
         L.ko_objective_and_gradient.argtypes = [P, VP, VP, _abi.dptr, KP, _abi.dptr]
         L.ko_max_point_displacement.argtypes = [VP, _abi.dptr, _abi.dptr]
+        L.ko_directional_terms.argtypes = [P, VP, VP, _abi.dptr, _abi.dptr, KP, _abi.dptr]
         L.ko_max_point_displacement.restype = D
         L.ko_diameter.argtypes = [VP]
         L.ko_diameter.restype = D
@@ -133,6 +134,14 @@ class Oracle:
         a, ap = _d12(built)
         b, bp = _d12(now)
         return self.lib.ko_max_point_displacement(Z.view(), ap, bp)
+
+    def directional_terms(self, pairs, X, Z, T, xi, params):
+        t, tp = _d12(T)
+        x = np.ascontiguousarray(np.asarray(xi, dtype=np.float64).reshape(6))
+        out = np.zeros(3)
+        self.lib.ko_directional_terms(pairs.h, X.view(), Z.view(), tp, _abi.as_ptr(x), params.cstruct(),
+                                      _abi.as_ptr(out))
+        return out
 
     def diameter(self, X):
         return self.lib.ko_diameter(X.view())
