@@ -4,9 +4,11 @@
  * (/root/reference/proj, a C++20 library `kreg`). The reference has no FFI;
  * its boundary is the public C++ API. Every entry point below replaces one
  * function of that API (cited per function) with plain pointers, sizes and
- * status codes, so a ctypes / cgo / JNI binding can sit on it directly. The
- * C++ façade in include/kreg_b200/kreg.hpp restores the reference's names,
- * value types and exceptions on top of this ABI.
+ * status codes, so a ctypes / cgo / JNI binding can sit on it directly.
+ * include/kreg_b200/kreg.hpp is the C++ RAII layer over this ABI (handles,
+ * status -> exception mapping); paper_2012_03683_b200/facade/kreg_facade.cpp
+ * restores the reference's own API (names, value types, exceptions) on top
+ * of it as a drop-in for inner_product.cpp + registration.cpp.
  *
  * Conventions
  *  - Isometry = double[12], row-major 3x4 [R | t] (reference se3.hpp:27-34).

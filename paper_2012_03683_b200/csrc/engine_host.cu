@@ -735,6 +735,7 @@ RoundSlot::~RoundSlot() {
 }
 
 void begin_round(kreg_ctx* ctx, RoundSlot& S, std::vector<BuildJob>&& builds_in, std::vector<EvalJob>&& evals_in) {
+  NvtxScope nvtx("kreg.round.launch");
   S.builds = std::move(builds_in);
   S.evals = std::move(evals_in);
   std::vector<BuildJob>& builds = S.builds;
@@ -816,6 +817,7 @@ void begin_round(kreg_ctx* ctx, RoundSlot& S, std::vector<BuildJob>&& builds_in,
 
 void end_round(kreg_ctx* ctx, RoundSlot& S) {
   if (!S.in_flight) return;
+  NvtxScope nvtx("kreg.round.complete");
   using clk = std::chrono::steady_clock;
   const auto t1 = clk::now();
   KREG_CUDA(cudaEventSynchronize(S.done));

@@ -4,6 +4,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <chrono>
 #include <atomic>
@@ -23,6 +24,16 @@
 #include "engine.cuh"
 
 namespace kreg_host {
+
+// NVTX range for the duration of a scope (SURVEY.md §5 tracing): rounds,
+// their launch / wait phases and whole solver calls show up on the host
+// timeline of nsys / ncu --nvtx (a no-op without an attached tool).
+struct NvtxScope {
+  explicit NvtxScope(const char* name) { nvtxRangePushA(name); }
+  ~NvtxScope() { nvtxRangePop(); }
+  NvtxScope(const NvtxScope&) = delete;
+  NvtxScope& operator=(const NvtxScope&) = delete;
+};
 
 // Exception carrying a kreg_status; the C-ABI maps it back to a code.
 struct Error : std::runtime_error {

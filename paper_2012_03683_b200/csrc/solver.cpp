@@ -508,6 +508,7 @@ void reduce_round(RoundSlot& S, const Collective& coll) {
 }
 
 void register_many(kreg_ctx* ctx, std::vector<RegJob>& jobs, const Collective* coll) {
+  NvtxScope nvtx("kreg.register_many");
   const int k_first = std::max(1, std::min(8, env_int("KREG_K_FIRST", 2)));
   const bool fail_grad = env_int("KREG_FAIL_GRAD", 0) != 0;
   std::vector<std::unique_ptr<Reg>> regs;
