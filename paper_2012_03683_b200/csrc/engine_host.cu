@@ -721,6 +721,12 @@ RoundSlot* round_slot(kreg_ctx* ctx, int i) {
     KREG_CUDA(cudaEventCreate(&S->ev1));
     KREG_CUDA(cudaEventCreate(&S->evb0));
     KREG_CUDA(cudaEventCreate(&S->evb1));
+    S->stream = ctx->stream;
+    if (i == 1) {
+      KREG_CUDA(cudaStreamCreateWithFlags(&S->stream, cudaStreamNonBlocking));
+      KREG_CUDA(cudaEventCreateWithFlags(&S->ordered, cudaEventDisableTiming));
+      S->own_stream = true;
+    }
     ctx->rs[i] = S;
   }
   return ctx->rs[i];
@@ -732,6 +738,8 @@ RoundSlot::~RoundSlot() {
   if (ev1) cudaEventDestroy(ev1);
   if (evb0) cudaEventDestroy(evb0);
   if (evb1) cudaEventDestroy(evb1);
+  if (ordered) cudaEventDestroy(ordered);
+  if (own_stream && stream) cudaStreamDestroy(stream);
 }
 
 void begin_round(kreg_ctx* ctx, RoundSlot& S, std::vector<BuildJob>&& builds_in, std::vector<EvalJob>&& evals_in) {
@@ -771,13 +779,17 @@ void begin_round(kreg_ctx* ctx, RoundSlot& S, std::vector<BuildJob>&& builds_in,
     builds[b].pairs->last_req.refilter = 0;
     builds[b].pairs->index_valid = false;
   }
+  if (S.own_stream) {  // after everything already issued on the context stream (cloud uploads)
+    KREG_CUDA(cudaEventRecord(S.ordered, ctx->stream));
+    KREG_CUDA(cudaStreamWaitEvent(S.stream, S.ordered, 0));
+  }
   // builds go to the device before the sweep requests are prepared
   if (nb) {
     KREG_CUDA(cudaMemcpyAsync(S.d_build.ptr, S.h_build.ptr, sizeof(kreg_dev::BuildReq) * nb, cudaMemcpyHostToDevice,
-                              ctx->stream));
-    if (ctx->profiling) KREG_CUDA(cudaEventRecord(S.evb0, ctx->stream));
-    kreg_dev::build_pairs_batched(S.h_build.ptr, S.d_build.ptr, nb, ctx->stream);
-    if (ctx->profiling) KREG_CUDA(cudaEventRecord(S.evb1, ctx->stream));
+                              S.stream));
+    if (ctx->profiling) KREG_CUDA(cudaEventRecord(S.evb0, S.stream));
+    kreg_dev::build_pairs_batched(S.h_build.ptr, S.d_build.ptr, nb, S.stream);
+    if (ctx->profiling) KREG_CUDA(cudaEventRecord(S.evb1, S.stream));
   }
   const auto tb = clk::now();
   ctx->t_build_prep += std::chrono::duration<double>(tb - t0).count();
@@ -803,14 +815,14 @@ void begin_round(kreg_ctx* ctx, RoundSlot& S, std::vector<BuildJob>&& builds_in,
   ctx->t_sweep_prep += std::chrono::duration<double>(ts - tb).count();
   if (ne)
     KREG_CUDA(cudaMemcpyAsync(S.d_sweep.ptr, S.h_sweep.ptr, sizeof(kreg_dev::SweepReq) * ne, cudaMemcpyHostToDevice,
-                              ctx->stream));
+                              S.stream));
   if (ne) {
     S.sweep_issue = ctx->sweep_issued++;
-    kreg_dev::sweep_batched(S.h_sweep.ptr, S.d_sweep.ptr, ne, ctx->sm_count, S.counter_arena.ptr, ctx->stream,
+    kreg_dev::sweep_batched(S.h_sweep.ptr, S.d_sweep.ptr, ne, ctx->sm_count, S.counter_arena.ptr, S.stream,
                             ctx->profiling ? S.ev0 : nullptr, ctx->profiling ? S.ev1 : nullptr);
   }
   KREG_CUDA(cudaGetLastError());
-  KREG_CUDA(cudaEventRecord(S.done, ctx->stream));
+  KREG_CUDA(cudaEventRecord(S.done, S.stream));
   S.in_flight = true;
   ctx->t_prepare += std::chrono::duration<double>(clk::now() - t0).count();
 }

@@ -378,6 +378,12 @@ struct RoundSlot {
   DevBuf<float> g_feat;
   DevBuf<long long> g_scan;
   cudaEvent_t done = nullptr, ev0 = nullptr, ev1 = nullptr, evb0 = nullptr, evb1 = nullptr;
+  // the slot's stream: the context stream, or (slot 1 of a two-group batch)
+  // a second stream, so the two groups' rounds overlap on the device (one
+  // group's sweep tail with the other's builds and sweep)
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  cudaEvent_t ordered = nullptr;  // context-stream work (uploads) before this slot's round
   std::vector<BuildJob> builds;
   std::vector<EvalJob> evals;
   size_t n_res = 0;

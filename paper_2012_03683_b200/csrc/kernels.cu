@@ -1015,9 +1015,6 @@ __device__ __forceinline__ void reduce_group(const SweepReq& R, int grp, int C, 
 // A request's work item (chunk group or displacement slice) is complete; the
 // warp completing its last item finishes the request.
 __device__ __noinline__ void item_done(const SweepReq& R, SweepCtl* ctl, int r, int n_items, int lane) {
-#ifdef KREG_SEPARATE_REDUCE
-  return;  // k_sweep_finish reduces after the launch
-#endif
   __syncwarp();
   unsigned old = 0;
   if (lane == 0) old = atom_add_acq_rel(&ctl->req_done[r], 1u);
@@ -1059,7 +1056,6 @@ struct SweepWarp {
   int lane;
   int tc_r;          // request whose coefficients tc holds
   unsigned consumed, rec_used;
-  int next_g;        // KREG_ITEM_PREFETCH: item already grabbed for lane 0's next produce
 };
 
 __device__ __forceinline__ int disp_items(const SweepReq& R) { return (R.n_z + kDispItem - 1) / kDispItem; }
@@ -1079,14 +1075,7 @@ __device__ __forceinline__ bool produce(SweepWarp& w) {
   WarpQueue& Q = g_wq[threadIdx.x >> 5];
   while (Q.pu >= Q.pend) {
     if (Q.done || Q.tail - Q.head >= kQueueDepth) return false;
-#ifdef KREG_ITEM_PREFETCH
-    // the item grabbed one item ago; the next grab's latency overlaps this
-    // item's stages (its result is first read at the next grab)
-    const int g = w.next_g;
-    if (g < w.total) w.next_g = (int)atomicAdd(&w.ctl->next_item, 1u);
-#else
     const int g = (int)atomicAdd(&w.ctl->next_item, 1u);
-#endif
     if (g >= w.total) {
       Q.done = 1;
       return false;
@@ -1106,9 +1095,7 @@ __device__ __forceinline__ bool produce(SweepWarp& w) {
   const int nu = min(kStageUnits, Q.pend - Q.pu);
   const int s = Q.issued % kSweepStages;
   const SweepReq& P = w.reqs[Q.pr];
-#ifndef KREG_NO_PROXY_FENCE
   fence_proxy_async();
-#endif
   KREG_CHECK(((long long)Q.pu + nu) * kUnitSlots <= P.capacity && Q.pc < kMaxChunks && nu > 0, 6);
   mbar_expect_tx(&w.bars[s], nu * kUnitBytes + (Q.first ? (unsigned)sizeof(ChunkRec) : 0u));
   tma_load_1d(w.ring + s * kStageSlots, P.slots + (long long)Q.pu * kUnitSlots, nu * kUnitBytes, &w.bars[s]);
@@ -1343,9 +1330,6 @@ __device__ __forceinline__ void chunk_body(SweepWarp& w, const SweepReq& R, int 
       if (2 * p + 1 < M && lane == (i1 & 31)) part[i1] = (double)a1;
     }
   }
-#ifdef KREG_SEPARATE_REDUCE
-  return;  // k_sweep_finish sums groups and requests after the launch
-#endif
   // chunk group done? its last chunk sums the group's partials in order
   __syncwarp();
   const int grp = c / kChunkGroup;
@@ -1433,10 +1417,6 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepCtasPerSm) k_sweep(const 
   mbar_fence_init();
   __syncthreads();
   w.total = cbase[n_req];
-  w.next_g = 0;
-#ifdef KREG_ITEM_PREFETCH
-  if (lane == 0) w.next_g = (int)atomicAdd(&ctl->next_item, 1u);
-#endif
   if (lane == 0)
     for (int s = 0; s < kSweepStages; ++s)
       if (!produce(w)) break;
@@ -1506,22 +1486,6 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepCtasPerSm) k_sweep(const 
       ctl->exited = 0u;
     }
   }
-}
-
-// KREG_SEPARATE_REDUCE: after a sweep launch, warp per request: group sums,
-// then the request's totals (the same fixed-order trees as the in-kernel
-// finishers, so the results are bitwise those of the default build).
-__global__ void k_sweep_finish(const SweepReq* reqs, int n_req) {
-  const int r = blockIdx.x;
-  if (r >= n_req) return;
-  const SweepReq& R = reqs[r];
-  const int lane = threadIdx.x & 31;
-  const int NV = R.second ? kNvSecond : (R.grad ? 7 : 1);
-  const int C = chunk_count(request_units(R), R.chunk_pref);
-  const int NG = (C + kChunkGroup - 1) / kChunkGroup;
-  for (int grp = 0; grp < NG; ++grp) reduce_group(R, grp, C, R.M * NV, lane);
-  __syncwarp();
-  finish_request(R, lane);
 }
 
 __global__ void k_interleave(const double* x, const double* y, const double* z, int n, double4* out) {
@@ -1648,10 +1612,6 @@ void sweep_batched(const SweepReq* h, const SweepReq* d, int n, int sm_count, un
     else if (max_mg <= 4) k_sweep<2><<<grid, kSweepThreads, kSweepSmem, st>>>(dr, r1 - r0, ctl);
     else k_sweep<4><<<grid, kSweepThreads, kSweepSmem, st>>>(dr, r1 - r0, ctl);
     ++launches;
-#ifdef KREG_SEPARATE_REDUCE
-    k_sweep_finish<<<r1 - r0, 32, 0, st>>>(dr, r1 - r0);
-    ++launches;
-#endif
   }
   count_launch(launches);
   if (ev1) cudaEventRecord(ev1, st);

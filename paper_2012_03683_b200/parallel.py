@@ -134,13 +134,21 @@ def shard_rows(Z: PointCloud, rank: int, world: int) -> PointCloud:
 
 # ------------------------------------------------------------- collective
 class TorchCollective:
-    """kreg_collective_fn over torch.distributed: SUM all-reduce of `sums`, MAX
-    all-reduce of `maxes`, in place (CUDA tensors under NCCL, CPU under gloo).
-    Keep the object alive while the engine may call it."""
+    """kreg_collective_fn over torch.distributed (CUDA tensors under NCCL, CPU
+    under gloo), in place on the engine's host arrays. Keep the object alive
+    while the engine may call it.
 
-    def __init__(self, group=None):
+    deterministic=True (default): ONE all_gather of every rank's [sums, maxes]
+    and the sums added in rank order on every rank, so the totals are
+    bitwise independent of the collective's algorithm (ring / tree / NVLS) and
+    equal on all ranks. deterministic=False: a SUM all_reduce of `sums` and a
+    MAX all_reduce of `maxes` (two collectives, the backend's summation
+    order)."""
+
+    def __init__(self, group=None, deterministic: bool = True):
         from . import api
         self.group = group
+        self.deterministic = deterministic
         self.calls = 0
         self.c_fn = api.COLLECTIVE_FN(self._call)
 
@@ -149,13 +157,28 @@ class TorchCollective:
             import torch
             import torch.distributed as dist
             dev = _device()
-            for ptr, n, op in ((sums, n_sums, dist.ReduceOp.SUM), (maxes, n_maxes, dist.ReduceOp.MAX)):
-                if n <= 0:
-                    continue
-                host = np.ctypeslib.as_array(ptr, shape=(n,))
-                t = torch.from_numpy(host.copy()).to(dev)
-                dist.all_reduce(t, op=op, group=self.group)
-                host[:] = t.cpu().numpy()
+            s = np.ctypeslib.as_array(sums, shape=(n_sums,)) if n_sums > 0 else np.zeros(0)
+            m = np.ctypeslib.as_array(maxes, shape=(n_maxes,)) if n_maxes > 0 else np.zeros(0)
+            if self.deterministic:
+                world = dist.get_world_size(self.group)
+                t = torch.from_numpy(np.concatenate([s, m])).to(dev)
+                out = [torch.empty_like(t) for _ in range(world)]
+                dist.all_gather(out, t, group=self.group)
+                parts = np.stack([o.cpu().numpy() for o in out])  # [world, n_sums + n_maxes]
+                tot = parts[0, :n_sums].copy()
+                for r in range(1, world):  # fixed rank order
+                    tot = tot + parts[r, :n_sums]
+                if n_sums > 0:
+                    s[:] = tot
+                if n_maxes > 0:
+                    m[:] = parts[:, n_sums:].max(axis=0)
+            else:
+                for host, op in ((s, dist.ReduceOp.SUM), (m, dist.ReduceOp.MAX)):
+                    if host.size == 0:
+                        continue
+                    t = torch.from_numpy(host.copy()).to(dev)
+                    dist.all_reduce(t, op=op, group=self.group)
+                    host[:] = t.cpu().numpy()
             self.calls += 1
             return 0
         except Exception:  # surfaced by the engine as a failed call
@@ -163,15 +186,16 @@ class TorchCollective:
 
 
 # ------------------------------------------------------------- front ends
-def register_clouds_sharded(X: PointCloud, Z: PointCloud, initial, params, config, ctx=None, group=None):
+def register_clouds_sharded(X: PointCloud, Z: PointCloud, initial, params, config, ctx=None, group=None,
+                            deterministic: bool = True):
     """register_clouds(X, Z, ...) with Z's rows sharded over the ranks (C4).
-    Every rank returns the same RegistrationResult."""
+    Every rank returns the same RegistrationResult (TorchCollective modes)."""
     from . import api
     import torch.distributed as dist
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     Zr = shard_rows(Z, rank, world) if world > 1 else Z
-    coll = TorchCollective(group) if world > 1 else None
+    coll = TorchCollective(group, deterministic) if world > 1 else None
     return api.register_clouds_rows(X, Zr, Z.size(), initial, params, config, ctx=ctx, collective=coll)
 
 

@@ -92,11 +92,14 @@ def test_assemble_sequence_composes_trajectory():
 # ------------------------------------------------------------ collective
 def _collective_worker(rank, world, port, out_dir):
     _init(rank, world, port)
-    coll = parallel.TorchCollective()
-    sums = (C.c_double * 3)(1.0 + rank, 10.0 * rank, -2.0)
-    maxes = (C.c_double * 2)(float(rank), 5.0 - rank)
-    rc = coll.c_fn(None, sums, 3, maxes, 2)
-    np.save(os.path.join(out_dir, f"r{rank}.npy"), np.array([rc, *sums, *maxes], dtype=np.float64))
+    rows = []
+    for det in (True, False):  # all_gather + rank-order sum, and the two all_reduces
+        coll = parallel.TorchCollective(deterministic=det)
+        sums = (C.c_double * 3)(1.0 + rank, 10.0 * rank, -2.0)
+        maxes = (C.c_double * 2)(float(rank), 5.0 - rank)
+        rc = coll.c_fn(None, sums, 3, maxes, 2)
+        rows.append([rc, *sums, *maxes])
+    np.save(os.path.join(out_dir, f"r{rank}.npy"), np.array(rows, dtype=np.float64))
     assert parallel.reduce_scalar(float(rank + 1), "max") == float(world)
     assert parallel.reduce_scalar(1.0, "sum") == float(world)
 
@@ -105,10 +108,10 @@ def test_collective_callback_over_gloo():
     with tempfile.TemporaryDirectory() as d:
         _spawn(_collective_worker, 2, d)
         for r in range(2):
-            v = np.load(os.path.join(d, f"r{r}.npy"))
-            assert v[0] == 0
-            assert np.array_equal(v[1:4], [3.0, 10.0, -4.0])
-            assert np.array_equal(v[4:6], [1.0, 5.0])
+            for v in np.load(os.path.join(d, f"r{r}.npy")):
+                assert v[0] == 0
+                assert np.array_equal(v[1:4], [3.0, 10.0, -4.0])
+                assert np.array_equal(v[4:6], [1.0, 5.0])
 
 
 # ------------------------------------- row-sharded registration (mock device)
