@@ -447,10 +447,17 @@ static void prepare_build(kreg_ctx* ctx, BuildJob& job, kreg_dev::BuildReq& R) {
   // Reuse the resident candidate list when it provably contains every pair
   // of the new list: max_j |T z_j - Ts z_j| <= sup_disp + disp_hint (triangle
   // inequality over the list being replaced) and that must fit in R_s - cutoff.
+  // ... and while it is not much larger than a fresh one: annealing shrinks
+  // the cutoff, so a list kept from a larger lengthscale makes every filter
+  // scan (R_s / R_s,new)^3 times the entries (first-frame schedule: 0.95 ->
+  // 0.0475); above ctx->sup_shrink the grid is searched again
   const double margin = 1e-9 * p->sup_radius;
+  const double fresh = cutoff * (1.0 + std::max(0.0, ctx->skin));
+  const double grow = p->sup_radius / fresh;
   const bool reuse = !job.force_full && ctx->skin > 0.0 && p->sup_valid && p->sup_X == X && p->sup_Z == Z &&
                      std::memcmp(&p->sup_cp, &R.cp, sizeof(R.cp)) == 0 && job.disp_hint >= 0.0 &&
-                     p->sup_disp + job.disp_hint + cutoff <= p->sup_radius - 2.0 * margin;
+                     p->sup_disp + job.disp_hint + cutoff <= p->sup_radius - 2.0 * margin &&
+                     grow * grow * grow <= ctx->sup_shrink;
   // ... and the resident sweep list, filtered from that candidate list at
   // T_build with the old cutoff, holds every pair of the new list when
   // max_j |T z_j - T_build z_j| + cutoff <= old cutoff (annealing shrinks the
@@ -489,7 +496,8 @@ static void prepare_build(kreg_ctx* ctx, BuildJob& job, kreg_dev::BuildReq& R) {
     // the candidate radius, 3 other (clouds, coefficients, skin)
     const int why = !p->sup_valid ? 0 : job.force_full ? 1
                     : (p->sup_X == X && p->sup_Z == Z && job.disp_hint >= 0.0 && ctx->skin > 0.0 &&
-                       std::memcmp(&p->sup_cp, &R.cp, sizeof(R.cp)) == 0) ? 2 : 3;
+                       std::memcmp(&p->sup_cp, &R.cp, sizeof(R.cp)) == 0) ? (grow * grow * grow > ctx->sup_shrink ? 3 : 2)
+                                                                            : 3;
     ++ctx->full_why[why];
     ++p->full_builds;
     const double rs = cutoff * (1.0 + std::max(0.0, ctx->skin));

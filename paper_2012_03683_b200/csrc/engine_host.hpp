@@ -196,6 +196,9 @@ struct kreg_ctx {
   double build_ms = 0.0;
   long long build_rounds = 0, filter_entries = 0, built_slots = 0;
   long long full_why[4] = {0, 0, 0, 0};  // grid builds by cause (prepare_build)
+  // a resident candidate list is searched again once it holds more than
+  // sup_shrink x the entries of a fresh one (its radius^3 ratio; KREG_SUP_SHRINK)
+  double sup_shrink = std::getenv("KREG_SUP_SHRINK") ? std::atof(std::getenv("KREG_SUP_SHRINK")) : 3.0;
   long long refilter_builds = 0;         // filter builds that read the resident sweep list
   // sweep-list refilters (opt-in, KREG_REFILTER=1: equal results, but their
   // warp-per-tile kernels are load-imbalanced and measured slower than the
