@@ -39,6 +39,8 @@ sys.path.insert(0, ROOT)
 from paper_2012_03683_b200 import synth  # noqa: E402
 
 METRIC = "registrations/sec (KITTI-shape 19-class pairs)"
+C3_WORKLOAD = "C3 KITTI-shaped 40k-point semantic pairs (colour + 19-class), subsequent schedule l 0.1 -> 0.0475"
+SEED = 2012036830
 UNIT = "registrations/s"
 HBM_PEAK_FALLBACK = 6551.7
 
@@ -51,7 +53,7 @@ def measured_peaks():
         return {}
 
 
-def make_workload(rank: int, batch: int, n_points: int, seed: int = 2012036830):
+def make_workload(rank: int, batch: int, n_points: int, seed: int = SEED):
     """B independent KITTI-shaped frame pairs per rank: each
     pair is its own ray-cast street, second frame 1.0 m forward + 0.5 deg yaw,
     initial guess = true motion composed with a small error."""
@@ -376,11 +378,10 @@ def run_reference_arm(args, world, rank):
         "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "impl": "reference",
-        "config": {"workload": "C3 KITTI-shaped 40k-point semantic pairs (colour + 19-class), subsequent schedule "
-                               "l 0.1 -> 0.0475", "points": args.points,
-                   "step": "one frame pair registered to convergence (latency mode)",
-                   "mean_iterations": float(np.mean(iters)),
-                   "pairs": "make_workload(rank 0): the first steps + warmup pairs of the GPU arm's batch"},
+        "config": {"workload": C3_WORKLOAD, "points": args.points, "seed": SEED},
+        "execution": {"step": "one frame pair registered to convergence (latency mode)",
+                      "pairs": "make_workload(rank 0): the first steps + warmup pairs of the GPU arm's batch"},
+        "mean_iterations": float(np.mean(iters)),
         "cpu_modes": {"latency": {"value": v_lat, "pairs": args.steps, "threads_per_pair": cores,
                                   "mean_iterations": float(np.mean(iters))},
                       "throughput": {"value": v_thr, "pairs": cores, "threads_per_pair": 1, "seconds": secs,
@@ -509,11 +510,13 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dt_max / args.steps * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic",
-            "config": {"workload": "C3 KITTI-shaped 40k-point semantic pairs (colour + 19-class), subsequent "
-                                   "schedule l 0.1 -> 0.0475", "points": args.points, "pairs_per_step_per_gpu": B,
-                       "parallelism": f"independent pairs x {world} GPU(s), lockstep batch per GPU",
-                       "l2": "inputs larger than L2 (B pair lists > 126 MB)",
-                       "mean_iterations": float(np.mean(iters)) if iters else None},
+            # config: identical in both arms (same generator, same pairs);
+            # how each arm runs them is in "execution"
+            "config": {"workload": C3_WORKLOAD, "points": args.points, "seed": SEED},
+            "execution": {"pairs_per_step_per_gpu": B,
+                          "parallelism": f"independent pairs x {world} GPU(s), lockstep batch per GPU",
+                          "l2": "inputs larger than L2 (B pair lists > 126 MB)"},
+            "mean_iterations": float(np.mean(iters)) if iters else None,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
             "rounds_per_step": host["rounds"] / max(1, args.steps),

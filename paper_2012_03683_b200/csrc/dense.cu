@@ -20,6 +20,7 @@ namespace {
 
 constexpr int kDenseThreads = 128;
 constexpr int kDenseTile = 32;
+constexpr int kDenseJ = 4;  // target points per inner iteration (kDenseTile multiple)
 
 template <int DMAX>
 __global__ void __launch_bounds__(kDenseThreads) k_dense(const DenseReq* reqs) {
@@ -48,29 +49,48 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense(const DenseReq* reqs) {
       for (int k = threadIdx.x; k < nt * D; k += kDenseThreads) bf[k / D][k % D] = R.bf[t0 * D + k];
     __syncthreads();
     if (!active) continue;
-    for (int j = 0; j < nt; ++j) {
-      const double dx = px - bp[j][0], dy = py - bp[j][1], dz = pz - bp[j][2];
-      double expo = (dx * dx + dy * dy + dz * dz) * R.neg_inv_2l2;  // kernels.hpp:45-47
-      double c = 1.0;
+    // kDenseJ target points at a time: independent FP64 dependency chains
+    // (the per-pair dot products and exponent sums are serial otherwise)
+    for (int j0 = 0; j0 < nt; j0 += kDenseJ) {
+      double expo[kDenseJ], c[kDenseJ];
+#pragma unroll
+      for (int q = 0; q < kDenseJ; ++q) {
+        const int j = min(j0 + q, nt - 1);
+        const double dx = px - bp[j][0], dy = py - bp[j][1], dz = pz - bp[j][2];
+        expo[q] = (dx * dx + dy * dy + dz * dz) * R.neg_inv_2l2;  // kernels.hpp:45-47
+        c[q] = 1.0;
+      }
       if (DMAX > 0) {
         for (int k = 0; k < R.n_channels; ++k) {  // kernels.cpp:34-52
           const DenseChannel& ch = R.ch[k];
-          double s = 0.0;
+          double sq[kDenseJ];
+#pragma unroll
+          for (int q = 0; q < kDenseJ; ++q) sq[q] = 0.0;
           if (ch.linear) {
-#pragma unroll 4
-            for (int d = 0; d < ch.dim; ++d) s += su[ch.offset + d][threadIdx.x] * bf[j][ch.offset + d];
-            c *= s;
-          } else {
-#pragma unroll 4
             for (int d = 0; d < ch.dim; ++d) {
-              const double e = su[ch.offset + d][threadIdx.x] - bf[j][ch.offset + d];
-              s += e * e;
+              const double u = su[ch.offset + d][threadIdx.x];
+#pragma unroll
+              for (int q = 0; q < kDenseJ; ++q) sq[q] += u * bf[min(j0 + q, nt - 1)][ch.offset + d];
             }
-            expo += s * ch.neg_inv_2l2;
+#pragma unroll
+            for (int q = 0; q < kDenseJ; ++q) c[q] *= sq[q];
+          } else {
+            for (int d = 0; d < ch.dim; ++d) {
+              const double u = su[ch.offset + d][threadIdx.x];
+#pragma unroll
+              for (int q = 0; q < kDenseJ; ++q) {
+                const double e = u - bf[min(j0 + q, nt - 1)][ch.offset + d];
+                sq[q] += e * e;
+              }
+            }
+#pragma unroll
+            for (int q = 0; q < kDenseJ; ++q) expo[q] += sq[q] * ch.neg_inv_2l2;
           }
         }
       }
-      acc += c * exp(expo);
+#pragma unroll
+      for (int q = 0; q < kDenseJ; ++q)
+        if (j0 + q < nt) acc += c[q] * exp(expo[q]);
     }
   }
   // fixed-order block reduction
