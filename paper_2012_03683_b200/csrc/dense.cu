@@ -20,7 +20,10 @@ namespace {
 
 constexpr int kDenseThreads = 128;
 constexpr int kDenseTile = 32;
-constexpr int kDenseJ = 4;  // target points per inner iteration (kDenseTile multiple)
+#ifndef KREG_DENSE_J
+#define KREG_DENSE_J 2
+#endif
+constexpr int kDenseJ = KREG_DENSE_J;  // target points per inner iteration (divides kDenseTile)
 
 template <int DMAX>
 __global__ void __launch_bounds__(kDenseThreads) k_dense(const DenseReq* reqs) {
