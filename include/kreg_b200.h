@@ -216,6 +216,17 @@ kreg_status kreg_ctx_build_profile(const kreg_ctx* ctx, double out[9]);
  * NULL clears the hook. */
 typedef int32_t (*kreg_collective_fn)(void* user, double* sums, int32_t n_sums, double* maxes, int32_t n_maxes);
 kreg_status kreg_ctx_set_collective(kreg_ctx* ctx, kreg_collective_fn fn, void* user);
+/* Native NCCL form of the collective (no host callback): every rank creates
+ * the communicator from one ncclUniqueId (kreg_nccl_unique_id on rank 0,
+ * shared by the caller), then the round's values are combined by NCCL on the
+ * context stream. deterministic != 0: one ncclAllGather and a rank-order sum
+ * on every rank (bitwise independent of NCCL's algorithm); 0: ncclAllReduce
+ * (sum, max). world <= 0 detaches. NCCL is loaded at run time (libnccl.so.2).
+ * The deterministic gather is SURVEY.md §8(e)'s "deterministic mode". */
+kreg_status kreg_nccl_unique_id(uint8_t id[128]);
+kreg_status kreg_ctx_set_nccl(kreg_ctx* ctx, const uint8_t id[128], int32_t rank, int32_t world,
+                              int32_t deterministic);
+int64_t kreg_ctx_nccl_calls(const kreg_ctx* ctx); /* rounds combined through NCCL */
 
 /* Upload a cloud into device SoA (replaces constructing kreg::PointCloud,
  * point_cloud.cpp:49-59; same validation and messages). */

@@ -106,6 +106,10 @@ def lib():
                                                    CP, C.POINTER(_abi.kreg_sequence_result)]
         L.kreg_register_clouds_rows.argtypes = [P, P, P, C.c_int64, _abi.dptr, KP, CP, RP]
         L.kreg_ctx_set_collective.argtypes = [P, COLLECTIVE_FN, VP_]
+        L.kreg_nccl_unique_id.argtypes = [C.c_void_p]
+        L.kreg_ctx_set_nccl.argtypes = [P, C.c_void_p, C.c_int32, C.c_int32, C.c_int32]
+        L.kreg_ctx_nccl_calls.argtypes = [P]
+        L.kreg_ctx_nccl_calls.restype = C.c_int64
         L.kreg_exact_cosine.argtypes = [P, VP, VP, _abi.dptr, KP, _abi.dptr, _abi.dptr]
         L.kreg_select_points.argtypes = [P, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
                                          C.POINTER(_abi.kreg_selector_config), C.c_void_p, C.c_int64,
@@ -576,13 +580,17 @@ def register_clouds_rows(X, Z_rows, n_z_total: int, initial, params: KernelParam
     t, tp = _t12(initial)
     buf = _abi.TraceBuffers(trace_capacity or config.max_iterations)
     cfg = config.cstruct()
-    fn = collective.c_fn if collective is not None else COLLECTIVE_FN()
-    _check(lib().kreg_ctx_set_collective(ctx.h, fn, None))
+    if getattr(collective, "native", False):  # parallel.NcclCollective: NCCL inside the engine
+        collective.attach(ctx)
+    else:
+        fn = collective.c_fn if collective is not None else COLLECTIVE_FN()
+        _check(lib().kreg_ctx_set_collective(ctx.h, fn, None))
     try:
         _check(lib().kreg_register_clouds_rows(ctx.h, dx.h, dz.h, int(n_z_total), tp, params.cstruct(), C.byref(cfg),
                                                C.byref(buf.struct)))
     finally:
-        lib().kreg_ctx_set_collective(ctx.h, COLLECTIVE_FN(), None)
+        if not getattr(collective, "native", False):  # an NCCL communicator stays with its context
+            lib().kreg_ctx_set_collective(ctx.h, COLLECTIVE_FN(), None)
     return RegistrationResult.from_buffers(buf)
 
 

@@ -15,7 +15,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libkreg_b200.so")
 OBJ_DIR = os.path.join(HERE, "_build")
 
-SOURCES = ["kernels.cu", "dense.cu", "ingest.cu", "ply.cu", "engine_host.cu", "solver.cpp", "capi.cpp"]
+SOURCES = ["kernels.cu", "dense.cu", "ingest.cu", "ply.cu", "engine_host.cu", "solver.cpp", "capi.cpp", "nccl_coll.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O3", "-Xptxas", "-v",
               "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include")]
@@ -60,7 +60,7 @@ def build(verbose: bool = False, force: bool = False, defines=(), lib: str = LIB
             with open(obj + ".log", "w") as f:
                 f.write(r.stdout + r.stderr)
     if force or _stale(lib, objs):
-        cmd = [nvcc, *ARCH, "-shared", "-o", lib, *objs, "-lcudart"]
+        cmd = [nvcc, *ARCH, "-shared", "-o", lib, *objs, "-lcudart", "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)

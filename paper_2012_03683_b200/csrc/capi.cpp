@@ -701,10 +701,33 @@ kreg_status kreg_register_clouds_rows(kreg_ctx* ctx, const kreg_cloud* X, const 
 kreg_status kreg_ctx_set_collective(kreg_ctx* ctx, kreg_collective_fn fn, void* user) {
   return guarded([&] {
     require(ctx != nullptr, "NULL context");
+    nccl_detach(ctx);
     ctx->collective.fn = fn;
     ctx->collective.user = user;
   });
 }
+
+kreg_status kreg_nccl_unique_id(uint8_t id[128]) {
+  return guarded([&] {
+    require(id != nullptr, "NULL argument");
+    nccl_unique_id(id);
+  });
+}
+
+kreg_status kreg_ctx_set_nccl(kreg_ctx* ctx, const uint8_t id[128], int32_t rank, int32_t world,
+                              int32_t deterministic) {
+  return guarded([&] {
+    require(ctx != nullptr, "NULL context");
+    if (world <= 0) {
+      nccl_detach(ctx);
+      return;
+    }
+    require(id != nullptr, "NULL unique id");
+    nccl_attach(ctx, id, rank, world, deterministic != 0);
+  });
+}
+
+int64_t kreg_ctx_nccl_calls(const kreg_ctx* ctx) { return ctx ? nccl_calls(ctx) : 0; }
 
 kreg_status kreg_register_clouds_host(kreg_ctx* ctx, const kreg_cloud_view* X, const kreg_cloud_view* Z,
                                       const double initial[12], const kreg_kernel_params* params,

@@ -14,6 +14,7 @@
 #include "engine_host.hpp"
 
 kreg_ctx::~kreg_ctx() {
+  kreg_host::nccl_free(nccl);
   for (kreg_pairs* p : pool) delete p;
   pool.clear();
   for (auto*& S : rs) {

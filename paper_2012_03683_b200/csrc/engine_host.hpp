@@ -141,6 +141,14 @@ struct Collective {
   void* user = nullptr;
 };
 
+// Native NCCL collective (nccl_coll.cpp): installed as a context's collective.
+struct NcclState;
+void nccl_unique_id(unsigned char out[128]);
+void nccl_attach(kreg_ctx* ctx, const unsigned char id[128], int rank, int world, bool deterministic);
+void nccl_detach(kreg_ctx* ctx);
+void nccl_free(NcclState* s);
+long long nccl_calls(const kreg_ctx* ctx);
+
 }  // namespace kreg_host
 
 struct kreg_ctx {
@@ -205,6 +213,7 @@ struct kreg_ctx {
   // candidate-list filter on the KITTI batch)
   bool refilter = std::getenv("KREG_REFILTER") != nullptr;
   kreg_host::Collective collective;  // row-sharded registrations (kreg_ctx_set_collective)
+  kreg_host::NcclState* nccl = nullptr;  // kreg_ctx_set_nccl (owned)
   // host-side round accounting (seconds)
   long long rounds = 0;
   double t_prepare = 0.0, t_wait = 0.0, t_total = 0.0;

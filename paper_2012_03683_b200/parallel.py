@@ -18,6 +18,7 @@ Two ways the registration path shards:
 """
 from __future__ import annotations
 
+import ctypes as C
 import os
 
 import numpy as np
@@ -150,9 +151,12 @@ class TorchCollective:
         self.group = group
         self.deterministic = deterministic
         self.calls = 0
+        self.seconds = 0.0  # host wall time inside the callback (per-round collective latency)
         self.c_fn = api.COLLECTIVE_FN(self._call)
 
     def _call(self, user, sums, n_sums, maxes, n_maxes):
+        import time
+        t0 = time.perf_counter()
         try:
             import torch
             import torch.distributed as dist
@@ -180,9 +184,45 @@ class TorchCollective:
                     dist.all_reduce(t, op=op, group=self.group)
                     host[:] = t.cpu().numpy()
             self.calls += 1
+            self.seconds += time.perf_counter() - t0
             return 0
         except Exception:  # surfaced by the engine as a failed call
             return 1
+
+
+class NcclCollective:
+    """The collective as NCCL calls inside the engine (kreg_ctx_set_nccl: no
+    host callback): rank 0 creates the ncclUniqueId, torch.distributed
+    broadcasts it, and every rank's context joins one communicator on first
+    use. deterministic=True: one ncclAllGather + rank-order sums (bitwise
+    independent of NCCL's algorithm), else ncclAllReduce (sum, max)."""
+
+    native = True
+
+    def __init__(self, group=None, deterministic: bool = True):
+        import torch.distributed as dist
+        from . import api
+        self.group = group
+        self.deterministic = deterministic
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        uid = (C.c_uint8 * 128)()
+        if self.rank == 0:
+            api._check(api.lib().kreg_nccl_unique_id(uid))
+        box = [bytes(uid)]
+        dist.broadcast_object_list(box, src=0, group=group)
+        self.uid = (C.c_uint8 * 128).from_buffer_copy(box[0])
+        self._attached = set()
+
+    def attach(self, ctx):
+        from . import api
+        if id(ctx) not in self._attached:  # one communicator per context
+            api._check(api.lib().kreg_ctx_set_nccl(ctx.h, self.uid, self.rank, self.world, int(self.deterministic)))
+            self._attached.add(id(ctx))
+
+    def calls(self, ctx) -> int:
+        from . import api
+        return int(api.lib().kreg_ctx_nccl_calls(ctx.h))
 
 
 # ------------------------------------------------------------- front ends

@@ -263,7 +263,7 @@ def _sharded_worker(rank, world, port, out_dir):
         res = api.register_clouds_rows(X, Zr, Z.size(), init, p, cfg, ctx=c, collective=coll)
         np.savez(os.path.join(out_dir, f"r{rank}.npz"), T=res.transform.as12(), obj=res.objective_trace,
                  it=res.iterations, pc=res.pair_count_trace, step=res.step_trace, rb=res.rebuild_trace,
-                 ls=res.lengthscale_trace, calls=coll.calls, launches=c.kernel_launches())
+                 ls=res.lengthscale_trace, calls=coll.calls, launches=c.kernel_launches(), coll_s=coll.seconds)
     finally:
         dist.destroy_process_group()
 
@@ -278,6 +278,8 @@ def test_row_sharded_two_ranks_on_device(ctx):
     with tempfile.TemporaryDirectory() as d:
         mp.spawn(_sharded_worker, args=(2, _free_port(), d), nprocs=2, join=True)
         got = [np.load(os.path.join(d, f"r{r}.npz")) for r in range(2)]
+    print(f"row-sharded 2 ranks (gloo): {int(got[0]['calls'])} collective calls, "
+          f"{1e6 * float(got[0]['coll_s']) / max(1, int(got[0]['calls'])):.0f} us per call (rank 0)")
     for g in got:
         assert int(g["calls"]) > 0 and int(g["launches"]) > 0
         assert np.array_equal(g["T"], got[0]["T"]) and np.array_equal(g["obj"], got[0]["obj"])
@@ -346,3 +348,40 @@ def test_sequence_host_matches_device_frames(ctx):
         assert np.array_equal(a.fallback, b.fallback)
         for x, y in zip(a.relative, b.relative):
             assert np.array_equal(x.as12(), y.as12())
+
+
+def _nccl_worker(rank, world, port, out_dir):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        X, Z, init, p, cfg = _sharded_case()
+        c = api.Context(0)
+        for det in (True, False):
+            coll = parallel.NcclCollective(deterministic=det)
+            res = api.register_clouds_rows(X, Z, Z.size(), init, p, cfg, ctx=c, collective=coll)
+            np.savez(os.path.join(out_dir, f"r{rank}_{int(det)}.npz"), T=res.transform.as12(), obj=res.objective_trace,
+                     it=res.iterations, calls=coll.calls(c))
+            api.lib().kreg_ctx_set_nccl(c.h, None, 0, 0, 0)  # detach before the next communicator
+    finally:
+        dist.destroy_process_group()
+
+
+def test_native_nccl_collective_world_one(ctx):
+    """The in-engine NCCL collective (kreg_ctx_set_nccl, no host callback) on
+    the one GPU available: a one-rank communicator must reproduce the
+    unsharded registration bit for bit in both modes (all_gather + rank-order
+    sum, and all_reduce), and combine every round through NCCL."""
+    import torch.multiprocessing as mp
+    X, Z, init, p, cfg = _sharded_case()
+    want = api.register_clouds(X, Z, init, p, cfg)
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_nccl_worker, args=(1, _free_port(), d), nprocs=1, join=True)
+        for det in (1, 0):
+            g = np.load(os.path.join(d, f"r0_{det}.npz"))
+            assert int(g["calls"]) > 0
+            assert int(g["it"]) == want.iterations
+            assert np.array_equal(g["obj"], want.objective_trace)
+            assert np.array_equal(g["T"], want.transform.as12())
