@@ -190,6 +190,7 @@ struct alignas(16) SweepReq {
   const int4* slots;
   long long capacity;    // slot capacity (an overflowed build is skipped)
   int grad;              // 0: F (+ displacement) only, 1: F + gradient
+  int no_disp;           // 1: no displacement items (the host's bound decides, EvalJob::disp_limit)
   int second;            // 1 (M = 1, grad): also dF/d eps, d2F/d eps2 along exp(eps xi) T -> out[kOut .. kOut + 1]
   float dir[6];          // xi = {omega, omega x anchor + v} (second-order requests)
   int chunk_pref;        // the list's sweep chunking (chunk_units)

@@ -648,6 +648,36 @@ static void prepare_sweep(EvalJob& job, kreg_dev::SweepReq& R, double* partials,
   R.slots = p->slot_buf.ptr;
   R.capacity = static_cast<long long>(p->slot_buf.cap);
   R.grad = job.grad || job.second ? 1 : 0;
+  // analytic displacement bound: |(R_m - R_b) z + (t_m - t_b)| <= ||R_m - R_b||_F h + |(R_m - R_b) c + (t_m - t_b)|
+  // for z in Z's bounding box (centre c, half-diagonal h)
+  job.no_disp = false;
+  if (job.disp_limit > 0.0) {
+    const kreg_cloud* Zc = p->Z;
+    double c[3], h2 = 0.0;
+    for (int k = 0; k < 3; ++k) {
+      c[k] = 0.5 * (Zc->lo[k] + Zc->hi[k]);
+      h2 += 0.25 * (Zc->hi[k] - Zc->lo[k]) * (Zc->hi[k] - Zc->lo[k]);
+    }
+    const double h = std::sqrt(h2);
+    bool all = true;
+    for (int m = 0; m < job.M && all; ++m) {
+      double fro = 0.0, off2 = 0.0;
+      for (int r = 0; r < 3; ++r) {
+        double o = job.T[m][4 * r + 3] - p->T_build[4 * r + 3];
+        for (int k = 0; k < 3; ++k) {
+          const double d = job.T[m][4 * r + k] - p->T_build[4 * r + k];
+          fro += d * d;
+          o += d * c[k];
+        }
+        off2 += o * o;
+      }
+      const double b = (std::sqrt(fro) * h + std::sqrt(off2)) * (1.0 + 1e-9) + 1e-300;
+      job.disp_bound[m] = b;
+      all = b <= job.disp_limit;
+    }
+    job.no_disp = all;
+  }
+  R.no_disp = job.no_disp ? 1 : 0;
   R.second = job.second ? 1 : 0;
   if (job.second) {  // u_j = omega x T z_j + v = omega x (arm_j) + (omega x anchor + v)
     const double* w = job.dir;
@@ -926,6 +956,8 @@ void end_round(kreg_ctx* ctx, RoundSlot& S) {
   for (int e = 0; e < ne; ++e) {
     std::memcpy(evals[e].out, res + static_cast<size_t>(e) * kreg_dev::kMaxCandidates * kreg_dev::kOut,
                 sizeof(double) * (kreg_dev::kOut * evals[e].M + (evals[e].second ? 2 : 0)));
+    if (evals[e].no_disp)  // the bound stands in for the maximum (EvalJob::disp_limit)
+      for (int m = 0; m < evals[e].M; ++m) evals[e].out[m * kreg_dev::kOut + 7] = evals[e].disp_bound[m];
     ctx->pair_evals += evals[e].pairs->P * evals[e].M;
     round_pairs += evals[e].pairs->P;
     round_slots += evals[e].pairs->slots;

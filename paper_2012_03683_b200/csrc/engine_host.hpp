@@ -369,6 +369,14 @@ struct EvalJob {
   double* out;         // host, M x 8 {F, omega, v, disp}; filled after run_round
   bool grad = true;    // false: F + displacement only (gradient left zero)
   bool second = false; // M = 1: also {dF/d eps, d2F/d eps2} along exp(eps dir) T in out[8..9]
+  // > 0: the caller only needs max_j |T_m z_j - T_build z_j| up to this value
+  // (solver: the rebuild and reuse thresholds). When an analytic upper bound
+  // of every candidate's displacement (bbox of Z) is below it, the sweep runs
+  // no displacement items and out[7] receives the bound; the caller's
+  // decisions are the same as with the exact maximum.
+  double disp_limit = -1.0;
+  bool no_disp = false;
+  double disp_bound[kreg_dev::kMaxCandidates] = {};
   double dir[6] = {0, 0, 0, 0, 0, 0};
 };
 

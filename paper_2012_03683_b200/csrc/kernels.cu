@@ -1058,7 +1058,9 @@ struct SweepWarp {
   unsigned consumed, rec_used;
 };
 
-__device__ __forceinline__ int disp_items(const SweepReq& R) { return (R.n_z + kDispItem - 1) / kDispItem; }
+__device__ __forceinline__ int disp_items(const SweepReq& R) {
+  return R.no_disp ? 0 : (R.n_z + kDispItem - 1) / kDispItem;
+}
 
 __device__ __forceinline__ int locate_item(const SweepWarp& w, int g) {
   int lo = 0, hi = w.n_req - 1;
@@ -1602,7 +1604,8 @@ void sweep_batched(const SweepReq* h, const SweepReq* d, int n, int sm_count, un
     for (int r = r0; r < r1; ++r) {
       if (h[r].grad) max_mg = max(max_mg, h[r].M);
       if (h[r].second) max_mg = max(max_mg, 3);  // NPG = 2 instantiation
-      items += h[r].units >= 0 ? chunk_count(h[r].units, h[r].chunk_pref) + (h[r].n_z + kDispItem - 1) / kDispItem
+      items += h[r].units >= 0 ? chunk_count(h[r].units, h[r].chunk_pref) +
+                                     (h[r].no_disp ? 0 : (h[r].n_z + kDispItem - 1) / kDispItem)
                                : (1LL << 40);
     }
     const int grid = (int)max(1LL, min((long long)kSweepCtasPerSm * sm_count, (items + kSweepWarps - 1) / kSweepWarps));

@@ -259,6 +259,25 @@ void end_iteration(Reg& r, bool searched, bool accepted, int backtracks, double 
   r.phase = Phase::kStartIter;
 }
 
+// The displacement max_j |T z_j - T_build z_j| the loop's decisions need
+// (EvalJob::disp_limit): the rebuild rule compares it with 0.5 cutoff
+// (registration.cpp:123-128), the next build's candidate-list reuse with
+// R_s - 2 margin - sup_disp - cutoff_next (prepare_build), cutoff_next in
+// {cutoff, decay x cutoff} (one anneal step at most). Any value at or below
+// the returned limit leads to the same decisions as the exact maximum.
+double disp_limit(const Reg& r) {
+  const kreg_pairs* p = r.pairs.get();
+  double lim = 0.5 * p->cutoff_radius;
+  if (p->sup_valid) {
+    const double base = p->sup_radius - 2e-9 * p->sup_radius - p->sup_disp;
+    for (const double cut : {p->cutoff_radius, p->cutoff_radius * r.cfg.decay_factor}) {
+      const double b = base - cut;
+      if (b >= 0.0) lim = std::min(lim, b);
+    }
+  }
+  return lim * (1.0 - 1e-12);
+}
+
 void schedule_build_eval(Reg& r, std::vector<BuildJob>& builds, std::vector<EvalJob>& evals,
                          std::vector<Reg*>& eval_owner) {
   BuildJob b;
@@ -280,6 +299,7 @@ void schedule_build_eval(Reg& r, std::vector<BuildJob>& builds, std::vector<Eval
   e.lengthscale = r.lengthscale;
   e.sigma = r.wp.sigma;
   e.out = r.ev;
+  e.disp_limit = disp_limit(r);
   evals.push_back(e);
   eval_owner.push_back(&r);
   r.memo.clear();
@@ -333,6 +353,7 @@ void plan(Reg& r, std::vector<BuildJob>& builds, std::vector<EvalJob>& evals, st
           e.lengthscale = r.lengthscale;
           e.sigma = r.wp.sigma;
           e.out = r.ev;
+          e.disp_limit = disp_limit(r);
           evals.push_back(e);
           owners.push_back(&r);
           ++r.sweeps;
@@ -418,6 +439,7 @@ void plan(Reg& r, std::vector<BuildJob>& builds, std::vector<EvalJob>& evals, st
           e.lengthscale = r.lengthscale;
           e.sigma = r.wp.sigma;
           e.out = &r.cand_out[b][0];
+          e.disp_limit = disp_limit(r);
           e.grad = r.cand_grad;
           evals.push_back(e);
           owners.push_back(&r);

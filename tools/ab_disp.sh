@@ -1,0 +1,6 @@
+# A/B: analytic displacement screen (no displacement items when the bbox bound
+# decides the rebuild / reuse tests) vs the previous build
+for v in prev base prev base; do
+  if [ "$v" = "base" ]; then lib=""; else lib="paper_2012_03683_b200/_variants/$v.so"; fi
+  echo "== $v"; KREG_LIB=$lib STEPS=3 timeout 300 python tools/ab_step.py 2>&1 | grep "profiling=False"
+done
