@@ -222,7 +222,25 @@ void cloud_stage(const kreg_cloud_view* v, kreg_cloud* c, double* sx, double* sy
     }
     keys[static_cast<size_t>(i)] = {m, i};
   }
-  std::sort(keys.begin(), keys.end());
+  // stable LSD radix sort on the 63-bit key (6 passes of 11 bits): the order
+  // of std::sort on (key, index) pairs, in O(n)
+  {
+    std::vector<std::pair<uint64_t, int>> tmp(keys.size());
+    std::vector<uint32_t> hist(2048);
+    for (int pass = 0; pass < 6; ++pass) {
+      const int sh = 11 * pass;
+      std::fill(hist.begin(), hist.end(), 0u);
+      for (const auto& kv : keys) ++hist[(kv.first >> sh) & 2047u];
+      uint32_t run = 0;
+      for (uint32_t& h : hist) {
+        const uint32_t c = h;
+        h = run;
+        run += c;
+      }
+      for (const auto& kv : keys) tmp[hist[(kv.first >> sh) & 2047u]++] = kv;
+      keys.swap(tmp);
+    }
+  }
   c->order.resize(static_cast<size_t>(n));
   c->rank.resize(static_cast<size_t>(n));
   std::vector<int> src_off;
