@@ -159,6 +159,13 @@ int64_t kreg_ctx_kernel_launches(const kreg_ctx* ctx);
 kreg_status kreg_ctx_sweep_stats(const kreg_ctx* ctx, double* sweep_ms, int64_t* sweep_launches,
                                  int64_t* pair_evals);
 kreg_status kreg_ctx_set_profiling(kreg_ctx* ctx, int32_t enabled);
+/* Device-side timing of a region on the context's stream (CUDA events):
+ * mark(0) records the start event, mark(1) the stop event; elapsed returns
+ * the milliseconds between them (synchronises on the stop event). Work the
+ * context issues from other streams (two-group rounds) is ordered before
+ * the stop mark by the calls that issued it (they complete before returning). */
+kreg_status kreg_ctx_timer_mark(kreg_ctx* ctx, int32_t which);
+kreg_status kreg_ctx_timer_elapsed(kreg_ctx* ctx, double* ms);
 /* Throughput mode: at most `n` registrations in flight at once (0 = all);
  * a finished registration is replaced by the next one immediately. */
 kreg_status kreg_ctx_set_max_active(kreg_ctx* ctx, int32_t n);

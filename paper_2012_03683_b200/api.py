@@ -58,6 +58,8 @@ def lib():
         L.kreg_ctx_kernel_launches.restype = C.c_int64
         L.kreg_ctx_sweep_stats.argtypes = [P, _abi.dptr, _abi.i64ptr, _abi.i64ptr]
         L.kreg_ctx_set_profiling.argtypes = [P, C.c_int32]
+        L.kreg_ctx_timer_mark.argtypes = [P, C.c_int32]
+        L.kreg_ctx_timer_elapsed.argtypes = [P, _abi.dptr]
         L.kreg_ctx_set_max_active.argtypes = [P, C.c_int32]
         L.kreg_ctx_host_stats.argtypes = [P, _abi.dptr]
         L.kreg_ctx_stats.argtypes = [P, _abi.dptr]
@@ -166,6 +168,16 @@ class Context:
 
     def set_profiling(self, on: bool):
         _check(lib().kreg_ctx_set_profiling(self.h, int(on)))
+
+    def timer_mark(self, which: int):
+        """Record the start (0) / stop (1) CUDA event on the context's stream."""
+        _check(lib().kreg_ctx_timer_mark(self.h, int(which)))
+
+    def timer_ms(self) -> float:
+        """Device milliseconds between the start and stop marks."""
+        v = C.c_double()
+        _check(lib().kreg_ctx_timer_elapsed(self.h, C.byref(v)))
+        return v.value
 
     def reset_stats(self):
         _check(lib().kreg_ctx_reset_stats(self.h))

@@ -707,6 +707,25 @@ kreg_status kreg_ctx_set_collective(kreg_ctx* ctx, kreg_collective_fn fn, void* 
   });
 }
 
+kreg_status kreg_ctx_timer_mark(kreg_ctx* ctx, int32_t which) {
+  return guarded([&] {
+    require(ctx != nullptr && (which == 0 || which == 1), "timer_mark: NULL context or bad mark");
+    KREG_CUDA(cudaSetDevice(ctx->device));
+    if (!ctx->timer[which]) KREG_CUDA(cudaEventCreate(&ctx->timer[which]));
+    KREG_CUDA(cudaEventRecord(ctx->timer[which], ctx->stream));
+  });
+}
+
+kreg_status kreg_ctx_timer_elapsed(kreg_ctx* ctx, double* ms) {
+  return guarded([&] {
+    require(ctx != nullptr && ms != nullptr && ctx->timer[0] && ctx->timer[1], "timer_elapsed: marks missing");
+    KREG_CUDA(cudaEventSynchronize(ctx->timer[1]));
+    float f = 0.0f;
+    KREG_CUDA(cudaEventElapsedTime(&f, ctx->timer[0], ctx->timer[1]));
+    *ms = static_cast<double>(f);
+  });
+}
+
 kreg_status kreg_nccl_unique_id(uint8_t id[128]) {
   return guarded([&] {
     require(id != nullptr, "NULL argument");

@@ -15,6 +15,8 @@
 
 kreg_ctx::~kreg_ctx() {
   kreg_host::nccl_free(nccl);
+  for (cudaEvent_t& e : timer)
+    if (e) cudaEventDestroy(e);
   for (kreg_pairs* p : pool) delete p;
   pool.clear();
   for (auto*& S : rs) {

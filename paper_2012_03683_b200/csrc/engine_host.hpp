@@ -214,6 +214,7 @@ struct kreg_ctx {
   bool refilter = std::getenv("KREG_REFILTER") != nullptr;
   kreg_host::Collective collective;  // row-sharded registrations (kreg_ctx_set_collective)
   kreg_host::NcclState* nccl = nullptr;  // kreg_ctx_set_nccl (owned)
+  cudaEvent_t timer[2] = {nullptr, nullptr};  // kreg_ctx_timer_mark / _elapsed
   // host-side round accounting (seconds)
   long long rounds = 0;
   double t_prepare = 0.0, t_wait = 0.0, t_total = 0.0;
