@@ -165,6 +165,10 @@ kreg_status kreg_ctx_set_profiling(kreg_ctx* ctx, int32_t enabled);
  * context issues from other streams (two-group rounds) is ordered before
  * the stop mark by the calls that issued it (they complete before returning). */
 kreg_status kreg_ctx_timer_mark(kreg_ctx* ctx, int32_t which);
+/* Displacement screen of the solver's sweeps: {requests that only needed the
+ * displacement up to a decision threshold, requests whose displacement came
+ * from the analytic bound (no FP64 displacement pass)} since the last reset. */
+kreg_status kreg_ctx_screen_stats(const kreg_ctx* ctx, int64_t out[2]);
 kreg_status kreg_ctx_timer_elapsed(kreg_ctx* ctx, double* ms);
 /* Throughput mode: at most `n` registrations in flight at once (0 = all);
  * a finished registration is replaced by the next one immediately. */

@@ -59,6 +59,7 @@ def lib():
         L.kreg_ctx_sweep_stats.argtypes = [P, _abi.dptr, _abi.i64ptr, _abi.i64ptr]
         L.kreg_ctx_set_profiling.argtypes = [P, C.c_int32]
         L.kreg_ctx_timer_mark.argtypes = [P, C.c_int32]
+        L.kreg_ctx_screen_stats.argtypes = [P, _abi.i64ptr]
         L.kreg_ctx_timer_elapsed.argtypes = [P, _abi.dptr]
         L.kreg_ctx_set_max_active.argtypes = [P, C.c_int32]
         L.kreg_ctx_host_stats.argtypes = [P, _abi.dptr]
@@ -168,6 +169,12 @@ class Context:
 
     def set_profiling(self, on: bool):
         _check(lib().kreg_ctx_set_profiling(self.h, int(on)))
+
+    def screen_stats(self) -> dict:
+        """Displacement screen: sweep requests asked / answered by the bound."""
+        out = np.zeros(2, dtype=np.int64)
+        _check(lib().kreg_ctx_screen_stats(self.h, _abi.as_ptr(out, C.c_int64)))
+        return {"asked": int(out[0]), "screened": int(out[1])}
 
     def timer_mark(self, which: int):
         """Record the start (0) / stop (1) CUDA event on the context's stream."""

@@ -323,6 +323,14 @@ kreg_status kreg_ctx_stats(const kreg_ctx* ctx, double out[8]) {
   });
 }
 
+kreg_status kreg_ctx_screen_stats(const kreg_ctx* ctx, int64_t out[2]) {
+  return guarded([&] {
+    require(ctx != nullptr && out != nullptr, "NULL argument");
+    out[0] = ctx->disp_asked;
+    out[1] = ctx->disp_screened;
+  });
+}
+
 kreg_status kreg_ctx_io_stats(const kreg_ctx* ctx, int64_t out[2]) {
   return guarded([&] {
     require(ctx != nullptr && out != nullptr, "NULL argument");
@@ -376,6 +384,7 @@ kreg_status kreg_ctx_reset_stats(kreg_ctx* ctx) {
     ctx->full_builds = ctx->filter_builds = 0;
     ctx->build_ms = 0.0;
     ctx->build_rounds = ctx->filter_entries = ctx->built_slots = 0;
+    ctx->disp_asked = ctx->disp_screened = 0;
     for (long long& w : ctx->full_why) w = 0;
     ctx->refilter_builds = 0;
   });

@@ -696,6 +696,10 @@ static void prepare_sweep(EvalJob& job, kreg_dev::SweepReq& R, double* partials,
       all = b <= job.disp_limit;
     }
     job.no_disp = all;
+    if (p->ctx) {
+      ++p->ctx->disp_asked;
+      if (all) ++p->ctx->disp_screened;
+    }
   }
   R.no_disp = job.no_disp ? 1 : 0;
   R.second = job.second ? 1 : 0;

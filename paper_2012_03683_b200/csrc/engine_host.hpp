@@ -215,6 +215,9 @@ struct kreg_ctx {
   kreg_host::Collective collective;  // row-sharded registrations (kreg_ctx_set_collective)
   kreg_host::NcclState* nccl = nullptr;  // kreg_ctx_set_nccl (owned)
   cudaEvent_t timer[2] = {nullptr, nullptr};  // kreg_ctx_timer_mark / _elapsed
+  // displacement screen (EvalJob::disp_limit): sweep requests that asked for
+  // it, and those whose displacement came from the analytic bound
+  long long disp_asked = 0, disp_screened = 0;
   // host-side round accounting (seconds)
   long long rounds = 0;
   double t_prepare = 0.0, t_wait = 0.0, t_total = 0.0;
