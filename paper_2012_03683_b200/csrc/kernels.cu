@@ -825,7 +825,9 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 //    the partials in a fixed shuffle-tree order: bitwise reproducible,
 //    independent of scheduling and batch composition.
 //  * max_j |T_m z_j - T_b z_j| (inner_product.cpp:238-246) comes from the
-//    launch's displacement work items in FP64 over the original coordinates.
+//    launch's displacement work items in FP64 over the original coordinates,
+//    except for requests the host answered with an analytic bound
+//    (SweepReq::no_disp, engine_host.cu prepare_sweep).
 __device__ __forceinline__ long long request_units(const SweepReq& R) {
   // an overflowed build is skipped (its result is discarded by the host); the
   // unit count is passed by the host when the pair list was built earlier
