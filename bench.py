@@ -432,9 +432,9 @@ def main():
         api.register_batch(dev_X, dev_Z, inits, params, cfg, ctx=ctx)
     ctx.synchronize()
 
-    # ---- device-resident timed region: K steps
+    # ---- device-resident timed region: K steps (the engine's default: the
+    # batch's rounds alternate between two groups on two streams)
     ctx.reset_stats()
-    ctx.set_profiling(True)
     clocks = ClockSampler(local)
     clocks.start()
     barrier(world)
@@ -453,13 +453,32 @@ def main():
     wall = time.perf_counter() - t0
     dt = ctx.timer_ms() * 1e-3
     clk = clocks.stop()
-    ctx.set_profiling(False)
-    sweep = ctx.sweep_stats()
     host = ctx.host_stats()
     launches = ctx.kernel_launches()
     dt_max = max_over_ranks(dt, world)
     total = sum_over_ranks(B * args.steps, world)
     value = total / dt_max
+
+    # ---- kernel roofline: one more step with the rounds on ONE stream and
+    # per-launch CUDA events (with two streams a launch's events would also
+    # span the other stream's concurrent kernels); not part of `value`
+    prev_groups = os.environ.get("KREG_GROUPS")
+    os.environ["KREG_GROUPS"] = "1"
+    try:
+        ctx.reset_stats()
+        ctx.set_profiling(True)
+        ctx.timer_mark(0)
+        api.register_batch(dev_X, dev_Z, inits, params, cfg, ctx=ctx)
+        ctx.timer_mark(1)
+        ctx.synchronize()
+        dt_prof = ctx.timer_ms() * 1e-3
+        ctx.set_profiling(False)
+        sweep = ctx.sweep_stats()
+    finally:
+        if prev_groups is None:
+            del os.environ["KREG_GROUPS"]
+        else:
+            os.environ["KREG_GROUPS"] = prev_groups
 
     # ---- end to end through the public API with host buffers (one untimed
     # call first: it sizes the pinned staging and the device cloud arena)
@@ -506,7 +525,9 @@ def main():
                 "kernel": "k_sweep (fused F + SE(3) gradient + displacement)",
                 "algorithmic_bytes_per_pair": 8,
                 "pair_evals_per_s": sweep["pair_evals"] / (sweep["sweep_ms"] * 1e-3) if sweep["sweep_ms"] else 0.0,
-                "sweep_share_of_step": sweep["sweep_ms"] * 1e-3 / dt,
+                "sweep_share_of_step": sweep["sweep_ms"] * 1e-3 / dt_prof,
+                "measured_in": "one extra step after the timed region with the rounds on one stream (per-launch "
+                               "CUDA events around the sweep launches on that stream)",
                 **issue_fractions(sweep, clk),
                 "peak_source": "MEASURED_PEAKS.json" if "hbm_gbs" in peaks else "fallback"}
 

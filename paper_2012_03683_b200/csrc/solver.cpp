@@ -611,7 +611,7 @@ void register_many(kreg_ctx* ctx, std::vector<RegJob>& jobs, const Collective* c
   // do not depend on the window or the grouping: every sweep request is
   // evaluated independently of what else shares its launch.
   const size_t window = ctx && ctx->max_active > 0 ? static_cast<size_t>(ctx->max_active) : regs.size();
-  const int n_groups = ctx && window >= 2 && env_int("KREG_GROUPS", 1) >= 2 ? 2 : 1;
+  const int n_groups = ctx && window >= 2 && env_int("KREG_GROUPS", 2) >= 2 ? 2 : 1;
   size_t started = 0;
   struct Group {
     std::vector<Reg*> active;
@@ -620,7 +620,9 @@ void register_many(kreg_ctx* ctx, std::vector<RegJob>& jobs, const Collective* c
     bool pending = false;  // a round of this group is in flight
   };
   Group groups[2];
-  for (int g = 0; g < n_groups; ++g) groups[g].slot = round_slot(ctx, g);
+  // two groups: each on its own stream (slots 3 and 1), so their rounds
+  // overlap on the device; both order after the context stream's uploads
+  for (int g = 0; g < n_groups; ++g) groups[g].slot = round_slot(ctx, n_groups == 2 ? (g == 0 ? 3 : 1) : 0);
   const size_t per_group = (window + n_groups - 1) / n_groups;
 
   // Memory-aware admission: a registration starts only when the device has
