@@ -785,7 +785,7 @@ RoundSlot* round_slot(kreg_ctx* ctx, int i) {
     KREG_CUDA(cudaEventCreate(&S->evb0));
     KREG_CUDA(cudaEventCreate(&S->evb1));
     S->stream = ctx->stream;
-    if (i == 1 || i == 3) {
+    if (i == 1 || i >= 3) {
       KREG_CUDA(cudaStreamCreateWithFlags(&S->stream, cudaStreamNonBlocking));
       KREG_CUDA(cudaEventCreateWithFlags(&S->ordered, cudaEventDisableTiming));
       S->own_stream = true;

@@ -166,8 +166,8 @@ struct kreg_ctx {
   // round staging: slots 0 and 1 alternate in the batched solver (one round
   // in flight on the device while the host plans the other), slot 2 serves
   // the synchronous calls
-  // (slot 3: group 0 of a two-group batch, on its own stream like slot 1)
-  kreg_host::RoundSlot* rs[4] = {nullptr, nullptr, nullptr, nullptr};
+  // (slots 3-5: groups 0, 2, 3 of a multi-group batch, on their own streams like slot 1)
+  kreg_host::RoundSlot* rs[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   kreg_host::DevBuf<double> d_T2;
   kreg_host::DevBuf<unsigned long long> d_disp;
   // end-to-end calls: pinned host staging and device arena of their clouds

@@ -611,7 +611,10 @@ void register_many(kreg_ctx* ctx, std::vector<RegJob>& jobs, const Collective* c
   // do not depend on the window or the grouping: every sweep request is
   // evaluated independently of what else shares its launch.
   const size_t window = ctx && ctx->max_active > 0 ? static_cast<size_t>(ctx->max_active) : regs.size();
-  const int n_groups = ctx && window >= 2 && env_int("KREG_GROUPS", 2) >= 2 ? 2 : 1;
+  constexpr int kMaxGroups = 4;
+  const int n_groups =
+      ctx ? static_cast<int>(std::min<size_t>(window, static_cast<size_t>(std::clamp(env_int("KREG_GROUPS", 2), 1, kMaxGroups))))
+          : 1;
   size_t started = 0;
   struct Group {
     std::vector<Reg*> active;
@@ -619,10 +622,13 @@ void register_many(kreg_ctx* ctx, std::vector<RegJob>& jobs, const Collective* c
     RoundSlot* slot = nullptr;
     bool pending = false;  // a round of this group is in flight
   };
-  Group groups[2];
+  Group groups[kMaxGroups];
   // two groups: each on its own stream (slots 3 and 1), so their rounds
   // overlap on the device; both order after the context stream's uploads
-  for (int g = 0; g < n_groups; ++g) groups[g].slot = round_slot(ctx, n_groups == 2 ? (g == 0 ? 3 : 1) : 0);
+  // several groups: each on its own stream (round slots 3, 1, 4, 5), so
+  // their rounds overlap on the device; all order after the context stream's
+  // uploads. One group runs on the context stream (slot 0).
+  for (int g = 0; g < n_groups; ++g) groups[g].slot = round_slot(ctx, n_groups == 1 ? 0 : (g == 0 ? 3 : g == 1 ? 1 : g + 2));
   const size_t per_group = (window + n_groups - 1) / n_groups;
 
   // Memory-aware admission: a registration starts only when the device has
@@ -749,8 +755,14 @@ void register_many(kreg_ctx* ctx, std::vector<RegJob>& jobs, const Collective* c
       // every active registration finished without device work: refill
     }
   };
-  bool live[2] = {true, n_groups > 1};
-  while (live[0] || live[1]) {
+  bool live[kMaxGroups];
+  for (int g = 0; g < kMaxGroups; ++g) live[g] = g < n_groups;
+  auto any_live = [&] {
+    for (int g = 0; g < n_groups; ++g)
+      if (live[g]) return true;
+    return false;
+  };
+  while (any_live()) {
     for (int g = 0; g < n_groups; ++g)
       if (live[g]) live[g] = step(groups[g]);
   }
