@@ -613,7 +613,8 @@ void register_many(kreg_ctx* ctx, std::vector<RegJob>& jobs, const Collective* c
   const size_t window = ctx && ctx->max_active > 0 ? static_cast<size_t>(ctx->max_active) : regs.size();
   constexpr int kMaxGroups = 4;
   const int n_groups =
-      ctx ? static_cast<int>(std::min<size_t>(window, static_cast<size_t>(std::clamp(env_int("KREG_GROUPS", 2), 1, kMaxGroups))))
+      ctx ? std::max(1, static_cast<int>(std::min<size_t>(
+                            window, static_cast<size_t>(std::clamp(env_int("KREG_GROUPS", 2), 1, kMaxGroups)))))
           : 1;
   size_t started = 0;
   struct Group {
