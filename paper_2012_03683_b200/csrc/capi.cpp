@@ -851,11 +851,6 @@ kreg_status kreg_register_sequence_host(kreg_ctx* ctx, const kreg_cloud_view* fr
     require(ctx && frames && params && config && result && n_chains >= 1, "invalid argument");
     std::vector<const kreg_cloud_view*> views;
     for (int k = 0; k < n_frames; ++k) views.push_back(&frames[k]);
-    // frames are staged and uploaded on worker threads in order while the
-    // first pairs already run
-    std::unique_ptr<AsyncUpload> up = cloud_upload_async(ctx, views.data(), n_frames, 1);
-    std::vector<const kreg_cloud*> fr;
-    for (auto& c : up->clouds) fr.push_back(c.get());
     const int m = n_frames - 1;
     const int nc = std::min(n_chains, m);
     std::vector<int> b, e;
@@ -863,6 +858,29 @@ kreg_status kreg_register_sequence_host(kreg_ctx* ctx, const kreg_cloud_view* fr
       b.push_back(static_cast<int>(static_cast<long long>(m) * c / nc));
       e.push_back(static_cast<int>(static_cast<long long>(m) * (c + 1) / nc));
     }
+    // frames are staged and uploaded on worker threads while the first pairs
+    // already run, interleaved across the chains (frame k of every chain,
+    // then k + 1, ...) so that every chain can start at once
+    std::vector<int> order;
+    std::vector<char> seen(static_cast<size_t>(n_frames), 0);
+    for (int k = 0;; ++k) {
+      bool any = false;
+      for (int c = 0; c < nc; ++c) {
+        const int f = b[c] + k;
+        if (f > e[c]) continue;  // chain c covers frames b_c .. e_c
+        any = true;
+        if (!seen[static_cast<size_t>(f)]) {
+          seen[static_cast<size_t>(f)] = 1;
+          order.push_back(f);
+        }
+      }
+      if (!any) break;
+    }
+    for (int f = 0; f < n_frames; ++f)
+      if (!seen[static_cast<size_t>(f)]) order.push_back(f);
+    std::unique_ptr<AsyncUpload> up = cloud_upload_async(ctx, views.data(), n_frames, 1, std::move(order));
+    std::vector<const kreg_cloud*> fr;
+    for (auto& c : up->clouds) fr.push_back(c.get());
     try {
       run_chains(ctx, fr.data(), n_frames, b, e, to_params(params), *config, result, up->ready.data());
     } catch (...) {

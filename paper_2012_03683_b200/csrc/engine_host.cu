@@ -379,7 +379,12 @@ AsyncUpload::~AsyncUpload() {
 }
 
 std::unique_ptr<AsyncUpload> cloud_upload_async(kreg_ctx* ctx, const kreg_cloud_view* const* views, int n_jobs,
-                                                int per_unit) {
+                                                int per_unit, std::vector<int> order) {
+  if (order.size() != static_cast<size_t>(n_jobs)) {
+    order.resize(static_cast<size_t>(n_jobs));
+    for (int j = 0; j < n_jobs; ++j) order[static_cast<size_t>(j)] = j;
+  }
+  auto ord = std::make_shared<std::vector<int>>(std::move(order));
   auto up = std::make_unique<AsyncUpload>();
   const int n = per_unit * n_jobs;
   up->clouds.resize(static_cast<size_t>(n));
@@ -408,11 +413,12 @@ std::unique_ptr<AsyncUpload> cloud_upload_async(kreg_ctx* ctx, const kreg_cloud_
   auto next = std::make_shared<std::atomic<int>>(0);
   AsyncUpload* U = up.get();
   const int device = ctx->device;
-  auto work = [U, ctx, views, doff, foff, woff, next, n_jobs, per_unit, device]() {
+  auto work = [U, ctx, views, doff, foff, woff, next, n_jobs, per_unit, device, ord]() {
     cudaSetDevice(device);
     for (;;) {
-      const int job = next->fetch_add(1);
-      if (job >= n_jobs) return;
+      const int pos = next->fetch_add(1);
+      if (pos >= n_jobs) return;
+      const int job = (*ord)[static_cast<size_t>(pos)];
       try {
         for (int h = 0; h < per_unit; ++h) {
           const int k = per_unit * job + h;

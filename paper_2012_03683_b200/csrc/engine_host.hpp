@@ -338,9 +338,10 @@ struct AsyncUpload {
   ~AsyncUpload();
 };
 // `per_unit` consecutive clouds form one unit with one ready flag (2: a
-// batch job's X and Z; 1: a sequence frame)
+// batch job's X and Z; 1: a sequence frame); `order` (optional, n_units
+// entries) is the order in which the workers stage the units
 std::unique_ptr<AsyncUpload> cloud_upload_async(kreg_ctx* ctx, const kreg_cloud_view* const* views, int n_units,
-                                                int per_unit = 2);
+                                                int per_unit = 2, std::vector<int> order = {});
 
 // Many clouds: host staging on worker threads, device copies into a context
 // arena (valid until the next call of this function on the context).
