@@ -132,7 +132,8 @@ void fill_sequence(const std::vector<double>& rel, const std::vector<uint8_t>& f
 // reference's register_sequence).
 void run_chains(kreg_ctx* ctx, const kreg_cloud* const* frames, int n_frames, const std::vector<int>& begins,
                 const std::vector<int>& ends, const Params& params, const kreg_registration_config& config,
-                kreg_sequence_result* out, const std::atomic<int>* frame_ready = nullptr) {
+                kreg_sequence_result* out, const std::atomic<int>* frame_ready = nullptr,
+                const cudaEvent_t* frame_done = nullptr) {
   const int m = n_frames - 1;
   std::vector<double> rel(static_cast<size_t>(m) * 12);
   for (int k = 0; k < m; ++k) kreg_se3::identity(rel.data() + 12 * k);  // pairs outside the spans
@@ -155,6 +156,10 @@ void run_chains(kreg_ctx* ctx, const kreg_cloud* const* frames, int n_frames, co
       if (frame_ready) {  // end-to-end: the pair starts once both frames are on the device
         j.ready = &frame_ready[k - 1];
         j.ready2 = &frame_ready[k];
+        if (frame_done) {
+          j.ready_ev = frame_done[k - 1];
+          j.ready_ev2 = frame_done[k];
+        }
       }
       kreg_se3::identity(j.initial);
       j.params = params;
@@ -803,6 +808,7 @@ kreg_status kreg_register_batch_host(kreg_ctx* ctx, int32_t n, const kreg_cloud_
       make_jobs(up->clouds[2 * k].get(), up->clouds[2 * k + 1].get(), initials + 12 * k, params, config, &results[k],
                 jobs[k]);
       jobs[k].ready = &up->ready[static_cast<size_t>(k)];
+      jobs[k].ready_ev = up->done[static_cast<size_t>(k)];
     }
     try {
       register_many(ctx, jobs);
@@ -882,7 +888,8 @@ kreg_status kreg_register_sequence_host(kreg_ctx* ctx, const kreg_cloud_view* fr
     std::vector<const kreg_cloud*> fr;
     for (auto& c : up->clouds) fr.push_back(c.get());
     try {
-      run_chains(ctx, fr.data(), n_frames, b, e, to_params(params), *config, result, up->ready.data());
+      run_chains(ctx, fr.data(), n_frames, b, e, to_params(params), *config, result, up->ready.data(),
+                 up->done.data());
     } catch (...) {
       up.reset();  // join the workers before the clouds go away
       throw;

@@ -376,6 +376,8 @@ std::vector<std::unique_ptr<kreg_cloud>> cloud_create_many(kreg_ctx* ctx, const 
 AsyncUpload::~AsyncUpload() {
   for (auto& t : workers)
     if (t.joinable()) t.join();
+  for (cudaEvent_t e : done)
+    if (e) cudaEventDestroy(e);
 }
 
 std::unique_ptr<AsyncUpload> cloud_upload_async(kreg_ctx* ctx, const kreg_cloud_view* const* views, int n_jobs,
@@ -404,6 +406,8 @@ std::unique_ptr<AsyncUpload> cloud_upload_async(kreg_ctx* ctx, const kreg_cloud_
   ctx->arena_f.ensure(foff[n] + 4, false, 1.25);
   ctx->arena_w.ensure(woff[n] + 1, false, 1.25);
   up->ready = std::vector<std::atomic<int>>(static_cast<size_t>(n_jobs));
+  up->done.assign(static_cast<size_t>(n_jobs), nullptr);
+  for (auto& e : up->done) KREG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   for (auto& r : up->ready) r.store(0);
   const unsigned hw = std::max(2u, std::thread::hardware_concurrency());
   // staging threads (the solver thread keeps a core); KREG_STAGE_WORKERS overrides
@@ -430,6 +434,7 @@ std::unique_ptr<AsyncUpload> cloud_upload_async(kreg_ctx* ctx, const kreg_cloud_
           cloud_upload(ctx, c, d, d + m, d + 2 * m, ctx->stage_f.ptr + foff[k], a, a + m, a + 2 * m,
                        ctx->arena_f.ptr + foff[k], ctx->arena_w.ptr + woff[k]);
         }
+        KREG_CUDA(cudaEventRecord(U->done[static_cast<size_t>(job)], ctx->stream));
         U->ready[job].store(1, std::memory_order_release);
       } catch (...) {
         {
@@ -848,9 +853,10 @@ void begin_round(kreg_ctx* ctx, RoundSlot& S, std::vector<BuildJob>&& builds_in,
     builds[b].pairs->last_req.refilter = 0;
     builds[b].pairs->index_valid = false;
   }
-  if (S.own_stream) {  // after everything already issued on the context stream (cloud uploads)
-    KREG_CUDA(cudaEventRecord(S.ordered, ctx->stream));
-    KREG_CUDA(cudaStreamWaitEvent(S.stream, S.ordered, 0));
+  if (S.own_stream) {  // after the uploads of the clouds this round's first builds read
+    for (const BuildJob& bj : builds)
+      for (cudaEvent_t e : bj.wait_ev)
+        if (e) KREG_CUDA(cudaStreamWaitEvent(S.stream, e, 0));
   }
   // builds go to the device before the sweep requests are prepared
   if (nb) {

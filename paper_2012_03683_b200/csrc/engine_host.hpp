@@ -332,6 +332,7 @@ kreg_cloud* cloud_describe(kreg_ctx* ctx, const kreg_cloud_view* v);
 struct AsyncUpload {
   std::vector<std::unique_ptr<kreg_cloud>> clouds;
   std::vector<std::atomic<int>> ready;  // per job: 0 pending, 1 enqueued, -1 failed
+  std::vector<cudaEvent_t> done;        // per job: recorded on the context stream after its copies
   std::vector<std::thread> workers;
   std::mutex mu;
   std::exception_ptr error;
@@ -362,6 +363,9 @@ struct BuildJob {
   // unknown); lets the build reuse the resident candidate list
   double disp_hint = -1.0;
   bool force_full = false;
+  // end-to-end first builds: the uploads of X / Z (a round on a stream other
+  // than the context stream waits for these events, not for every upload)
+  cudaEvent_t wait_ev[2] = {nullptr, nullptr};
   bool no_refilter = false;  // filter the candidate list even if the sweep list covers the new one
 };
 

@@ -291,6 +291,10 @@ void schedule_build_eval(Reg& r, std::vector<BuildJob>& builds, std::vector<Eval
   // displacement of T from the current list's build transform (from the
   // sweep that evaluated T); lets the engine filter its candidate list
   b.disp_hint = r.phase == Phase::kInit ? -1.0 : r.ev[7];
+  if (r.phase == Phase::kInit) {  // the first build reads the uploaded clouds
+    b.wait_ev[0] = r.job->ready_ev;
+    b.wait_ev[1] = r.job->ready_ev2;
+  }
   builds.push_back(b);
   EvalJob e;
   e.pairs = r.pairs.get();

@@ -19,6 +19,8 @@ struct RegJob {
   long long n_z_total = 0;        // row sharding: size of the whole source (0: Z->n)
   const std::atomic<int>* ready = nullptr;  // end-to-end: clouds enqueued (1), failed (-1); null = ready
   const std::atomic<int>* ready2 = nullptr; // a second flag (sequences: X and Z are separate frames)
+  cudaEvent_t ready_ev = nullptr;           // end-to-end: recorded after the clouds' copies (ready / ready2)
+  cudaEvent_t ready_ev2 = nullptr;
   // sequence chains (register_sequence, registration.cpp:191-230): the job
   // starts when job `pred` has finished, from pred's relative motion (pred's
   // own initial guess when pred fell back on NoOverlapError); -1 = no link
