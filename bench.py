@@ -227,6 +227,8 @@ def run_other(args, world, rank, local):
     """The hand-run measurements (module docstring). Prints one JSON line."""
     from paper_2012_03683_b200 import api
     ctx = api.Context(local)
+    if args.chunk_units > 0:
+        ctx.set_chunk_units(args.chunk_units)
     params = synth.kitti_params()
     clocks = ClockSampler(local)
     if args.workload == "c5":
@@ -406,6 +408,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=25.0)
     ap.add_argument("--mode", default="throughput", choices=["throughput", "latency"])
+    ap.add_argument("--chunk-units", type=int, default=0,
+                    help="sweep chunk size of new pair lists (0 = engine default, 48; ~12 suits one registration at a time)")
     ap.add_argument("--workload", default="c3", choices=["c3", "first", "c5"])
     ap.add_argument("--frames", type=int, default=257, help="c5: frames in the sequence")
     ap.add_argument("--chains", type=int, default=16, help="c5: independent chains")
