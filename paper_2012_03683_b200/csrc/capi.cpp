@@ -767,11 +767,21 @@ kreg_status kreg_register_clouds_host(kreg_ctx* ctx, const kreg_cloud_view* X, c
                                       const kreg_registration_config* config, kreg_registration_result* result) {
   return guarded([&] {
     require(ctx && X && Z, "NULL argument");
-    std::unique_ptr<kreg_cloud> cx(cloud_create(ctx, X));
-    std::unique_ptr<kreg_cloud> cz(cloud_create(ctx, Z));
+    // staged on a worker thread into the context's upload arena (no device
+    // allocation per call once the arena holds a pair of this size)
+    const kreg_cloud_view* views[2] = {X, Z};
+    std::unique_ptr<AsyncUpload> up = cloud_upload_async(ctx, views, 1);
     std::vector<RegJob> jobs(1);
-    make_jobs(cx.get(), cz.get(), initial, params, config, result, jobs[0]);
-    register_many(ctx, jobs);
+    make_jobs(up->clouds[0].get(), up->clouds[1].get(), initial, params, config, result, jobs[0]);
+    jobs[0].ready = &up->ready[0];
+    jobs[0].ready_ev = up->done[0];
+    try {
+      register_many(ctx, jobs);
+    } catch (...) {
+      up.reset();  // join the worker before the clouds go away
+      throw;
+    }
+    up.reset();
     if (jobs[0].status != KREG_OK) throw Error(jobs[0].status, jobs[0].error);
   });
 }

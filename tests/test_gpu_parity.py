@@ -377,6 +377,19 @@ def test_host_buffer_batch_matches_device_batch(ctx):
             assert np.array_equal(ra.objective_trace, rb.objective_trace)
 
 
+def test_host_buffer_single_matches_device(ctx):
+    """register_clouds_host (one pair staged into the context's upload arena,
+    the CLI path) gives bitwise the result of register_clouds, call after call."""
+    X, Z, T = synth.kitti_pair(41, 6000)
+    init = synth.perturbed(T, 41)
+    p, cfg = synth.kitti_params(), synth.kitti_subsequent_config()
+    a = api.register_clouds(X, Z, init, p, cfg)
+    for _ in range(2):
+        b = api.register_clouds_host(X, Z, init, p, cfg)
+        assert np.array_equal(a.transform.as12(), b.transform.as12())
+        assert np.array_equal(a.objective_trace, b.objective_trace)
+
+
 def test_kitti_registration_end_to_end_vs_reference(ctx, ref):
     X, Z, Ts = synth.kitti_pair(7, 40000)
     p, cfg = synth.kitti_params(), synth.kitti_subsequent_config()
